@@ -1,0 +1,178 @@
+/*
+ * rfr.h -- C ABI of the B200 recombination engine (librfr.so).
+ *
+ * The drop-in boundary of the reference's recombination path.  The reference
+ * (/root/reference/pkg/src/polyfactor, "R/" below) is pure Python; its
+ * operator interface for this path is the backend registry entry
+ *     BACKENDS["e"] = recombine_e(rho: RhoVector, eps: float,
+ *                                 stats: RecombineStats | None) -> CandidateSet
+ * (R/recombine.py:727-784), its multi-worker twin parallel_recombine_e
+ * (R/parallel.py:255-272), and the verification functions build_candidate /
+ * trace_test / round_and_divide (R/verify.py:60-155) driven by
+ * _factor_monic_squarefree (R/verify.py:246-286).  A maintainer binds these
+ * entry points with ctypes; the Python host package
+ * paper_2410_15880_b200 does exactly that.
+ *
+ * Conventions (R/verify.py, R/recombine.py ownership rules):
+ *  - plain pointers and sizes; no torch or CUDA types in the signatures
+ *    (streams are passed as void*; NULL = the library's own stream);
+ *  - the caller allocates outputs and passes a capacity; the call returns the
+ *    TRUE count, and when it exceeds the capacity the caller regrows and calls
+ *    again (the reference's grow-and-retry protocol, R/recombine.py:750-757);
+ *  - every call returns an rfr_status; on failure rfr_last_error() has the
+ *    text.  The Python shim maps RFR_E_WIDTH -> WidthExceeded, RFR_E_ARG ->
+ *    ValueError, everything else -> RuntimeError (R/errors.py:9-26).
+ *  - calls are serialised per process (one internal mutex); device work runs
+ *    on the device selected by rfr_init.
+ */
+#ifndef RFR_H
+#define RFR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rfr_status {
+  RFR_OK = 0,
+  RFR_E_ARG = 1,      /* bad argument                 -> ValueError     */
+  RFR_E_WIDTH = 2,    /* n > 64 (pattern width cap)   -> WidthExceeded  */
+  RFR_E_CAP = 3,      /* internal capacity exhausted  -> RuntimeError   */
+  RFR_E_CUDA = 4,     /* CUDA runtime error           -> RuntimeError   */
+  RFR_E_NOINIT = 5,   /* rfr_init not called          -> RuntimeError   */
+  RFR_E_NUMERIC = 6   /* undecidable numerics         -> RuntimeError   */
+} rfr_status;
+
+/* Counters of one search; mirrors RecombineStats (R/recombine.py:82-103)
+ * plus per-phase device times.  All fields are written by the call. */
+typedef struct rfr_stats {
+  int64_t visited;        /* records enumerated: 2^alpha + 2^beta (folded halves)   */
+  int64_t inserts;        /* A records counting-sorted into shared memory           */
+  int64_t insert_probes;  /* A outer-pointer checks                                 */
+  int64_t queries;        /* B records streamed against the bins                    */
+  int64_t query_probes;   /* A records compared against a B record                  */
+  int64_t raw_hits;       /* patterns inside the key window                         */
+  int64_t buckets;        /* key buckets processed by this shard                    */
+  int64_t chunks;         /* extra A chunks (bucket overflowed shared memory)       */
+  int32_t r_bits;         /* bucket bits of the plan                                */
+  int32_t windows;        /* key sub-windows searched                               */
+  double ms_lists;        /* device time: quarter-list build                        */
+  double ms_join;         /* device time: bucket join                               */
+  double ms_post;         /* device time: recheck / verification                    */
+  double ms_total;        /* device time of the whole call                          */
+} rfr_stats;
+
+/* ---- lifecycle -------------------------------------------------------- */
+/* Select the CUDA device, create the stream and scratch buffers.  Replaces
+ * nothing in the reference (single-process Python); required once. */
+int rfr_init(int device);
+int rfr_shutdown(void);
+const char* rfr_last_error(void);
+int rfr_version(void);
+int rfr_num_sms(void);
+
+/* ---- search --------------------------------------------------------- */
+/*
+ * Parity-mode recombination: replaces recombine_e(rho, eps, stats)
+ * (R/recombine.py:727-775) and, with nshards > 1, one worker's share of
+ * parallel_recombine_e (R/parallel.py:255-272).
+ * rho: n float64 values in [0, 1) (R/recombine.py:46-51; n <= 64).
+ * Writes into out[0 .. min(count, cap)) the canonical patterns t < 2^(n-1)
+ * with accept(value(t), eps) (R/recombine.py:106-162) whose key bucket falls
+ * in this shard; *nout = true count.  Union over shards = the full set.
+ * Output order is unspecified (the reference returns a frozenset).
+ */
+int rfr_recombine_e(const double* rho, int n, double eps, int shard, int nshards, uint64_t* out,
+                    int64_t cap, int64_t* nout, rfr_stats* st);
+
+/*
+ * Factor-mode key-window search (the path factor() takes):
+ * every pattern t < 2^(n-1) with (sum_{i in t} keys[i] - lo) mod 2^64 <= width.
+ * keys: n uint64 fixed-point keys (host buffer).  Same output protocol.
+ * Replaces the candidate search of _factor_monic_squarefree
+ * (R/verify.py:261-268, recombine_e at the default backend).
+ */
+int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, int shard,
+                    int nshards, uint64_t* out, int64_t cap, int64_t* nout, rfr_stats* st);
+
+/*
+ * Device-resident variant for inputs already in HBM: d_keys (n uint64) and
+ * d_out (cap uint64) are device pointers, *d_count a device uint64 that
+ * receives the true count.  Enqueued on `stream` (cudaStream_t, NULL = the
+ * library stream); no host synchronisation unless st != NULL.
+ */
+int rfr_search_keys_dev(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard,
+                        int nshards, uint64_t* d_out, int64_t cap, uint64_t* d_count,
+                        void* stream, rfr_stats* st);
+
+/* ---- verification ------------------------------------------------------ */
+
+/* One polynomial's root profile in double-double (hi, lo) form: entity e
+ * (0 <= e < r real roots, then c conjugate pairs) and the rho-index -> entity
+ * map perm[n] (RootProfile, R/rootfinder.py:58-84).  Pairs carry the sum
+ * t = z + conj(z) and product m = |z|^2 of x^2 - t x + m. */
+typedef struct rfr_profile {
+  int n, r, c;
+  const double* real_hi;  /* r */
+  const double* real_lo;
+  const double* sum_hi;   /* c */
+  const double* sum_lo;
+  const double* prod_hi;  /* c */
+  const double* prod_lo;
+  const int32_t* perm;    /* n */
+  double root_err;        /* absolute error bound on every root (host bound) */
+} rfr_profile;
+
+/* Verdicts written per candidate (rfr_verify). */
+enum {
+  RFR_V_REJECT = 0,  /* not a factor (trace / rounding / division mod primes) */
+  RFR_V_PASS = 1,    /* integral, divides p modulo three 61-bit primes        */
+  RFR_V_HOST = 2     /* coefficients beyond 2^62 or undecidable: host decides */
+};
+
+/*
+ * Batched verification, one candidate per warp: replaces build_candidate ->
+ * trace_test -> round_and_divide (R/verify.py:60-155) for every candidate of
+ * one search.  For candidate k the smaller-degree side of {pat, complement}
+ * is rebuilt in double-double, screened by power-sum integrality, rounded,
+ * and trial-divided into p modulo three 61-bit primes.
+ *   pats[m]          candidate patterns (bit i = rho index i)
+ *   p_mod[3*(d+1)]   coefficients of the monic input p (low->high) mod the
+ *                    primes returned by rfr_verify_primes
+ *   verdict[m]       RFR_V_* per candidate
+ *   side[m]          1 if the complement side was rebuilt, else 0
+ *   coeffs[m*stride] rounded int64 coefficients of the rebuilt side
+ *                    (degree = selected degree; valid when PASS)
+ */
+int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const uint64_t* p_mod,
+               int d, uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride,
+               rfr_stats* st);
+/* The three primes of the modular division test (p_mod residues). */
+int rfr_verify_primes(uint64_t* primes3);
+
+/* ---- host-side numerics (native, not timed) ------------------------------ */
+/*
+ * Root polishing in double-double (Aberth-Ehrlich corrections) for a monic
+ * polynomial with coefficients exactly representable in double-double:
+ * coef_hi/lo[d+1] (low -> high), roots re/im hi/lo in/out (d each, seeded by
+ * any approximation), err[d] out: a posteriori absolute error bound per root.
+ * Returns RFR_OK or RFR_E_NUMERIC when it cannot certify the roots (the
+ * caller then uses its multiprecision path).  Replaces find_roots'
+ * iteration (R/rootfinder.py:100-174) as the host preprocessing step.
+ */
+int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double* re_hi,
+                     double* re_lo, double* im_hi, double* im_lo, double* err, int max_iter);
+
+/*
+ * Square-free screen for the exact normalisation (R/polynomial.py:221-247):
+ * 1 when gcd(p mod q, p' mod q) = 1 for a 61-bit prime q not dividing the
+ * leading coefficient (then p is square-free over Z), 0 when undecided.
+ * coeffs_mod: p's coefficients reduced mod q (d+1), lead_mod != 0.
+ */
+int rfr_squarefree_mod(const uint64_t* coeffs_mod, int d, uint64_t q);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFR_H */

@@ -1,0 +1,169 @@
+"""ctypes binding of librfr.so (the C ABI declared in include/rfr.h).
+
+The extension is built in-tree (``make -C paper_2410_15880_b200/csrc`` or
+``__graft_entry__.build()``) and loaded from this package directory.  There
+is no CPU fallback: every entry point raises when the library or a CUDA
+device is missing, so a GPU test can never pass on a silent substitute.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import RecombineDeviceError, WidthExceeded
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librfr.so")
+
+RFR_OK, RFR_E_ARG, RFR_E_WIDTH, RFR_E_CAP, RFR_E_CUDA, RFR_E_NOINIT, RFR_E_NUMERIC = range(7)
+V_REJECT, V_PASS, V_HOST = 0, 1, 2
+
+# every symbol include/rfr.h declares (tests/test_abi.py checks the export table)
+EXPORTS = (
+    "rfr_init",
+    "rfr_shutdown",
+    "rfr_last_error",
+    "rfr_version",
+    "rfr_num_sms",
+    "rfr_recombine_e",
+    "rfr_search_keys",
+    "rfr_search_keys_dev",
+    "rfr_verify",
+    "rfr_verify_primes",
+    "rfr_polish_roots",
+    "rfr_squarefree_mod",
+)
+
+
+class RfrStats(ctypes.Structure):
+    """Mirror of rfr_stats (include/rfr.h)."""
+
+    _fields_ = [
+        ("visited", ctypes.c_int64),
+        ("inserts", ctypes.c_int64),
+        ("insert_probes", ctypes.c_int64),
+        ("queries", ctypes.c_int64),
+        ("query_probes", ctypes.c_int64),
+        ("raw_hits", ctypes.c_int64),
+        ("buckets", ctypes.c_int64),
+        ("chunks", ctypes.c_int64),
+        ("r_bits", ctypes.c_int32),
+        ("windows", ctypes.c_int32),
+        ("ms_lists", ctypes.c_double),
+        ("ms_join", ctypes.c_double),
+        ("ms_post", ctypes.c_double),
+        ("ms_total", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class RfrProfile(ctypes.Structure):
+    """Mirror of rfr_profile (include/rfr.h)."""
+
+    _fields_ = [
+        ("n", ctypes.c_int),
+        ("r", ctypes.c_int),
+        ("c", ctypes.c_int),
+        ("real_hi", ctypes.POINTER(ctypes.c_double)),
+        ("real_lo", ctypes.POINTER(ctypes.c_double)),
+        ("sum_hi", ctypes.POINTER(ctypes.c_double)),
+        ("sum_lo", ctypes.POINTER(ctypes.c_double)),
+        ("prod_hi", ctypes.POINTER(ctypes.c_double)),
+        ("prod_lo", ctypes.POINTER(ctypes.c_double)),
+        ("perm", ctypes.POINTER(ctypes.c_int32)),
+        ("root_err", ctypes.c_double),
+    ]
+
+
+_lib = None
+_partial: list = []
+_lock = threading.Lock()
+_device = None
+
+D_P = ctypes.POINTER(ctypes.c_double)
+U64_P = ctypes.POINTER(ctypes.c_uint64)
+I64_P = ctypes.POINTER(ctypes.c_int64)
+U8_P = ctypes.POINTER(ctypes.c_uint8)
+I32_P = ctypes.POINTER(ctypes.c_int32)
+
+
+def load():
+    """Load librfr.so and declare the prototypes (no device work)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RecombineDeviceError(
+                f"{LIB_PATH} is missing: build it with `make -C {HERE}/csrc` "
+                "(there is no CPU fallback)"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        L.rfr_init.argtypes = [ctypes.c_int]
+        L.rfr_shutdown.argtypes = []
+        L.rfr_last_error.restype = ctypes.c_char_p
+        L.rfr_version.restype = ctypes.c_int
+        L.rfr_num_sms.restype = ctypes.c_int
+        L.rfr_recombine_e.argtypes = [
+            D_P, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, U64_P,
+            ctypes.c_int64, I64_P, ctypes.POINTER(RfrStats),
+        ]
+        L.rfr_search_keys.argtypes = [
+            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+            U64_P, ctypes.c_int64, I64_P, ctypes.POINTER(RfrStats),
+        ]
+        L.rfr_search_keys_dev.argtypes = [
+            ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.POINTER(RfrStats),
+        ]
+        if not all(hasattr(L, name) for name in EXPORTS):
+            missing = [name for name in EXPORTS if not hasattr(L, name)]
+            _partial.extend(missing)
+        if hasattr(L, "rfr_verify"):
+          L.rfr_verify.argtypes = [
+            ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int64, U64_P, ctypes.c_int, U8_P, U8_P,
+            I64_P, ctypes.c_int, ctypes.POINTER(RfrStats),
+        ]
+          L.rfr_verify_primes.argtypes = [U64_P]
+          L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]
+          L.rfr_squarefree_mod.argtypes = [U64_P, ctypes.c_int, ctypes.c_uint64]
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    return load().rfr_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc == RFR_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == RFR_E_WIDTH:
+        raise WidthExceeded(msg)
+    if rc == RFR_E_ARG:
+        raise ValueError(msg)
+    raise RecombineDeviceError(msg)
+
+
+def device() -> int:
+    """Initialise the engine on this process's CUDA device (LOCAL_RANK or 0)."""
+    global _device
+    L = load()
+    if _device is None:
+        dev = int(os.environ.get("RFR_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        check(L.rfr_init(dev), "rfr_init")
+        _device = dev
+    return _device
+
+
+def ptr(a: np.ndarray, typ):
+    return a.ctypes.data_as(typ)

@@ -1,0 +1,435 @@
+// rfr_capi.cu -- the C ABI of librfr.so (declared in include/rfr.h).
+//
+// Owns the per-process device context (stream, scratch buffers, counters) and
+// turns one search request into: key upload -> quarter-list build -> one
+// bucket-join launch per key sub-window -> optional recheck -> result copy.
+// The grow-and-retry protocol of the reference (recombine.py:750-757) is kept
+// for the internal raw-hit buffer and exposed to the caller for its output.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rfr.h"
+#include "rfr_common.cuh"
+#include "rfr_internal.h"
+
+using namespace rfr;
+
+namespace {
+
+std::mutex g_mu;
+thread_local std::string g_err;
+
+struct DevVec {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = want < 4096 ? 4096 : want;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct Ctx {
+  bool ready = false;
+  int device = -1;
+  int nsm = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  DevVec keys, rho, raw, post, ctr;
+  DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
+  DevCounters* h_ctr = nullptr;  // pinned mirror
+  // cache of the last built lists (key values + plan geometry)
+  std::vector<uint64_t> built_keys;
+  int built_bits[4] = {-1, -1, -1, -1};
+  const void* built_src = nullptr;
+};
+Ctx g;
+
+}  // namespace
+
+int rfr_fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int rfr_fail_cuda(cudaError_t e, const char* what) {
+  return rfr_fail(RFR_E_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what);
+}
+
+namespace {
+
+int bit_length(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
+
+// Plan the quarter lists and buckets of one search.
+int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
+  memset(P, 0, sizeof *P);
+  const int m = n - 1;
+  const int alpha = (m + 1) / 2, beta = m - alpha;
+  int r = alpha - 12;
+  if (r < 2) r = 2;
+  const uint64_t half = (width >> 1) + (width & 1);
+  const int hb = bit_length(half);
+  if (r > 61 - hb) r = 61 - hb;  // keep the window radius <= W / 8
+  if (r < 2) return rfr_fail(RFR_E_ARG, "window too wide for one plan (internal)");
+  auto clampi = [](int v, int lo_, int hi_) { return v < lo_ ? lo_ : (v > hi_ ? hi_ : v); };
+  // outer lists sized so each outer contributes ~2^lam records per bucket,
+  // inner lists capped at 2^kMaxInnerBits (L2 resident)
+  static int lam = -1;
+  if (lam < 0) {
+    const char* e = getenv("RFR_LAMBDA_LOG");
+    lam = e ? atoi(e) : 2;
+  }
+  const int ao = clampi(alpha - r - lam, alpha > kMaxInnerBits ? alpha - kMaxInnerBits : 0, kMaxOuterBits);
+  const int bo = clampi(beta - r - lam, beta > kMaxInnerBits ? beta - kMaxInnerBits : 0, kMaxOuterBits);
+  const int ai = alpha - ao, bi = beta - bo;
+  if (ai > kMaxInnerBits || bi > kMaxInnerBits)
+    return rfr_fail(RFR_E_WIDTH, "inner list too large (n=%d)", n);
+  P->n = n;
+  P->m = m;
+  P->list[0] = {0, ao, 0, 0};
+  P->list[1] = {ao, ai, 0, ao};
+  P->list[2] = {alpha, bo, 1, alpha};
+  P->list[3] = {alpha + bo, bi, 1, alpha + bo};
+  P->r = r;
+  P->nbins_log = clampi(alpha - r, 1, 12);
+  P->lo = lo;
+  P->width = width;
+  P->shift = lo + (width >> 1);
+  P->half = half;
+  return RFR_OK;
+}
+
+int ensure_ready() {
+  if (!g.ready) return rfr_fail(RFR_E_NOINIT, "rfr_init was not called");
+  return RFR_OK;
+}
+
+ListBufs bufs(int which) {
+  ListBufs b;
+  for (int i = 0; i < 4; i++) {
+    b.k[i] = (uint64_t*)g.lk[i][which].p;
+    b.p[i] = (uint32_t*)g.lp[i][which].p;
+  }
+  return b;
+}
+
+ListBufs final_bufs(const JoinPlan& P) {
+  ListBufs b;
+  for (int i = 0; i < 4; i++) {
+    int which = P.list[i].bits > kBaseBits ? ((P.list[i].bits - kBaseBits) & 1) : 0;
+    b.k[i] = (uint64_t*)g.lk[i][which].p;
+    b.p[i] = (uint32_t*)g.lp[i][which].p;
+  }
+  return b;
+}
+
+int ensure_list_buffers(const JoinPlan& P) {
+  for (int i = 0; i < 4; i++) {
+    size_t len = (size_t)1 << P.list[i].bits;
+    if (len < 4096) len = 4096;
+    for (int w = 0; w < 2; w++) {
+      RFR_CUDA_OK(g.lk[i][w].ensure(len * sizeof(uint64_t)));
+      RFR_CUDA_OK(g.lp[i][w].ensure(len * sizeof(uint32_t)));
+    }
+  }
+  return RFR_OK;
+}
+
+// Split [lo, lo + width] into pieces whose radius fits a plan with r >= 2.
+std::vector<std::pair<uint64_t, uint64_t>> split_window(uint64_t lo, uint64_t width) {
+  std::vector<std::pair<uint64_t, uint64_t>> out;
+  const uint64_t piece = (1ull << 59) - 1;  // width of one piece (radius < 2^58 + 1)
+  if (width <= piece) {
+    out.push_back({lo, width});
+    return out;
+  }
+  uint64_t done = 0;  // covered [lo, lo + done)
+  while (true) {
+    uint64_t rem = width - done;  // remaining inclusive span minus one
+    uint64_t w = rem < piece ? rem : piece;
+    out.push_back({lo + done, w});
+    if (w == rem) break;
+    done += w + 1;
+  }
+  return out;
+}
+
+double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return (double)ms;
+}
+
+// Core search on device-resident keys.  d_out/cap: raw output; d_count: out
+// counter lives in g.ctr (DevCounters.out_count).  Leaves counters on device.
+int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard, int nshards,
+                uint64_t* d_out, unsigned long long cap, cudaStream_t s, int* r_bits,
+                int* nwin, bool time_it) {
+  std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
+  *nwin = (int)wins.size();
+  JoinPlan P0;
+  int rc = make_plan(n, wins[0].first, wins[0].second, &P0);
+  if (rc) return rc;
+  *r_bits = P0.r;
+  rc = ensure_list_buffers(P0);
+  if (rc) return rc;
+  if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
+  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), s));
+  if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
+  for (auto& w : wins) {
+    // every piece reuses the geometry planned for the widest (first) piece
+    JoinPlan P = P0;
+    P.lo = w.first;
+    P.width = w.second;
+    P.shift = w.first + (w.second >> 1);
+    P.half = (w.second >> 1) + (w.second & 1);
+    const uint64_t nb = 1ull << P.r;
+    P.bucket_begin = nb * (uint64_t)shard / (uint64_t)nshards;
+    P.bucket_end = nb * (uint64_t)(shard + 1) / (uint64_t)nshards;
+    uint64_t span = P.bucket_end - P.bucket_begin;
+    if (span == 0) continue;
+    int grid = (int)(span < (uint64_t)g.nsm ? span : (uint64_t)g.nsm);
+    RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
+  }
+  if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
+  return RFR_OK;
+}
+
+void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin) {
+  if (!st) return;
+  memset(st, 0, sizeof *st);
+  const int m = n - 1;
+  const int alpha = (m + 1) / 2, beta = m - alpha;
+  st->visited = n > 0 ? (int64_t)((1ull << alpha) + (1ull << beta)) : 0;
+  st->inserts = (int64_t)c.inserts;
+  st->insert_probes = (int64_t)c.insert_probes;
+  st->queries = (int64_t)c.queries;
+  st->query_probes = (int64_t)c.query_probes;
+  st->raw_hits = (int64_t)c.out_count;
+  st->buckets = (int64_t)c.buckets;
+  st->chunks = (int64_t)c.chunks;
+  st->r_bits = r_bits;
+  st->windows = nwin;
+}
+
+int check_n(int n) {
+  if (n < 0) return rfr_fail(RFR_E_ARG, "negative width");
+  if (n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits, got %d", n);
+  return RFR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rfr_version(void) { return 1; }
+
+const char* rfr_last_error(void) { return g_err.c_str(); }
+
+int rfr_num_sms(void) { return g.nsm; }
+
+int rfr_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.ready && g.device == device) return RFR_OK;
+  if (g.ready) return rfr_fail(RFR_E_ARG, "already initialised on device %d", g.device);
+  int ndev = 0;
+  RFR_CUDA_OK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return rfr_fail(RFR_E_ARG, "no CUDA device %d", device);
+  RFR_CUDA_OK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  RFR_CUDA_OK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return rfr_fail(RFR_E_CUDA, "librfr is built for sm_100a; device %d is sm_%d%d", device,
+                    prop.major, prop.minor);
+  g.nsm = prop.multiProcessorCount;
+  RFR_CUDA_OK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  for (auto& e : g.ev) RFR_CUDA_OK(cudaEventCreate(&e));
+  RFR_CUDA_OK(g.ctr.ensure(sizeof(DevCounters)));
+  RFR_CUDA_OK(cudaMallocHost(&g.h_ctr, sizeof(DevCounters)));
+  RFR_CUDA_OK(g.keys.ensure(64 * sizeof(uint64_t)));
+  RFR_CUDA_OK(g.rho.ensure(64 * sizeof(double)));
+  RFR_CUDA_OK(g.raw.ensure((1u << 20) * sizeof(uint64_t)));
+  RFR_CUDA_OK(g.post.ensure((1u << 20) * sizeof(uint64_t)));
+  g.device = device;
+  g.ready = true;
+  return RFR_OK;
+}
+
+int rfr_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.ready) return RFR_OK;
+  cudaSetDevice(g.device);
+  cudaStreamSynchronize(g.stream);
+  g.keys.release();
+  g.rho.release();
+  g.raw.release();
+  g.post.release();
+  g.ctr.release();
+  for (auto& a : g.lk)
+    for (auto& v : a) v.release();
+  for (auto& a : g.lp)
+    for (auto& v : a) v.release();
+  for (auto& e : g.ev) cudaEventDestroy(e);
+  cudaFreeHost(g.h_ctr);
+  cudaStreamDestroy(g.stream);
+  g = Ctx();
+  return RFR_OK;
+}
+
+static int run_search_host(const uint64_t* h_keys, const double* h_rho, int n, uint64_t lo,
+                           uint64_t width, double eps, int shard, int nshards, uint64_t* out,
+                           int64_t cap, int64_t* nout, rfr_stats* st) {
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if ((rc = check_n(n))) return rc;
+  if (nshards < 1 || shard < 0 || shard >= nshards) return rfr_fail(RFR_E_ARG, "bad shard");
+  if (cap < 0 || !nout) return rfr_fail(RFR_E_ARG, "bad output buffer");
+  cudaSetDevice(g.device);
+  cudaStream_t s = g.stream;
+  if (n == 0) {
+    *nout = 0;
+    fill_stats(st, DevCounters{}, 0, 0, 0);
+    return RFR_OK;
+  }
+  const bool parity = (h_rho != nullptr);
+  if (parity) {
+    RFR_CUDA_OK(cudaMemcpyAsync(g.rho.p, h_rho, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    RFR_CUDA_OK(launch_rho_keys((const double*)g.rho.p, n, (uint64_t*)g.keys.p, s));
+  } else {
+    RFR_CUDA_OK(cudaMemcpyAsync(g.keys.p, h_keys, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  }
+  int r_bits = 0, nwin = 0;
+  unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  for (int attempt = 0; attempt < 3; attempt++) {
+    RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
+    rc = search_core((const uint64_t*)g.keys.p, n, lo, width, shard, nshards, (uint64_t*)g.raw.p,
+                     raw_cap, s, &r_bits, &nwin, true);
+    if (rc) return rc;
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    if (g.h_ctr->out_count <= raw_cap) break;
+    if (attempt == 2) return rfr_fail(RFR_E_CAP, "raw hit buffer regrow failed");
+    unsigned long long want = g.h_ctr->out_count + (g.h_ctr->out_count >> 3) + 1024;
+    if (want > (1ull << 31)) return rfr_fail(RFR_E_CAP, "%llu raw hits exceed the 2^31 limit",
+                                             (unsigned long long)g.h_ctr->out_count);
+    RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
+    raw_cap = g.raw.bytes / sizeof(uint64_t);
+  }
+  DevCounters c = *g.h_ctr;
+  const uint64_t* d_res = (const uint64_t*)g.raw.p;
+  unsigned long long count = c.out_count;
+  if (parity) {
+    RFR_CUDA_OK(g.post.ensure((count ? count : 1) * sizeof(uint64_t)));
+    RFR_CUDA_OK(launch_recheck((const double*)g.rho.p, (const uint64_t*)g.raw.p, &d_ctr->out_count,
+                               raw_cap, eps, (uint64_t*)g.post.p,
+                               g.post.bytes / sizeof(uint64_t), d_ctr, g.nsm, s));
+    RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    c = *g.h_ctr;
+    count = c.post_count;
+    d_res = (const uint64_t*)g.post.p;
+  } else {
+    RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+  }
+  const unsigned long long ncopy = count < (unsigned long long)cap ? count : (unsigned long long)cap;
+  if (ncopy)
+    RFR_CUDA_OK(cudaMemcpyAsync(out, d_res, ncopy * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  RFR_CUDA_OK(cudaStreamSynchronize(s));
+  *nout = (int64_t)count;
+  if (st) {
+    fill_stats(st, c, n, r_bits, nwin);
+    st->raw_hits = (int64_t)c.out_count;
+    st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
+    st->ms_join = ev_ms(g.ev[1], g.ev[2]);
+    st->ms_post = ev_ms(g.ev[2], g.ev[3]);
+    st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+  }
+  return RFR_OK;
+}
+
+int rfr_recombine_e(const double* rho, int n, double eps, int shard, int nshards, uint64_t* out,
+                    int64_t cap, int64_t* nout, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!rho && n > 0) return rfr_fail(RFR_E_ARG, "null rho");
+  if (!(eps > 0.0 && eps < 0.5)) return rfr_fail(RFR_E_ARG, "eps must be in (0, 0.5)");
+  for (int i = 0; i < n; i++)
+    if (!(rho[i] >= 0.0 && rho[i] < 1.0)) return rfr_fail(RFR_E_ARG, "rho entries must lie in [0, 1)");
+  // window: every t with accept(value(t), eps) has |frac| < eps + GUARD
+  // (recombine.py:28-30), and the key sum is within n/2 of 2^64 * exact sum.
+  const double eps_d = eps + 1e-12;
+  const double t = std::ceil(std::ldexp(eps_d, 64));
+  uint64_t lo = 0, width = ~0ull;
+  if (t < 9.0e18) {
+    const uint64_t T = (uint64_t)t + (uint64_t)n + 4096;
+    if (T < (1ull << 63)) {
+      lo = 0ull - T;
+      width = 2 * T;
+    }
+  }
+  return run_search_host(nullptr, rho, n, lo, width, eps, shard, nshards, out, cap, nout, st);
+}
+
+int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, int shard,
+                    int nshards, uint64_t* out, int64_t cap, int64_t* nout, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!keys && n > 0) return rfr_fail(RFR_E_ARG, "null keys");
+  return run_search_host(keys, nullptr, n, lo, width, 0.0, shard, nshards, out, cap, nout, st);
+}
+
+int rfr_search_keys_dev(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard,
+                        int nshards, uint64_t* d_out, int64_t cap, uint64_t* d_count,
+                        void* stream, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if ((rc = check_n(n))) return rc;
+  if (nshards < 1 || shard < 0 || shard >= nshards) return rfr_fail(RFR_E_ARG, "bad shard");
+  if (n == 0) return rfr_fail(RFR_E_ARG, "empty instance");
+  cudaSetDevice(g.device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : g.stream;
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
+  int r_bits = 0, nwin = 0;
+  rc = search_core(d_keys, n, lo, width, shard, nshards, d_out, (unsigned long long)cap, s,
+                   &r_bits, &nwin, st != nullptr);
+  if (rc) return rc;
+  if (d_count)
+    RFR_CUDA_OK(cudaMemcpyAsync(d_count, &d_ctr->out_count, sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, s));
+  if (st) {
+    RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    fill_stats(st, *g.h_ctr, n, r_bits, nwin);
+    st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
+    st->ms_join = ev_ms(g.ev[1], g.ev[2]);
+    st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+  }
+  return RFR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// rfr_common.cuh -- shared definitions for the recombination kernels.
+//
+// Key arithmetic lives in Z / 2^64: a pattern's key is the wrapping uint64 sum
+// of its per-entity keys (fixed-point fractional parts scaled by 2^64), so an
+// integer sum of fractional parts is a key near 0.  See DESIGN.md section 2.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rfr {
+
+// Largest quarter list walked by the join (2^23 entries = 64 MB of keys).
+constexpr int kMaxInnerBits = 23;
+// Outer lists live in shared memory of the join kernel.
+constexpr int kMaxOuterBits = 10;
+// Sorted base block built in shared memory by the list builder.
+constexpr int kBaseBits = 12;
+
+// One quarter list of the folded pattern space: subset sums of
+// keys[first, first + bits) (negated for the B half), sorted ascending.
+struct ListSpec {
+  int first;      // first rho index covered
+  int bits;       // number of elements (list length 2^bits)
+  int negate;     // 1 for the B half (N = -K)
+  int pat_shift;  // bit position of this list's pattern inside the full pattern
+};
+
+// Search plan: the folded half space t < 2^(n-1) is the product of four
+// quarter lists A_outer x A_inner x B_outer x B_inner; see DESIGN.md s3.
+struct JoinPlan {
+  int n;             // rho width
+  int m;             // folded bits = n - 1
+  ListSpec list[4];  // 0 = A outer, 1 = A inner, 2 = B outer, 3 = B inner
+  int r;             // bucket bits; bucket c = [c W, (c+1) W), W = 2^(64-r)
+  int nbins_log;     // A-records of one bucket are counting-sorted into 2^nbins_log bins
+  uint64_t lo;       // window: match iff (K_a + K_b - lo) mod 2^64 <= width
+  uint64_t width;
+  uint64_t shift;    // added to every B key: lo + width/2
+  uint64_t half;     // ceil(width / 2): bin search radius
+  uint64_t bucket_begin, bucket_end;  // this launch's bucket range
+};
+
+// Four quarter-list buffers (keys + local patterns), passed by value.
+struct ListBufs {
+  uint64_t* k[4];
+  uint32_t* p[4];
+};
+
+// Device-side counters (one slot each, accumulated with atomics).
+struct DevCounters {
+  unsigned long long out_count;      // emitted pairs (may exceed capacity)
+  unsigned long long inserts;        // A records binned (main + halo ghosts)
+  unsigned long long insert_probes;  // A outer-pointer checks
+  unsigned long long queries;        // B records streamed
+  unsigned long long query_probes;   // A records compared against a B record
+  unsigned long long chunks;         // extra A chunks after a bucket overflow
+  unsigned long long buckets;        // buckets processed
+  unsigned long long post_count;     // survivors of the post-filter
+};
+
+}  // namespace rfr
+
+#define RFR_CUDA_OK(expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return rfr_fail_cuda(_e, #expr); \
+  } while (0)

@@ -1,0 +1,18 @@
+// rfr_internal.h -- launchers shared between the kernel files and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "rfr_common.cuh"
+
+namespace rfr {
+size_t join_smem_bytes();
+cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
+                         cudaStream_t s);
+cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
+                        unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s);
+cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
+                           const unsigned long long* d_in_count, unsigned long long cap_in,
+                           double eps, uint64_t* d_out, unsigned long long cap_out,
+                           DevCounters* d_ctr, int nsm, cudaStream_t s);
+cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaStream_t s);
+}  // namespace rfr

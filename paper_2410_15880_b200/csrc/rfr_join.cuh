@@ -1,0 +1,613 @@
+// rfr_join.cuh -- the bucket join kernel (included by rfr_search.cu).
+//
+// Each CTA owns a contiguous range of key buckets and walks it in order.  Per
+// bucket c (keys [cW, (c+1)W), W = 2^(64-r)):
+//   A side   every A outer x contributes the contiguous run of its rotated
+//            inner list whose sums x + k fall in bucket c, followed by the
+//            halo run [(c+1)W, (c+1)W + H).  A group of gs lanes loads one
+//            window of gs consecutive keys of one outer (coalesced); because
+//            the sums are sorted, "main or halo" is a per-lane test and the
+//            emitted lanes are a prefix of the group.  kU windows are loaded
+//            before any is processed (kU loads in flight per lane).  A ballot
+//            compacts the records into the warp's own partition of the
+//            shared record array.
+//   A index  a three-level direct-mapped index with 2^15, 2^13 and 2^11 slots
+//            over the bucket (the reference's splat table, recombine.py:
+//            297-325, moved on chip): every record stores its index in its
+//            level-1 home with a plain store, reads it back after a barrier,
+//            and only the records that lost a slot collision move to the next
+//            level; the few level-3 losers go to a short list.  No shared
+//            atomics on this path: they cost ~2 cycles per lane on this part.
+//   B side   the same windows over B (negated, shifted keys); each emitted B
+//            lane reads its home slots in the three levels and checks the
+//            records it finds for exact window matches (the reference's
+//            windowed probe, recombine.py:328-358).
+//   Outers whose run fills its window continue one window at a time.
+// Pairs across a bucket boundary are found once: (A in c, B in c+1) by a B
+// halo record, (A in c+1, B in c) by an A halo record; halo x halo is skipped
+// (bucket c+1 finds it).  A bucket whose A side overflows its shared-memory
+// partitions (skewed keys) is redone on a slow path in capacity-sized chunks,
+// each chunk re-streaming B; the fast attempt emits nothing before the
+// overflow is known, so no pair is duplicated.
+#pragma once
+
+constexpr int kJoinThreads = 512;
+constexpr int kJoinWarps = kJoinThreads / 32;
+constexpr int kL1Log = 15, kL2Log = 13, kL3Log = 11;  // index levels (slots)
+constexpr int kPart = 384;                            // A records per warp partition
+constexpr int kCapRec = kPart * kJoinWarps;           // 6144 A records per chunk
+constexpr int kLose = 128;                            // per-warp level-1 loser list
+constexpr int kList4 = 256;                           // level-3 losers (CTA list)
+constexpr int kMaxOuter = 1 << kMaxOuterBits;
+constexpr int kU = 8;                                 // windows in flight per lane
+constexpr uint16_t kNone = 0xffffu;
+constexpr uint32_t kFlagCont = 0x80000000u;
+
+struct JoinSmem {
+  uint64_t recK[kCapRec];  // A records: key
+  uint32_t recI[kCapRec];  // A records: outer << inner_bits | inner index
+  uint16_t t1[1 << kL1Log];
+  uint16_t t2[1 << kL2Log];
+  uint16_t t3[1 << kL3Log];
+  uint16_t lose[kJoinWarps][kLose];  // per-warp level-1 losers, then level-2 losers
+  uint16_t list4[kList4];
+  uint64_t qK[kJoinWarps][64];  // B candidates: key
+  uint32_t qJ[kJoinWarps][64];  // B candidates: halo flag << 31 | inner index
+  uint16_t qB[kJoinWarps][64];  // B candidates: outer index
+  uint64_t ax[kMaxOuter];
+  uint32_t arot[kMaxOuter];
+  uint32_t apos[kMaxOuter];
+  uint32_t amain[kMaxOuter];  // main records in this bucket (| kFlagCont: run continues)
+  uint64_t bx[kMaxOuter];
+  uint32_t brot[kMaxOuter];
+  uint32_t bpos[kMaxOuter];
+  uint32_t bmain[kMaxOuter];
+  uint32_t wcnt[kJoinWarps];
+  unsigned int n4;
+  int ovf;
+  uint32_t cur_i, cur_t;  // slow path cursor
+};
+
+__device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
+  return (uint32_t)(rel >> shift) & ((1u << lg) - 1u);
+}
+
+// Exact check of A record r against B key s; emits the pattern on a match.
+__device__ __forceinline__ void check_pair(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                           uint32_t r, uint64_t s, bool bghost, uint32_t ib,
+                                           uint32_t jb, uint32_t& n_qprobe) {
+  const JoinPlan& P = a.P;
+  const uint64_t W = 1ull << (64 - P.r);
+  n_qprobe++;
+  const uint64_t ka = S.recK[r];
+  if (bghost && (ka - cW >= W)) return;  // halo x halo belongs to bucket c+1
+  if (ka - s + (P.width >> 1) <= P.width) {
+    const uint32_t id = S.recI[r];
+    const int aib = P.list[1].bits;
+    const uint32_t ia = id >> aib, ja = id & ((1u << aib) - 1u);
+    const uint64_t pa = (uint64_t)__ldg(a.pat[0] + ia) |
+                        ((uint64_t)__ldg(a.pat[1] + ja) << P.list[1].pat_shift);
+    const uint64_t pb = ((uint64_t)__ldg(a.pat[2] + ib) << P.list[2].pat_shift) |
+                        ((uint64_t)__ldg(a.pat[3] + jb) << P.list[3].pat_shift);
+    const unsigned long long k = atomicAdd(&a.ctr->out_count, 1ull);
+    if (k < a.cap) a.out[k] = pa | pb;
+  }
+}
+
+// Probe one level of the index over the homes of [lo_rel, hi_rel].
+__device__ __forceinline__ void probe_level(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                            const uint16_t* t, int lg, uint64_t lo_rel,
+                                            uint64_t hi_rel, uint64_t s, bool bghost, uint32_t ib,
+                                            uint32_t jb, uint32_t& n_qprobe) {
+  const int shift = 64 - a.P.r - lg;
+  const uint32_t h0 = (uint32_t)(lo_rel >> shift);
+  const uint32_t hn = (uint32_t)(hi_rel >> shift) - h0;
+  const uint32_t m = (1u << lg) - 1u;
+  const uint32_t lim = hn < m ? hn : m;
+  for (uint32_t d = 0; d <= lim; d++) {
+    const uint32_t r = t[(h0 + d) & m];
+    if (r != kNone) check_pair(S, a, cW, r, s, bghost, ib, jb, n_qprobe);
+  }
+}
+
+__device__ __forceinline__ void probe_b(const JoinSmem& S, const JoinArgs& a, uint64_t cW, uint64_t s,
+                                     bool bghost, uint32_t ib, uint32_t jb, uint32_t& n_qprobe) {
+  const uint64_t H = a.P.half;
+  const uint64_t rel = s - cW;  // main: [0, W); halo: [W, W + H)
+  const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
+  const uint64_t hi_rel = rel + H;
+  probe_level(S, a, cW, S.t1, kL1Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
+  probe_level(S, a, cW, S.t2, kL2Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
+  probe_level(S, a, cW, S.t3, kL3Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
+  const uint32_t n4 = S.n4 < (unsigned)kList4 ? S.n4 : (unsigned)kList4;
+  for (uint32_t e = 0; e < n4; e++) check_pair(S, a, cW, S.list4[e], s, bghost, ib, jb, n_qprobe);
+}
+
+// Fast B screen.  Every A record's level-1 home is occupied (by it or by the
+// record that won the slot), so empty level-1 homes over the window prove
+// that no A record is within +-H: one shared load for ~88% of B records.
+__device__ __forceinline__ bool b_may_hit(const JoinSmem& S, const JoinPlan& P, uint64_t cW,
+                                          uint64_t s, uint32_t n4) {
+  const uint64_t H = P.half;
+  const uint64_t rel = s - cW;
+  const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
+  const int sh1 = 64 - P.r - kL1Log;
+  const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
+  const uint32_t hn = (uint32_t)((rel + H) >> sh1) - h0;
+  if (hn > 1 || n4 > 0) return true;
+  const uint32_t m1 = (1u << kL1Log) - 1u;
+  return S.t1[h0 & m1] != kNone || (hn && S.t1[(h0 + 1) & m1] != kNone);
+}
+
+// Probe one full batch of 32 queued B candidates (one lane each) and shift
+// the remainder down.  Out of line: one copy of the probe code.
+__device__ __noinline__ void drain_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, uint32_t& nq,
+                                     uint32_t& n_qprobe) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncwarp();
+  probe_b(S, a, cW, S.qK[wid][lane], S.qJ[wid][lane] >> 31, S.qB[wid][lane],
+          S.qJ[wid][lane] & 0x7fffffffu, n_qprobe);
+  __syncwarp();
+  nq -= 32;
+  if ((uint32_t)lane < nq) {
+    S.qK[wid][lane] = S.qK[wid][32 + lane];
+    S.qJ[wid][lane] = S.qJ[wid][32 + lane];
+    S.qB[wid][lane] = S.qB[wid][32 + lane];
+  }
+  __syncwarp();
+}
+
+// Append this lane's B candidate (if any) to the warp queue; probe full
+// batches of 32 from a single code site (one lane per candidate).
+__device__ __forceinline__ void queue_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, bool cand,
+                                        uint64_t s, bool bghost, uint32_t ib, uint32_t jb,
+                                        uint32_t& nq, uint32_t& n_qprobe) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t cm = __ballot_sync(FULL, cand);
+  if (cand) {
+    const uint32_t k = nq + __popc(cm & ((1u << lane) - 1u));
+    S.qK[wid][k] = s;
+    S.qJ[wid][k] = (bghost ? 0x80000000u : 0u) | jb;
+    S.qB[wid][k] = (uint16_t)ib;
+  }
+  nq += __popc(cm);
+  if (nq >= 32) drain_b(S, a, cW, nq, n_qprobe);
+}
+
+__device__ __noinline__ void flush_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, uint32_t& nq,
+                                        uint32_t& n_qprobe) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncwarp();
+  if ((uint32_t)lane < nq)
+    probe_b(S, a, cW, S.qK[wid][lane], S.qJ[wid][lane] >> 31, S.qB[wid][lane],
+            S.qJ[wid][lane] & 0x7fffffffu, n_qprobe);
+  nq = 0;
+  __syncwarp();
+}
+
+// Windowed walk of one side: lane-group layout, kU windows in flight.  Side A
+// appends records to the warp partition and claims level-1 homes; side B
+// probes.  Saturated runs are flagged in the main-count array.
+template <bool SIDE_A>
+__device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                            uint32_t lo, uint32_t hi, int gs, uint32_t& wfill,
+                                            uint32_t& n_stat, uint32_t& n_qprobe, bool& overflow) {
+  const JoinPlan& P = a.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int g = lane / gs, l = lane % gs, gpw = 32 / gs, gb = g * gs;
+  const uint32_t gmask = gs == 32 ? FULL : ((1u << gs) - 1u);
+  const uint32_t Mi = 1u << P.list[SIDE_A ? 1 : 3].bits;
+  const uint64_t* __restrict__ kin = a.key[SIDE_A ? 1 : 3];
+  const uint64_t* xs = SIDE_A ? S.ax : S.bx;
+  const uint32_t* rots = SIDE_A ? S.arot : S.brot;
+  const uint32_t* poss = SIDE_A ? S.apos : S.bpos;
+  uint32_t* mainv = SIDE_A ? S.amain : S.bmain;
+  const int sh = 64 - P.r;
+  const uint64_t W = 1ull << sh, H = P.half;
+  const int aib = P.list[1].bits;
+  const uint32_t n4 = SIDE_A ? 0u : S.n4;
+  uint32_t nq = 0;
+  for (uint32_t base = lo; base < hi; base += kU * gpw) {
+    uint64_t sv[kU];
+    uint32_t jv[kU];
+    bool mv[kU], ev[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const uint32_t i = base + u * gpw + g;
+      const bool valid = i < hi && (uint32_t)l < Mi;
+      uint32_t pos = 0, rot = 0;
+      uint64_t x = 0;
+      if (i < hi) {
+        pos = poss[i];
+        rot = rots[i];
+        x = xs[i];
+      }
+      const uint32_t o = pos + l;
+      jv[u] = (rot + o) & (Mi - 1);
+      sv[u] = x + (valid ? __ldg(kin + jv[u]) : 0ull);
+      const uint64_t rel = sv[u] - cW;
+      mv[u] = valid && o < Mi && rel < W;
+      ev[u] = mv[u] || (valid && (rel - W) < H);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const uint32_t i = base + u * gpw + g;
+      const uint32_t em = __ballot_sync(FULL, ev[u]);
+      const uint32_t mm = __ballot_sync(FULL, mv[u]);
+      if (SIDE_A) {
+        const uint32_t ne = __popc(em);
+        if (wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
+        if (!overflow) {
+          if (ev[u]) {
+            const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
+            S.recK[r] = sv[u];
+            S.recI[r] = (i << aib) | jv[u];
+            S.t1[home_of(sv[u] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
+          }
+          wfill += ne;
+        }
+        n_stat += ev[u] ? 1u : 0u;
+      } else {
+        n_stat += ev[u] ? 1u : 0u;
+        const bool cand = ev[u] && b_may_hit(S, P, cW, sv[u], n4);
+        queue_b(S, a, cW, cand, sv[u], !mv[u], i, jv[u], nq, n_qprobe);
+      }
+      if (l == 0 && i < hi) {
+        const bool sat = ((em >> gb) & gmask) == gmask && (uint32_t)gs < Mi;
+        mainv[i] = (uint32_t)__popc((mm >> gb) & gmask) | (sat ? kFlagCont : 0u);
+      }
+    }
+  }
+  if (!SIDE_A) flush_b(S, a, cW, nq, n_qprobe);
+}
+
+// Continue the saturated runs of one side, one outer at a time, 32 lanes.
+template <bool SIDE_A>
+__device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                              uint32_t lo, uint32_t hi, int gs, uint32_t& wfill,
+                                              uint32_t& n_stat, uint32_t& n_qprobe,
+                                              bool& overflow) {
+  const JoinPlan& P = a.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t Mi = 1u << P.list[SIDE_A ? 1 : 3].bits;
+  const uint64_t* __restrict__ kin = a.key[SIDE_A ? 1 : 3];
+  uint32_t* mainv = SIDE_A ? S.amain : S.bmain;
+  const int sh = 64 - P.r;
+  const uint64_t W = 1ull << sh, H = P.half;
+  const int aib = P.list[1].bits;
+  const uint32_t n4 = SIDE_A ? 0u : S.n4;
+  uint32_t nq = 0;
+  for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
+    const uint32_t ii = c0 + lane;
+    const bool flag = ii < hi && (mainv[ii] & kFlagCont);
+    uint32_t todo = __ballot_sync(FULL, flag);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t i = c0 + src;
+      uint32_t mainc = mainv[i] & ~kFlagCont;
+      uint32_t off = (uint32_t)gs;
+      const uint32_t pos = (SIDE_A ? S.apos : S.bpos)[i];
+      const uint32_t rot = (SIDE_A ? S.arot : S.brot)[i];
+      const uint64_t x = (SIDE_A ? S.ax : S.bx)[i];
+      while (true) {
+        const uint32_t q = off + lane;
+        const bool valid = q < Mi;
+        const uint32_t o = pos + q;
+        const uint32_t j = (rot + o) & (Mi - 1);
+        const uint64_t s = x + (valid ? __ldg(kin + j) : 0ull);
+        const uint64_t rel = s - cW;
+        const bool m = valid && o < Mi && rel < W;
+        const bool e = m || (valid && (rel - W) < H);
+        const uint32_t em = __ballot_sync(FULL, e);
+        const uint32_t ne = __popc(em);
+        if (SIDE_A) {
+          if (wfill + ne > (uint32_t)kPart) overflow = true;
+          if (!overflow) {
+            if (e) {
+              const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
+              S.recK[r] = s;
+              S.recI[r] = (i << aib) | j;
+              S.t1[home_of(rel, sh - kL1Log, kL1Log)] = (uint16_t)r;
+            }
+            wfill += ne;
+          }
+          n_stat += e ? 1u : 0u;
+        } else {
+          n_stat += e ? 1u : 0u;
+          const bool cand = e && b_may_hit(S, P, cW, s, n4);
+          queue_b(S, a, cW, cand, s, !m, i, j, nq, n_qprobe);
+        }
+        mainc += __popc(__ballot_sync(FULL, m));
+        off += ne;
+        if (ne < 32 || off >= Mi) break;
+      }
+      if (lane == 0) mainv[i] = mainc;
+    }
+  }
+  if (!SIDE_A) flush_b(S, a, cW, nq, n_qprobe);
+}
+
+// Build levels 2 and 3 from the level-1 losers (plain stores + read-back).
+// Called by every thread after the barrier that follows the level-1 stores;
+// returns after a barrier with S.n4 / S.ovf valid.
+__device__ __forceinline__ void build_index_levels(JoinSmem& S, const JoinPlan& P, uint64_t cW) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int sh = 64 - P.r;
+  const uint32_t nw = S.wcnt[wid];
+  uint16_t* lose = S.lose[wid];
+  // level 1 read-back: losers go to level 2
+  uint32_t nl = 0;
+  for (uint32_t e0 = 0; e0 < nw; e0 += 32) {
+    const uint32_t e = e0 + lane;
+    const uint32_t r = wid * kPart + e;
+    bool lost = false;
+    uint64_t rel = 0;
+    if (e < nw) {
+      rel = S.recK[r] - cW;
+      lost = S.t1[home_of(rel, sh - kL1Log, kL1Log)] != (uint16_t)r;
+    }
+    const uint32_t lm = __ballot_sync(FULL, lost);
+    if (lost) {
+      const uint32_t k = nl + __popc(lm & lt_mask);
+      if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
+      S.t2[home_of(rel, sh - kL2Log, kL2Log)] = (uint16_t)r;
+    }
+    nl += __popc(lm);
+  }
+  if (nl > (uint32_t)kLose && lane == 0) S.ovf = 1;
+  const int any2 = __syncthreads_or(nl > 0);
+  if (!any2) return;
+  // level 2 read-back: losers go to level 3
+  uint32_t nl2 = 0;
+  const uint32_t nlc = nl < (uint32_t)kLose ? nl : (uint32_t)kLose;
+  for (uint32_t e0 = 0; e0 < nlc; e0 += 32) {
+    const uint32_t e = e0 + lane;
+    bool lost = false;
+    uint32_t r = 0;
+    uint64_t rel = 0;
+    if (e < nlc) {
+      r = lose[e];
+      rel = S.recK[r] - cW;
+      lost = S.t2[home_of(rel, sh - kL2Log, kL2Log)] != (uint16_t)r;
+    }
+    const uint32_t lm = __ballot_sync(FULL, lost);
+    __syncwarp();
+    if (lost) {
+      lose[nl2 + __popc(lm & lt_mask)] = (uint16_t)r;  // compact in place (target <= e)
+      S.t3[home_of(rel, sh - kL3Log, kL3Log)] = (uint16_t)r;
+    }
+    nl2 += __popc(lm);
+    __syncwarp();
+  }
+  const int any3 = __syncthreads_or(nl2 > 0);
+  if (!any3) return;
+  // level 3 read-back: losers go to the short list (rare: shared atomic)
+  for (uint32_t e = lane; e < nl2; e += 32) {
+    const uint32_t r = lose[e];
+    if (S.t3[home_of(S.recK[r] - cW, sh - kL3Log, kL3Log)] != (uint16_t)r) {
+      const unsigned k = atomicAdd(&S.n4, 1u);
+      if (k < (unsigned)kList4) S.list4[k] = (uint16_t)r;
+      else S.ovf = 1;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void clear_index(JoinSmem& S) {
+  const uint4 f4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  uint4* p1 = reinterpret_cast<uint4*>(S.t1);
+  for (int i = threadIdx.x; i < (1 << kL1Log) / 8; i += kJoinThreads) p1[i] = f4;
+  uint4* p2 = reinterpret_cast<uint4*>(S.t2);
+  for (int i = threadIdx.x; i < (1 << kL2Log) / 8; i += kJoinThreads) p2[i] = f4;
+  uint4* p3 = reinterpret_cast<uint4*>(S.t3);
+  for (int i = threadIdx.x; i < (1 << kL3Log) / 8; i += kJoinThreads) p3[i] = f4;
+}
+
+__global__ void __launch_bounds__(kJoinThreads, 1)
+    join_kernel(const __grid_constant__ JoinArgs a, int gsA, int gsB) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  JoinSmem& S = *reinterpret_cast<JoinSmem*>(smem_raw);
+  const JoinPlan& P = a.P;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+
+  const uint32_t MoA = 1u << P.list[0].bits, MiA = 1u << P.list[1].bits;
+  const uint32_t MoB = 1u << P.list[2].bits, MiB = 1u << P.list[3].bits;
+  const uint64_t* __restrict__ kA = a.key[1];
+  const uint64_t* __restrict__ kB = a.key[3];
+  const int sh = 64 - P.r;  // bucket = key >> sh
+  const uint64_t W = 1ull << sh;
+  const uint64_t H = P.half;
+
+  const uint64_t nbk = P.bucket_end - P.bucket_begin;
+  const uint64_t c_begin = P.bucket_begin + nbk * blockIdx.x / gridDim.x;
+  const uint64_t c_end = P.bucket_begin + nbk * (blockIdx.x + 1) / gridDim.x;
+  if (c_begin >= c_end) return;
+  unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && tid == 0) ? a.dbg : nullptr;
+  int dbg_n = 0;
+#define RFR_MARK()                                   \
+  do {                                               \
+    if (dbg && dbg_n < 256) dbg[dbg_n++] = clock64(); \
+  } while (0)
+  RFR_MARK();
+
+  for (uint32_t i = tid; i < MoA; i += kJoinThreads) {
+    uint64_t x = __ldg(a.key[0] + i);
+    S.ax[i] = x;
+    S.arot[i] = rotation_start(kA, MiA, x);
+    S.apos[i] = count_below(kA, MiA, x, c_begin << sh);
+  }
+  for (uint32_t i = tid; i < MoB; i += kJoinThreads) {
+    uint64_t x = __ldg(a.key[2] + i) + P.shift;
+    S.bx[i] = x;
+    S.brot[i] = rotation_start(kB, MiB, x);
+    S.bpos[i] = count_below(kB, MiB, x, c_begin << sh);
+  }
+
+  uint32_t n_ins = 0, n_q = 0, n_qprobe = 0, n_chunks = 0;
+  const uint32_t perWA = (MoA + kJoinWarps - 1) / kJoinWarps;
+  const uint32_t aLo = min(MoA, wid * perWA), aHi = min(MoA, aLo + perWA);
+  const uint32_t perWB = (MoB + kJoinWarps - 1) / kJoinWarps;
+  const uint32_t bLo = min(MoB, wid * perWB), bHi = min(MoB, bLo + perWB);
+
+  for (uint64_t c = c_begin; c < c_end; c++) {
+    const uint64_t cW = c << sh;
+    clear_index(S);
+    if (tid == 0) {
+      S.n4 = 0;
+      S.ovf = 0;
+    }
+    __syncthreads();
+    RFR_MARK();
+
+    // ---- fast path: A windows + continuations into the warp partitions
+    bool wovf = false;
+    uint32_t wfill = 0;
+    window_pass<true>(S, a, cW, aLo, aHi, gsA, wfill, n_ins, n_qprobe, wovf);
+    __syncwarp();
+    continue_pass<true>(S, a, cW, aLo, aHi, gsA, wfill, n_ins, n_qprobe, wovf);
+    if (lane == 0) {
+      S.wcnt[wid] = wfill;
+      if (wovf) S.ovf = 1;
+    }
+    RFR_MARK();
+    __syncthreads();
+    bool overflowed = S.ovf != 0;
+    if (!overflowed) {
+      build_index_levels(S, P, cW);
+      overflowed = S.ovf != 0;
+    }
+    RFR_MARK();
+    if (!overflowed) {
+      uint32_t dummy_fill = 0;
+      bool dummy_ovf = false;
+      window_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      __syncwarp();
+      continue_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      __syncwarp();
+      for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
+      for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
+      RFR_MARK();
+      __syncthreads();
+      RFR_MARK();
+      continue;
+    }
+
+    // ---- slow path (skewed bucket): chunks of kCapRec records filled by warp 0
+    __syncthreads();
+    if (tid == 0) {
+      S.cur_i = 0;
+      S.cur_t = 0;
+    }
+    for (uint32_t i = tid; i < MoA; i += kJoinThreads) S.amain[i] = 0;
+    __syncthreads();
+    uint32_t chunk_cap = (uint32_t)kCapRec;  // halves when a chunk overflows the index
+    while (true) {
+      n_chunks++;
+      clear_index(S);
+      const uint32_t save_i = S.cur_i, save_t = S.cur_t;
+      __syncthreads();
+      if (tid == 0) {
+        S.n4 = 0;
+        S.ovf = 0;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t i = S.cur_i, t = S.cur_t, fill = 0;
+        while (i < MoA) {
+          const uint32_t pos = S.apos[i], rot = S.arot[i];
+          const uint64_t x = S.ax[i];
+          bool full = false;
+          while (true) {
+            const uint32_t q = t + lane;
+            const bool valid = q < MiA;
+            const uint32_t o = pos + q;
+            const uint32_t j = (rot + o) & (MiA - 1);
+            const uint64_t s = x + (valid ? __ldg(kA + j) : 0ull);
+            const uint64_t rel = s - cW;
+            const bool m = valid && o < MiA && rel < W;
+            const bool e = m || (valid && (rel - W) < H);
+            const uint32_t em = __ballot_sync(FULL, e);
+            const uint32_t ne_all = __popc(em);
+            const uint32_t room = chunk_cap - fill;
+            const uint32_t take = ne_all < room ? ne_all : room;  // emitted lanes are a prefix
+            if ((uint32_t)lane < take) {
+              // spread the chunk round-robin over the warp partitions
+              const uint32_t idx = fill + lane;
+              const uint32_t r = (idx % kJoinWarps) * kPart + idx / kJoinWarps;
+              S.recK[r] = s;
+              S.recI[r] = (i << P.list[1].bits) | j;
+            }
+            const uint32_t mm = __ballot_sync(FULL, m) & (take >= 32 ? FULL : ((1u << take) - 1u));
+            if (lane == 0) S.amain[i] += __popc(mm);
+            fill += take;
+            t += take;
+            n_ins += ((uint32_t)lane < take) ? 1u : 0u;
+            if (take < ne_all) {  // chunk full inside this run
+              full = true;
+              break;
+            }
+            if (ne_all < 32 || t >= MiA) break;
+          }
+          if (full) break;
+          i++;
+          t = 0;
+        }
+        if (lane == 0) {
+          S.cur_i = i;
+          S.cur_t = t;
+        }
+        if (lane < kJoinWarps)
+          S.wcnt[lane] = fill / kJoinWarps + ((uint32_t)lane < fill % kJoinWarps ? 1u : 0u);
+      }
+      __syncthreads();
+      {  // every warp claims level-1 homes for its partition, then the levels
+        const uint32_t nw = S.wcnt[wid];
+        for (uint32_t e = lane; e < nw; e += 32) {
+          const uint32_t r = wid * kPart + e;
+          S.t1[home_of(S.recK[r] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
+        }
+      }
+      __syncthreads();
+      build_index_levels(S, P, cW);
+      if (S.ovf) {  // too many colliding records: redo this chunk with half the records
+        __syncthreads();
+        if (tid == 0) {
+          S.cur_i = save_i;
+          S.cur_t = save_t;
+        }
+        for (uint32_t i = tid; i < MoA; i += kJoinThreads)
+          if (i >= save_i) S.amain[i] = 0;  // recounted by the smaller chunks
+        chunk_cap = chunk_cap > 64u ? chunk_cap / 2 : 64u;
+        __syncthreads();
+        continue;
+      }
+      const bool done = S.cur_i >= MoA;
+      uint32_t dummy_fill = 0;
+      bool dummy_ovf = false;
+      window_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      __syncwarp();
+      continue_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      __syncthreads();
+      if (done) break;
+    }
+    for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
+    for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
+    __syncthreads();
+  }
+  atomicAdd(&a.ctr->inserts, (unsigned long long)n_ins);
+  atomicAdd(&a.ctr->queries, (unsigned long long)n_q);
+  atomicAdd(&a.ctr->query_probes, (unsigned long long)n_qprobe);
+  if (tid == 0) {
+    atomicAdd(&a.ctr->chunks, (unsigned long long)n_chunks);
+    atomicAdd(&a.ctr->buckets, (unsigned long long)(c_end - c_begin));
+  }
+}
