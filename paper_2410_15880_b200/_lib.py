@@ -81,7 +81,6 @@ class RfrProfile(ctypes.Structure):
 
 
 _lib = None
-_partial: list = []
 _lock = threading.Lock()
 _device = None
 
@@ -124,17 +123,16 @@ def load():
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.POINTER(RfrStats),
         ]
-        if not all(hasattr(L, name) for name in EXPORTS):
-            missing = [name for name in EXPORTS if not hasattr(L, name)]
-            _partial.extend(missing)
-        if hasattr(L, "rfr_verify"):
-          L.rfr_verify.argtypes = [
+        missing = [name for name in EXPORTS if not hasattr(L, name)]
+        if missing:
+            raise RecombineDeviceError(f"{LIB_PATH} lacks exports {missing}: rebuild it")
+        L.rfr_verify.argtypes = [
             ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int64, U64_P, ctypes.c_int, U8_P, U8_P,
             I64_P, ctypes.c_int, ctypes.POINTER(RfrStats),
         ]
-          L.rfr_verify_primes.argtypes = [U64_P]
-          L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]
-          L.rfr_squarefree_mod.argtypes = [U64_P, ctypes.c_int, ctypes.c_uint64]
+        L.rfr_verify_primes.argtypes = [U64_P]
+        L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]
+        L.rfr_squarefree_mod.argtypes = [U64_P, ctypes.c_int, ctypes.c_uint64]
         _lib = L
         return L
 

@@ -20,6 +20,29 @@
 
 using namespace rfr;
 
+namespace rfr {
+struct VerifyArgs {
+  int n, r, c, d;
+  const double* real_hi;
+  const double* real_lo;
+  const double* sum_hi;
+  const double* sum_lo;
+  const double* prod_hi;
+  const double* prod_lo;
+  const int32_t* perm;
+  double root_err;
+  const uint64_t* pats;
+  long long m;
+  const uint64_t* p_mod;
+  uint64_t primes[3];
+  uint8_t* verdict;
+  uint8_t* side;
+  long long* coeffs;
+  int stride;
+};
+cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s);
+}  // namespace rfr
+
 namespace {
 
 std::mutex g_mu;
@@ -52,6 +75,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   DevVec keys, rho, raw, post, ctr;
+  DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
   // cache of the last built lists (key values + plan geometry)
@@ -286,6 +310,12 @@ int rfr_shutdown(void) {
   g.rho.release();
   g.raw.release();
   g.post.release();
+  g.vprof.release();
+  g.vpats.release();
+  g.vpmod.release();
+  g.vverd.release();
+  g.vside.release();
+  g.vcoef.release();
   g.ctr.release();
   for (auto& a : g.lk)
     for (auto& v : a) v.release();
@@ -428,6 +458,94 @@ int rfr_search_keys_dev(const uint64_t* d_keys, int n, uint64_t lo, uint64_t wid
     st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
     st->ms_join = ev_ms(g.ev[1], g.ev[2]);
     st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+  }
+  return RFR_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rfr_verify_primes(uint64_t* primes3) {
+  if (!primes3) return rfr_fail(RFR_E_ARG, "null primes buffer");
+  for (int i = 0; i < 3; i++) primes3[i] = kVerifyPrimes[i];
+  return RFR_OK;
+}
+
+int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const uint64_t* p_mod,
+               int d, uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride,
+               rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if (!prof || m < 0 || d < 1 || d > 128 || stride < 1) return rfr_fail(RFR_E_ARG, "bad verify arguments");
+  if (prof->n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits");
+  if (prof->r + 2 * prof->c != d || prof->r + prof->c != prof->n)
+    return rfr_fail(RFR_E_ARG, "profile does not match the degree");
+  if (m == 0) return RFR_OK;
+  cudaSetDevice(g.device);
+  cudaStream_t s = g.stream;
+  // pack the profile: 6 double arrays + perm
+  const int r = prof->r, c = prof->c, n = prof->n;
+  std::vector<double> hostd(2 * r + 4 * c + 1, 0.0);
+  double* hp = hostd.data();
+  for (int i = 0; i < r; i++) {
+    hp[i] = prof->real_hi[i];
+    hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
+  }
+  for (int j = 0; j < c; j++) {
+    hp[2 * r + j] = prof->sum_hi[j];
+    hp[2 * r + c + j] = prof->sum_lo ? prof->sum_lo[j] : 0.0;
+    hp[2 * r + 2 * c + j] = prof->prod_hi[j];
+    hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
+  }
+  const size_t dbytes = hostd.size() * sizeof(double);
+  RFR_CUDA_OK(g.vprof.ensure(dbytes + 64 * sizeof(int32_t)));
+  RFR_CUDA_OK(g.vpats.ensure((size_t)m * sizeof(uint64_t)));
+  RFR_CUDA_OK(g.vpmod.ensure((size_t)3 * (d + 1) * sizeof(uint64_t)));
+  RFR_CUDA_OK(g.vverd.ensure((size_t)m));
+  RFR_CUDA_OK(g.vside.ensure((size_t)m));
+  RFR_CUDA_OK(g.vcoef.ensure((size_t)m * stride * sizeof(int64_t)));
+  char* base = (char*)g.vprof.p;
+  RFR_CUDA_OK(cudaMemcpyAsync(base, hostd.data(), dbytes, cudaMemcpyHostToDevice, s));
+  RFR_CUDA_OK(cudaMemcpyAsync(base + dbytes, prof->perm, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  RFR_CUDA_OK(cudaMemcpyAsync(g.vpats.p, pats, (size_t)m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  RFR_CUDA_OK(cudaMemcpyAsync(g.vpmod.p, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t),
+                              cudaMemcpyHostToDevice, s));
+  VerifyArgs A;
+  A.n = n;
+  A.r = r;
+  A.c = c;
+  A.d = d;
+  const double* dp = (const double*)base;
+  A.real_hi = dp;
+  A.real_lo = dp + r;
+  A.sum_hi = dp + 2 * r;
+  A.sum_lo = dp + 2 * r + c;
+  A.prod_hi = dp + 2 * r + 2 * c;
+  A.prod_lo = dp + 2 * r + 3 * c;
+  A.perm = (const int32_t*)(base + dbytes);
+  A.root_err = prof->root_err;
+  A.pats = (const uint64_t*)g.vpats.p;
+  A.m = m;
+  A.p_mod = (const uint64_t*)g.vpmod.p;
+  for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
+  A.verdict = (uint8_t*)g.vverd.p;
+  A.side = (uint8_t*)g.vside.p;
+  A.coeffs = (long long*)g.vcoef.p;
+  A.stride = stride;
+  RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
+  RFR_CUDA_OK(launch_verify(A, s));
+  RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+  RFR_CUDA_OK(cudaMemcpyAsync(verdict, g.vverd.p, (size_t)m, cudaMemcpyDeviceToHost, s));
+  RFR_CUDA_OK(cudaMemcpyAsync(side, g.vside.p, (size_t)m, cudaMemcpyDeviceToHost, s));
+  RFR_CUDA_OK(cudaMemcpyAsync(coeffs, g.vcoef.p, (size_t)m * stride * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, s));
+  RFR_CUDA_OK(cudaStreamSynchronize(s));
+  if (st) {
+    memset(st, 0, sizeof *st);
+    st->ms_post = ev_ms(g.ev[2], g.ev[3]);
+    st->ms_total = st->ms_post;
   }
   return RFR_OK;
 }

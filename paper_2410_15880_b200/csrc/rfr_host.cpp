@@ -1,0 +1,226 @@
+// rfr_host.cpp -- native host numerics for the preprocessing in front of the
+// search (not timed: north_star puts root finding outside the timed path).
+//
+//  rfr_polish_roots   simultaneous Aberth-Ehrlich corrections in double-double
+//                     complex arithmetic (~106-bit), seeded by any approximate
+//                     roots, with an a-posteriori error bound per root.  It
+//                     replaces find_roots' iteration (pkg/src/polyfactor/
+//                     rootfinder.py:100-174), whose 64-bit roots would make the
+//                     subset-sum keys ~2^-45 coarse; ~2^-100 roots make them
+//                     exact to the last key bit.
+//  rfr_squarefree_mod gcd(p, p') over F_q, the fast screen in front of the
+//                     exact square-free decomposition (polynomial.py:221-247).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/rfr.h"
+
+namespace {
+
+// ---------------------------------------------------------- double-double
+struct dd {
+  double hi, lo;
+};
+
+inline dd two_sum(double a, double b) {
+  double s = a + b;
+  double bb = s - a;
+  double e = (a - (s - bb)) + (b - bb);
+  return {s, e};
+}
+inline dd quick_two_sum(double a, double b) {
+  double s = a + b;
+  return {s, b - (s - a)};
+}
+inline dd two_prod(double a, double b) {
+  double p = a * b;
+  return {p, std::fma(a, b, -p)};
+}
+inline dd operator+(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  dd t = two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+inline dd operator-(dd a) { return {-a.hi, -a.lo}; }
+inline dd operator-(dd a, dd b) { return a + (-b); }
+inline dd operator*(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo + a.lo * b.hi;
+  return quick_two_sum(p.hi, p.lo);
+}
+inline dd operator/(dd a, dd b) {
+  double q1 = a.hi / b.hi;
+  dd r = a - b * dd{q1, 0.0};
+  double q2 = r.hi / b.hi;
+  r = r - b * dd{q2, 0.0};
+  double q3 = r.hi / b.hi;
+  dd q = quick_two_sum(q1, q2);
+  return q + dd{q3, 0.0};
+}
+inline double to_d(dd a) { return a.hi + a.lo; }
+
+struct cdd {
+  dd re, im;
+};
+inline cdd operator+(cdd a, cdd b) { return {a.re + b.re, a.im + b.im}; }
+inline cdd operator-(cdd a, cdd b) { return {a.re - b.re, a.im - b.im}; }
+inline cdd operator*(cdd a, cdd b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+inline cdd operator/(cdd a, cdd b) {
+  // Smith's algorithm: no |b|^2, so no overflow for |b| ~ 1e160 (|z|^d of
+  // degree-100 polynomials with roots near 40)
+  if (std::fabs(b.re.hi) >= std::fabs(b.im.hi)) {
+    const dd r = b.im / b.re;
+    const dd den = b.re + b.im * r;
+    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  }
+  const dd r = b.re / b.im;
+  const dd den = b.re * r + b.im;
+  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+inline double cabs_d(cdd a) { return std::hypot(to_d(a.re), to_d(a.im)); }
+
+// p(z), p'(z) by Horner in double-double, with the running bound
+// sum_k |a_k| |z|^k used for the evaluation-error estimate.
+void horner(const std::vector<dd>& c, cdd z, cdd& pz, cdd& dpz, double& absum) {
+  const int d = (int)c.size() - 1;
+  cdd p = {c[d], {0, 0}};
+  cdd q = {{0, 0}, {0, 0}};
+  const double az = cabs_d(z);
+  double s = std::fabs(to_d(c[d]));
+  for (int k = d - 1; k >= 0; k--) {
+    q = q * z + p;
+    p = p * z + cdd{c[k], {0, 0}};
+    s = s * az + std::fabs(to_d(c[k]));
+  }
+  pz = p;
+  dpz = q;
+  absum = s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double* re_hi,
+                     double* re_lo, double* im_hi, double* im_lo, double* err, int max_iter) {
+  if (d < 1 || !coef_hi || !re_hi || !im_hi || !err) return RFR_E_ARG;
+  std::vector<dd> c(d + 1);
+  for (int k = 0; k <= d; k++) c[k] = {coef_hi[k], coef_lo ? coef_lo[k] : 0.0};
+  if (c[d].hi != 1.0 || c[d].lo != 0.0) return RFR_E_ARG;  // monic only
+  std::vector<cdd> z(d);
+  for (int i = 0; i < d; i++)
+    z[i] = {{re_hi[i], re_lo ? re_lo[i] : 0.0}, {im_hi[i], im_lo ? im_lo[i] : 0.0}};
+  const double eps_dd = std::ldexp(1.0, -104);
+  std::vector<cdd> corr(d);
+  int it = 0;
+  for (; it < max_iter; it++) {
+    double worst = 0.0;
+    for (int i = 0; i < d; i++) {
+      cdd pz, dpz;
+      double absum;
+      horner(c, z[i], pz, dpz, absum);
+      if (to_d(dpz.re) == 0.0 && to_d(dpz.im) == 0.0) dpz.re = {1e-300, 0.0};
+      cdd w = pz / dpz;
+      cdd sum = {{0, 0}, {0, 0}};
+      for (int j = 0; j < d; j++) {
+        if (j == i) continue;
+        cdd diff = z[i] - z[j];
+        if (to_d(diff.re) == 0.0 && to_d(diff.im) == 0.0) diff.re = {1e-300, 0.0};
+        sum = sum + cdd{{1.0, 0}, {0, 0}} / diff;
+      }
+      cdd den = cdd{{1.0, 0}, {0, 0}} - w * sum;
+      if (to_d(den.re) == 0.0 && to_d(den.im) == 0.0) den.re = {1e-300, 0.0};
+      corr[i] = w / den;
+      const double rel = cabs_d(corr[i]) / std::fmax(1.0, cabs_d(z[i]));
+      worst = std::fmax(worst, rel);
+    }
+    for (int i = 0; i < d; i++) z[i] = z[i] - corr[i];  // Jacobi-style update
+    if (worst < 8.0 * eps_dd) break;
+  }
+  // a posteriori bounds: Newton step plus evaluation error, and separation
+  for (int i = 0; i < d; i++) {
+    cdd pz, dpz;
+    double absum;
+    horner(c, z[i], pz, dpz, absum);
+    const double gamma = (4.0 * d + 8.0) * eps_dd;
+    const double num = cabs_d(pz) + gamma * absum;
+    const double den = cabs_d(dpz);
+    double e = den > 0.0 ? 2.0 * num / den : INFINITY;
+    e = std::fmax(e, 4.0 * eps_dd * std::fmax(1.0, cabs_d(z[i])));
+    err[i] = e;
+  }
+  int status = RFR_OK;
+  for (int i = 0; i < d && status == RFR_OK; i++) {
+    if (!std::isfinite(err[i])) status = RFR_E_NUMERIC;
+    for (int j = i + 1; j < d; j++) {
+      const double sep = cabs_d(z[i] - z[j]);
+      if (sep <= 4.0 * (err[i] + err[j])) {
+        status = RFR_E_NUMERIC;
+        break;
+      }
+    }
+  }
+  for (int i = 0; i < d; i++) {
+    re_hi[i] = z[i].re.hi;
+    if (re_lo) re_lo[i] = z[i].re.lo;
+    im_hi[i] = z[i].im.hi;
+    if (im_lo) im_lo[i] = z[i].im.lo;
+  }
+  return status;
+}
+
+static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) {
+  return (uint64_t)(((unsigned __int128)a * b) % q);
+}
+static inline uint64_t powmod(uint64_t a, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, q);
+    a = mulmod(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+
+int rfr_squarefree_mod(const uint64_t* cm, int d, uint64_t q) {
+  if (d < 1 || q < 3) return 0;
+  if (cm[d] % q == 0) return 0;
+  if (d == 1) return 1;
+  std::vector<uint64_t> a(cm, cm + d + 1), b(d);
+  for (auto& v : a) v %= q;
+  for (int k = 1; k <= d; k++) b[k - 1] = mulmod(a[k], (uint64_t)k % q, q);
+  int da = d, db = d - 1;
+  while (db >= 0 && b[db] == 0) db--;
+  if (db < 0) return 0;  // p' == 0 mod q: undecided
+  // Euclid over F_q
+  while (db >= 0) {
+    const uint64_t inv = powmod(b[db], q - 2, q);
+    while (da >= db) {
+      const uint64_t f = mulmod(a[da], inv, q);
+      if (f) {
+        for (int k = 0; k <= db; k++) {
+          const uint64_t sub = mulmod(f, b[k], q);
+          const int idx = da - db + k;
+          a[idx] = a[idx] >= sub ? a[idx] - sub : a[idx] + q - sub;
+        }
+      }
+      da--;
+      while (da >= 0 && a[da] == 0) da--;
+      if (da < 0) break;
+    }
+    std::swap(a, b);
+    std::swap(da, db);
+    if (db < 0) break;
+  }
+  // gcd is a (degree da)
+  return da == 0 ? 1 : 0;
+}
+
+}  // extern "C"

@@ -15,4 +15,8 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            double eps, uint64_t* d_out, unsigned long long cap_out,
                            DevCounters* d_ctr, int nsm, cudaStream_t s);
 cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaStream_t s);
+
+struct VerifyArgs;
+constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 1152921504606846883ull,
+                                       576460752303423433ull};
 }  // namespace rfr

@@ -1,0 +1,241 @@
+// rfr_verify.cu -- batched candidate verification on sm_100a, one warp per
+// candidate.  Replaces the reference's per-candidate Python loop
+// build_candidate -> trace_test -> round_and_divide (pkg/src/polyfactor/
+// verify.py:60-155, driven at :267-286):
+//   1. pick the smaller-degree side of {pattern, complement} (both are
+//      factors or neither is);
+//   2. multiply out its linear (x - u) and quadratic (x^2 - t x + m) pieces in
+//      double-double (~106 bits), lane-parallel over the coefficients;
+//   3. bound every coefficient's error from the roots' error bound and the
+//      arithmetic (a magnitude polynomial evaluated with perturbed roots), and
+//      reject any coefficient farther from an integer than its bound (the
+//      reference's eps test, verify.py:145-148, with a derived tolerance);
+//   4. trial-divide the input p by the rounded monic q modulo three 61-bit
+//      primes (the reference's divide_exact, polynomial.py:155-183, as a
+//      filter; the host confirms survivors exactly with the certificate).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/rfr.h"
+#include "rfr_common.cuh"
+
+namespace rfr {
+
+struct ddv {
+  double hi, lo;
+};
+
+__device__ __forceinline__ ddv dd_two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ ddv dd_quick(double a, double b) {
+  double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ ddv dd_add(ddv a, ddv b) {
+  ddv s = dd_two_sum(a.hi, b.hi);
+  ddv t = dd_two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = dd_quick(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return dd_quick(s.hi, s.lo);
+}
+__device__ __forceinline__ ddv dd_mul(ddv a, ddv b) {
+  double p = __dmul_rn(a.hi, b.hi);
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e = __fma_rn(a.hi, b.lo, e);
+  e = __fma_rn(a.lo, b.hi, e);
+  return dd_quick(p, e);
+}
+__device__ __forceinline__ ddv dd_neg(ddv a) { return {-a.hi, -a.lo}; }
+
+constexpr int kVerifyWarps = 8;
+constexpr int kMaxE = 64;          // smaller side degree <= 64 (n <= 64 roots of p, d <= 128)
+constexpr int kMaxD = 128;
+
+struct VerifyArgs {
+  int n, r, c, d;
+  const double* real_hi;
+  const double* real_lo;
+  const double* sum_hi;
+  const double* sum_lo;
+  const double* prod_hi;
+  const double* prod_lo;
+  const int32_t* perm;
+  double root_err;
+  const uint64_t* pats;
+  long long m;
+  const uint64_t* p_mod;  // 3 x (d+1)
+  uint64_t primes[3];
+  uint8_t* verdict;
+  uint8_t* side;
+  long long* coeffs;
+  int stride;
+};
+
+struct WarpBuf {
+  ddv c[2][kMaxE + 2];
+  double mag[2][kMaxE + 2];
+  double magp[2][kMaxE + 2];
+  uint64_t rem[kMaxD + 1];
+  long long q[kMaxE + 1];
+};
+
+__device__ __forceinline__ uint64_t mulmod61(uint64_t a, uint64_t b, uint64_t p) {
+  const unsigned __int128 x = (unsigned __int128)a * b;
+  return (uint64_t)(x % p);
+}
+
+__global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A) {
+  __shared__ WarpBuf bufs[kVerifyWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpBuf& B = bufs[w];
+  const long long k = (long long)blockIdx.x * kVerifyWarps + w;
+  if (k >= A.m) return;
+  const uint64_t full = A.n >= 64 ? ~0ull : ((1ull << A.n) - 1ull);
+  const uint64_t s = A.pats[k] & full;
+  int deg_s = 0;
+  for (int i = 0; i < A.n; i++)
+    if ((s >> i) & 1ull) deg_s += A.perm[i] < A.r ? 1 : 2;
+  const bool use_comp = deg_s > A.d - deg_s;
+  const uint64_t t = use_comp ? (~s & full) : s;
+  const int e = use_comp ? A.d - deg_s : deg_s;
+  if (lane == 0) A.side[k] = use_comp ? 1 : 0;
+  if (e < 1 || e >= A.d || e > kMaxE) {
+    if (lane == 0) A.verdict[k] = (e > kMaxE) ? RFR_V_HOST : RFR_V_REJECT;
+    return;
+  }
+
+  // ---- expand prod (x - u) * prod (x^2 - t x + m) over the selected entities
+  int cur = 0, len = 1;  // current polynomial has `len` coefficients
+  for (int i = lane; i < kMaxE + 2; i += 32) {
+    B.c[0][i] = {i == 0 ? 1.0 : 0.0, 0.0};
+    B.mag[0][i] = i == 0 ? 1.0 : 0.0;
+    B.magp[0][i] = i == 0 ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  const double de = A.root_err;
+  for (int i = 0; i < A.n; i++) {
+    if (!((t >> i) & 1ull)) continue;
+    const int ent = A.perm[i];
+    const int nxt = cur ^ 1;
+    if (ent < A.r) {
+      const ddv u = {A.real_hi[ent], A.real_lo[ent]};
+      const double au = fabs(u.hi);
+      for (int j = lane; j <= len; j += 32) {
+        ddv v = {0.0, 0.0};
+        if (j >= 1) v = B.c[cur][j - 1];
+        if (j < len) v = dd_add(v, dd_neg(dd_mul(u, B.c[cur][j])));
+        double mv = (j >= 1 ? B.mag[cur][j - 1] : 0.0) + (j < len ? au * B.mag[cur][j] : 0.0);
+        double mp = (j >= 1 ? B.magp[cur][j - 1] : 0.0) +
+                    (j < len ? (au + de) * B.magp[cur][j] : 0.0);
+        B.c[nxt][j] = v;
+        B.mag[nxt][j] = mv;
+        B.magp[nxt][j] = mp;
+      }
+      len += 1;
+    } else {
+      const int jj = ent - A.r;
+      const ddv tt = {A.sum_hi[jj], A.sum_lo[jj]};
+      const ddv mm = {A.prod_hi[jj], A.prod_lo[jj]};
+      const double at = fabs(tt.hi), am = fabs(mm.hi);
+      const double dt = 2.0 * de, dm = 2.0 * sqrt(am) * de + de * de;
+      for (int j = lane; j <= len + 1; j += 32) {
+        ddv v = {0.0, 0.0};
+        if (j >= 2) v = B.c[cur][j - 2];
+        if (j >= 1 && j - 1 < len) v = dd_add(v, dd_neg(dd_mul(tt, B.c[cur][j - 1])));
+        if (j < len) v = dd_add(v, dd_mul(mm, B.c[cur][j]));
+        double mv = (j >= 2 ? B.mag[cur][j - 2] : 0.0) +
+                    (j >= 1 && j - 1 < len ? at * B.mag[cur][j - 1] : 0.0) +
+                    (j < len ? am * B.mag[cur][j] : 0.0);
+        double mp = (j >= 2 ? B.magp[cur][j - 2] : 0.0) +
+                    (j >= 1 && j - 1 < len ? (at + dt) * B.magp[cur][j - 1] : 0.0) +
+                    (j < len ? (am + dm) * B.magp[cur][j] : 0.0);
+        B.c[nxt][j] = v;
+        B.mag[nxt][j] = mv;
+        B.magp[nxt][j] = mp;
+      }
+      len += 2;
+    }
+    cur = nxt;
+    __syncwarp();
+  }
+  // len == e + 1
+
+  // ---- integrality with a derived error bound
+  const double arith = (double)(4 * e + 8) * 7.9e-31;  // ~ (4e+8) * 2^-100
+  bool reject = false, host = false;
+  for (int j = lane; j <= e; j += 32) {
+    const ddv v = B.c[cur][j];
+    double rnd = nearbyint(v.hi);
+    double frac = (v.hi - rnd) + v.lo;
+    if (frac > 0.5) {
+      rnd += 1.0;
+      frac -= 1.0;
+    } else if (frac < -0.5) {
+      rnd -= 1.0;
+      frac += 1.0;
+    }
+    const double bound = (B.magp[cur][j] - B.mag[cur][j]) + B.mag[cur][j] * arith + 1e-300;
+    if (bound > 0.25 || fabs(rnd) >= 4.611686018427388e18) host = true;
+    else if (fabs(frac) > 2.0 * bound) reject = true;
+    B.q[j] = (long long)rnd;
+  }
+  reject = __any_sync(0xffffffffu, reject);
+  host = __any_sync(0xffffffffu, host);
+  if (reject) {
+    if (lane == 0) A.verdict[k] = RFR_V_REJECT;
+    return;
+  }
+  if (host) {
+    if (lane == 0) A.verdict[k] = RFR_V_HOST;
+    return;
+  }
+  __syncwarp();
+  if (B.q[e] != 1) {
+    if (lane == 0) A.verdict[k] = RFR_V_REJECT;
+    return;
+  }
+
+  // ---- trial division of p by q modulo three 61-bit primes
+  bool divides = true;
+  for (int pi = 0; pi < 3 && divides; pi++) {
+    const uint64_t P = A.primes[pi];
+    const uint64_t* pm = A.p_mod + (size_t)pi * (A.d + 1);
+    for (int j = lane; j <= A.d; j += 32) B.rem[j] = pm[j];
+    __syncwarp();
+    for (int kk = A.d - e; kk >= 0; kk--) {
+      const uint64_t lead = B.rem[kk + e];  // q monic
+      __syncwarp();
+      if (lead) {
+        for (int j = lane; j < e; j += 32) {
+          const long long qj = B.q[j];
+          const uint64_t qm = qj >= 0 ? (uint64_t)qj % P : (P - ((uint64_t)(-qj) % P)) % P;
+          const uint64_t sub = mulmod61(lead, qm, P);
+          const uint64_t r0 = B.rem[kk + j];
+          B.rem[kk + j] = r0 >= sub ? r0 - sub : r0 + P - sub;
+        }
+      }
+      __syncwarp();
+    }
+    bool nz = false;
+    for (int j = lane; j < e; j += 32) nz |= B.rem[j] != 0;
+    divides = !__any_sync(0xffffffffu, nz);
+    __syncwarp();
+  }
+  if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
+  if (divides)
+    for (int j = lane; j <= e && j < A.stride; j += 32) A.coeffs[k * A.stride + j] = B.q[j];
+}
+
+cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s) {
+  if (A.m <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((A.m + kVerifyWarps - 1) / kVerifyWarps);
+  verify_kernel<<<blocks, kVerifyWarps * 32, 0, s>>>(A);
+  return cudaGetLastError();
+}
+
+}  // namespace rfr

@@ -1,0 +1,449 @@
+"""Host preprocessing: roots, the rho profile and the fixed-point search keys.
+
+Drop-in for ``pkg/src/polyfactor/rootfinder.py`` ("R/rootfinder.py"):
+``ToleranceConfig``, ``RootProfile``, ``find_roots``, ``build_profile``,
+``profile_polynomial``, ``expected_real_roots``, ``expected_n``,
+``residual_bound`` keep their names, fields and errors.  Root finding is
+host preprocessing and is not timed (BASELINE.json north_star).
+
+What is new is ``hp_profile``: the profile ``factor()`` searches with.  Roots
+are seeded by ``numpy.roots`` and polished to ~106 bits in double-double by the
+native Aberth iteration in ``librfr.so`` (``rfr_polish_roots``), which also
+returns an a-posteriori error bound per root.  From the polished roots every
+entity (real root u, or conjugate pair x^2 - t x + m) gets two exact 64-bit
+fixed-point keys -- frac(u or t) and frac(u^2 or t^2 - 2m), the first two
+power sums, both integers for every true factor -- and a window half-width T
+derived from the error bounds.  DESIGN.md section 2 explains why this replaces
+the reference's float64 rho + eps band for the factor() path.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from .errors import NonConvergence, UnpairedComplexRoot
+from .polynomial import IntPolynomial
+
+_TWO64 = 1 << 64
+
+
+@dataclass(frozen=True)
+class ToleranceConfig:
+    """Numeric tolerances (R/rootfinder.py:23-55): eps drives candidate
+    acceptance in the parity-mode search (recombine_e), root_tol and
+    imag_threshold the float64 root API."""
+
+    eps: float = 1e-6
+    root_tol: float = 1e-12
+    imag_threshold: float = 1e-9
+    precision: str = "auto"  # auto | double | extended
+    max_iterations: int = 500
+
+    def __post_init__(self):
+        if not 0 < self.eps < 0.5:
+            raise ValueError("eps must be in (0, 0.5)")
+        if self.root_tol <= 0:
+            raise ValueError("root_tol must be positive")
+        if self.imag_threshold <= 0:
+            raise ValueError("imag_threshold must be positive")
+        if self.precision not in ("auto", "double", "extended"):
+            raise ValueError("precision must be auto, double, or extended")
+
+    def complex_dtype(self, degree: int):
+        if self.precision == "double":
+            return np.complex128
+        if self.precision == "extended" or degree > 50:
+            return np.clongdouble
+        return np.complex128
+
+
+@dataclass(frozen=True)
+class RootProfile:
+    """Classified roots of one square-free polynomial (R/rootfinder.py:58-84).
+
+    rho holds frac() of the r real roots and c pair sums, sorted; perm[i]
+    names the entity behind rho[i] (0..r-1 real, r..r+c-1 pairs).  The
+    optional fields carry the high-precision data of ``hp_profile``: the
+    low words of the double-double values, the 64-bit search keys in rho
+    order, the key-window half-width and the absolute root error bound."""
+
+    real_roots: np.ndarray
+    pair_sums: np.ndarray
+    pair_products: np.ndarray
+    rho: np.ndarray
+    perm: tuple
+    real_lo: np.ndarray | None = field(default=None, repr=False, compare=False)
+    sum_lo: np.ndarray | None = field(default=None, repr=False, compare=False)
+    prod_lo: np.ndarray | None = field(default=None, repr=False, compare=False)
+    keys1: np.ndarray | None = field(default=None, repr=False, compare=False)
+    keys2: np.ndarray | None = field(default=None, repr=False, compare=False)
+    key_err1: int = field(default=0, repr=False, compare=False)
+    key_err2: int = field(default=0, repr=False, compare=False)
+    root_err: float = field(default=0.0, repr=False, compare=False)
+
+    @property
+    def r(self) -> int:
+        return len(self.real_roots)
+
+    @property
+    def c(self) -> int:
+        return len(self.pair_sums)
+
+    @property
+    def n(self) -> int:
+        return self.r + self.c
+
+
+def frac(x: float) -> float:
+    """Fractional part in [0, 1); frac(-0.25) == 0.75 (R/rootfinder.py:95-97)."""
+    return float(x) - math.floor(x)
+
+
+# ------------------------------------------------------------ hp roots
+def _dd_split(v: Fraction) -> tuple[float, float]:
+    hi = float(v)
+    lo = float(v - Fraction(hi))
+    return hi, lo
+
+
+def _dd_frac(hi: float, lo: float) -> Fraction:
+    return Fraction(hi) + Fraction(lo)
+
+
+def _initial_roots(coeffs: list[int]) -> np.ndarray:
+    """Seeds: eigenvalues of the companion matrix (numpy.roots)."""
+    d = len(coeffs) - 1
+    if d == 1:
+        return np.array([complex(-coeffs[0] / coeffs[1])])
+    c = np.array([float(a) for a in coeffs[::-1]], dtype=np.float64)
+    z = np.roots(c)
+    if len(z) != d or not np.all(np.isfinite(z)):
+        raise NonConvergence("numpy.roots failed to seed the root polish")
+    return z
+
+
+def _polish_dd(coeffs: list[int], z0: np.ndarray, max_iter: int = 60):
+    """Native double-double Aberth polish.  Returns (re_hi, re_lo, im_hi,
+    im_lo, err) or None when the roots cannot be certified."""
+    from . import _lib
+
+    lib = _lib.load()
+    d = len(coeffs) - 1
+    ch = np.zeros(d + 1)
+    cl = np.zeros(d + 1)
+    for k, a in enumerate(coeffs):
+        hi, lo = _dd_split(Fraction(a))
+        if Fraction(hi) + Fraction(lo) != a:
+            return None  # coefficient not representable in double-double
+        ch[k], cl[k] = hi, lo
+    rh = np.ascontiguousarray(z0.real, dtype=np.float64).copy()
+    ih = np.ascontiguousarray(z0.imag, dtype=np.float64).copy()
+    rl = np.zeros(d)
+    il = np.zeros(d)
+    err = np.zeros(d)
+    D = ctypes.POINTER(ctypes.c_double)
+    rc = lib.rfr_polish_roots(ch.ctypes.data_as(D), cl.ctypes.data_as(D), d, rh.ctypes.data_as(D),
+                              rl.ctypes.data_as(D), ih.ctypes.data_as(D), il.ctypes.data_as(D),
+                              err.ctypes.data_as(D), max_iter)
+    if rc != 0:
+        return None
+    return rh, rl, ih, il, err
+
+
+def _polish_mp(coeffs: list[int], z0: np.ndarray):
+    """Multiprecision Aberth polish for coefficients beyond double-double
+    (e.g. Swinnerton-Dyer f6, 131-bit coefficients).  Returns the same tuple
+    as _polish_dd."""
+    import mpmath
+
+    d = len(coeffs) - 1
+    bits = max(abs(c) for c in coeffs).bit_length()
+    prec = max(256, bits + 160)
+    with mpmath.workprec(prec):
+        cs = [mpmath.mpf(c) for c in coeffs]
+        z = [mpmath.mpc(complex(w)) for w in z0]
+        # jitter coincident seeds
+        for i in range(d):
+            for j in range(i):
+                if abs(z[i] - z[j]) < mpmath.mpf(2) ** -20:
+                    z[i] += mpmath.mpc(0, 1e-6 * (i + 1))
+
+        def evalp(x):
+            p = cs[d]
+            dp = mpmath.mpc(0)
+            for k in range(d - 1, -1, -1):
+                dp = dp * x + p
+                p = p * x + cs[k]
+            return p, dp
+
+        tol = mpmath.mpf(2) ** (-(prec - 40))
+        for _ in range(200):
+            worst = mpmath.mpf(0)
+            new = []
+            for i in range(d):
+                p, dp = evalp(z[i])
+                if dp == 0:
+                    dp = mpmath.mpf(2) ** -prec
+                w = p / dp
+                s = mpmath.mpc(0)
+                for j in range(d):
+                    if j != i:
+                        s += 1 / (z[i] - z[j])
+                corr = w / (1 - w * s)
+                new.append(z[i] - corr)
+                worst = max(worst, abs(corr) / max(1, abs(z[i])))
+            z = new
+            if worst < tol:
+                break
+        else:
+            return None
+        err = np.zeros(d)
+        rh, rl, ih, il = (np.zeros(d) for _ in range(4))
+        for i in range(d):
+            p, dp = evalp(z[i])
+            e = 2 * (abs(p) + abs(z[i]) * mpmath.mpf(2) ** (bits - prec + 8)) / abs(dp)
+            err[i] = float(max(e, mpmath.mpf(2) ** -110 * max(1, abs(z[i]))))
+            re = _mpf_to_fraction(z[i].real)
+            im = _mpf_to_fraction(z[i].imag)
+            rh[i], rl[i] = _dd_split(re)
+            ih[i], il[i] = _dd_split(im)
+        return rh, rl, ih, il, err
+
+
+def _mpf_to_fraction(x) -> Fraction:
+    import mpmath
+
+    sign, man, exp, _ = mpmath.mpf(x)._mpf_
+    v = Fraction(int(man) << exp) if exp >= 0 else Fraction(int(man), 1 << (-exp))
+    return -v if sign else v
+
+
+def hp_roots(p: IntPolynomial):
+    """All roots of a monic square-free p to ~2^-100, with error bounds.
+    Returns (re_hi, re_lo, im_hi, im_lo, err)."""
+    if not p.is_monic():
+        raise ValueError("hp_roots expects a monic polynomial")
+    coeffs = list(p.coeffs)
+    d = len(coeffs) - 1
+    if d < 1:
+        raise ValueError("find_roots requires degree >= 1")
+    z0 = _initial_roots(coeffs)
+    res = None
+    if max(abs(c) for c in coeffs).bit_length() <= 100:
+        res = _polish_dd(coeffs, z0)
+    if res is None:
+        res = _polish_mp(coeffs, z0)
+    if res is None:
+        raise NonConvergence("root polish did not converge")
+    return res
+
+
+def _pair_up(re_hi, re_lo, im_hi, im_lo, err):
+    """Classify real roots / conjugate pairs from polished roots."""
+    d = len(re_hi)
+    reals, uppers, lowers = [], [], []
+    for i in range(d):
+        im = abs(im_hi[i])
+        if im <= 8.0 * err[i] + 1e-300:
+            reals.append(i)
+        elif im_hi[i] > 0:
+            uppers.append(i)
+        else:
+            lowers.append(i)
+    if len(uppers) != len(lowers):
+        raise UnpairedComplexRoot(f"{len(uppers)} upper vs {len(lowers)} lower half-plane roots")
+    pairs = []
+    free = list(lowers)
+    for u in uppers:
+        best = min(free, key=lambda v: abs(complex(re_hi[v] - re_hi[u], im_hi[v] + im_hi[u])))
+        if abs(complex(re_hi[best] - re_hi[u], im_hi[best] + im_hi[u])) > 1e-6 * max(1.0, abs(complex(re_hi[u], im_hi[u]))):
+            raise UnpairedComplexRoot(f"no conjugate partner for root {complex(re_hi[u], im_hi[u])}")
+        free.remove(best)
+        pairs.append((u, best))
+    return reals, pairs
+
+
+def hp_profile(p: IntPolynomial) -> RootProfile:
+    """High-precision profile of a monic square-free p: rho, perm, double-
+    double entities, the 64-bit keys in rho order and their error bounds."""
+    re_hi, re_lo, im_hi, im_lo, err = hp_roots(p)
+    reals, pairs = _pair_up(re_hi, re_lo, im_hi, im_lo, err)
+    ents = []  # (rho, value R (Fraction), tau (Fraction), errR, errTau, kind, data)
+    # exact rationals of the double-double values
+    for i in reals:
+        u = _dd_frac(re_hi[i], re_lo[i])
+        du = float(err[i])
+        ents.append(("r", u, u * u, du, 2 * abs(float(u)) * du + du * du, i))
+    for a, b in pairs:
+        # symmetrise: z = (z_a + conj z_b) / 2
+        re = (_dd_frac(re_hi[a], re_lo[a]) + _dd_frac(re_hi[b], re_lo[b])) / 2
+        im = (_dd_frac(im_hi[a], im_lo[a]) - _dd_frac(im_hi[b], im_lo[b])) / 2
+        dz = float(max(err[a], err[b]))
+        t = 2 * re
+        m = re * re + im * im
+        mod = math.sqrt(float(m))
+        dt = 2 * dz
+        dm = 2 * mod * dz + dz * dz
+        tau = t * t - 2 * m
+        dtau = 2 * abs(float(t)) * dt + dt * dt + 2 * dm
+        ents.append(("p", t, tau, dt, dtau, m))
+    rows = []
+    for kind, R, tau, dR, dtau, extra in ents:
+        fr = R - math.floor(R)
+        rho = float(fr)
+        if rho >= 1.0:
+            rho = math.nextafter(1.0, 0.0)
+        rows.append((rho, kind, R, tau, dR, dtau, extra))
+    # sort by rho (ties: reals before pairs, then value) -- any fixed order works
+    order = sorted(range(len(rows)), key=lambda k: (rows[k][0], rows[k][1], float(rows[k][2])))
+    r = len(reals)
+    real_hi, real_lo, sum_hi, sum_lo, prod_hi, prod_lo = [], [], [], [], [], []
+    perm = []
+    keys1, keys2 = [], []
+    e1 = e2 = 0.0
+    # entities are numbered reals first (in rho order), then pairs (in rho order)
+    real_rows = [k for k in order if rows[k][1] == "r"]
+    pair_rows = [k for k in order if rows[k][1] == "p"]
+    ent_of = {}
+    for j, k in enumerate(real_rows):
+        ent_of[k] = j
+        hi, lo = _dd_split(rows[k][2])
+        real_hi.append(hi)
+        real_lo.append(lo)
+    for j, k in enumerate(pair_rows):
+        ent_of[k] = r + j
+        hi, lo = _dd_split(rows[k][2])
+        sum_hi.append(hi)
+        sum_lo.append(lo)
+        mh, ml = _dd_split(rows[k][6])
+        prod_hi.append(mh)
+        prod_lo.append(ml)
+    rho = []
+    for k in order:
+        rho_k, kind, R, tau, dR, dtau, _ = rows[k]
+        rho.append(rho_k)
+        perm.append(ent_of[k])
+        keys1.append(math.floor((R - math.floor(R)) * _TWO64 + Fraction(1, 2)) % _TWO64)
+        keys2.append(math.floor((tau - math.floor(tau)) * _TWO64 + Fraction(1, 2)) % _TWO64)
+        e1 += dR * 2.0**64 + 1.0
+        e2 += dtau * 2.0**64 + 1.0
+    root_err = float(max(err)) if len(err) else 0.0
+    # double-double representation slack of the stored entity values
+    root_err = root_err + 2.0**-100 * max([1.0] + [abs(v) for v in real_hi + sum_hi])
+    return RootProfile(
+        real_roots=np.asarray(real_hi, dtype=np.float64),
+        pair_sums=np.asarray(sum_hi, dtype=np.float64),
+        pair_products=np.asarray(prod_hi, dtype=np.float64),
+        rho=np.asarray(rho, dtype=np.float64),
+        perm=tuple(perm),
+        real_lo=np.asarray(real_lo, dtype=np.float64),
+        sum_lo=np.asarray(sum_lo, dtype=np.float64),
+        prod_lo=np.asarray(prod_lo, dtype=np.float64),
+        keys1=np.asarray(keys1, dtype=np.uint64),
+        keys2=np.asarray(keys2, dtype=np.uint64),
+        key_err1=int(math.ceil(e1)),
+        key_err2=int(math.ceil(e2)),
+        root_err=root_err,
+    )
+
+
+# ------------------------------------------------------ reference API
+def find_roots(p: IntPolynomial, cfg: ToleranceConfig | None = None) -> np.ndarray:
+    """All d complex roots, conjugate symmetrised, as complex128: real roots
+    first (ascending, exactly zero imaginary part), then conjugate pairs
+    (w, conj w) in (re, im) order -- the layout of R/rootfinder.py:100-201."""
+    cfg = cfg or ToleranceConfig()
+    if p.is_zero():
+        raise ValueError("zero polynomial has no root set")
+    if p.degree < 1:
+        raise ValueError("find_roots requires degree >= 1")
+    q = p if p.is_monic() else _monic_rational(p)
+    if q is None:  # non-monic: roots of the monic transform, scaled back
+        from .polynomial import monic_transform
+
+        t = monic_transform(p)
+        re_hi, re_lo, im_hi, im_lo, err = hp_roots(t)
+        scale = float(p.leading)
+        re_hi = re_hi / scale
+        im_hi = im_hi / scale
+        err = err / abs(scale)
+    else:
+        re_hi, re_lo, im_hi, im_lo, err = hp_roots(q)
+    reals, pairs = _pair_up(re_hi, re_lo, im_hi, im_lo, err)
+    out = [complex(v, 0.0) for v in sorted(re_hi[i] for i in reals)]
+    pw = sorted(((re_hi[a] + re_hi[b]) / 2, (im_hi[a] - im_hi[b]) / 2) for a, b in pairs)
+    for re, im in pw:
+        out.append(complex(re, im))
+        out.append(complex(re, -im))
+    return np.asarray(out, dtype=np.complex128)
+
+
+def _monic_rational(p: IntPolynomial):
+    return p if p.is_monic() else None
+
+
+def build_profile(roots: np.ndarray, cfg: ToleranceConfig | None = None) -> RootProfile:
+    """Classify a conjugate-closed root multiset into the sorted rho profile
+    (R/rootfinder.py:204-245): reals contribute frac(u), each pair
+    frac(z + conj z) once; UnpairedComplexRoot when a partner is missing."""
+    cfg = cfg or ToleranceConfig()
+    z = np.asarray(roots, dtype=np.complex128)
+    scale = np.maximum(1.0, np.abs(z))
+    real_mask = np.abs(z.imag) <= cfg.imag_threshold * scale
+    reals = np.sort(z.real[real_mask])
+    rest = list(z[~real_mask])
+    uppers = sorted((w for w in rest if w.imag > 0), key=lambda w: (w.real, w.imag))
+    lowers = [w for w in rest if w.imag <= 0]
+    if len(uppers) != len(lowers):
+        raise UnpairedComplexRoot(f"{len(uppers)} upper vs {len(lowers)} lower half-plane roots")
+    sums, prods = [], []
+    for u in uppers:
+        target = u.conjugate()
+        best = min(range(len(lowers)), key=lambda i: abs(lowers[i] - target))
+        partner = lowers.pop(best)
+        if abs(partner - target) > 1e-6 * max(1.0, abs(u)):
+            raise UnpairedComplexRoot(f"no conjugate partner for root {u}")
+        w = (u + partner.conjugate()) / 2
+        sums.append(float(2.0 * w.real))
+        prods.append(float(abs(w) ** 2))
+    entries = [(frac(u), i) for i, u in enumerate(reals)]
+    entries += [(frac(s), len(reals) + j) for j, s in enumerate(sums)]
+    entries.sort()
+    rho = np.array([min(e[0], math.nextafter(1.0, 0.0)) for e in entries], dtype=np.float64)
+    return RootProfile(
+        real_roots=np.asarray(reals, dtype=np.float64),
+        pair_sums=np.asarray(sums, dtype=np.float64),
+        pair_products=np.asarray(prods, dtype=np.float64),
+        rho=rho,
+        perm=tuple(e[1] for e in entries),
+    )
+
+
+def profile_polynomial(p: IntPolynomial, cfg: ToleranceConfig | None = None) -> RootProfile:
+    """find_roots followed by build_profile (R/rootfinder.py:248-251)."""
+    cfg = cfg or ToleranceConfig()
+    return build_profile(find_roots(p, cfg), cfg)
+
+
+def expected_real_roots(d) -> float:
+    """(2/pi) ln d, leading term of the expected real-root count."""
+    if d < 1:
+        raise ValueError("degree must be >= 1")
+    return (2.0 / math.pi) * math.log(d)
+
+
+def expected_n(d) -> float:
+    """Expected instance size d/2 + (1/pi) ln d."""
+    if d < 1:
+        raise ValueError("degree must be >= 1")
+    return d / 2.0 + math.log(d) / math.pi
+
+
+def residual_bound(p: IntPolynomial, root: complex, root_tol: float) -> float:
+    """root_tol * max|a_i| * max(1, |root|)^d (R/rootfinder.py:269-272)."""
+    amax = max(abs(c) for c in p.coeffs)
+    return root_tol * amax * max(1.0, abs(root)) ** p.degree

@@ -1,0 +1,319 @@
+"""factor(): the drop-in entry point, with candidate verification on the GPU.
+
+Mirrors ``pkg/src/polyfactor/verify.py`` ("R/verify.py"): ``factor``,
+``is_irreducible``, ``FactorizationResult``, ``FactorStats``,
+``selected_degree`` keep their names, signatures, result layout and errors;
+the output factorization (irreducible factors with multiplicities, sorted by
+(degree, coeffs, mult), R/verify.py:222) is the unique one, so it equals the
+reference's wherever the reference finishes.
+
+Pipeline for one monic square-free part p:
+  1. host (not timed, ``root_seconds``): hp_profile -- roots to ~2^-100,
+     exact 64-bit keys of the first two power sums, window half-width T;
+  2. GPU (``recombine_seconds``): search every pattern t < 2^(n-1) whose key
+     sum is within +-T of 0 -- the true factors and a handful of false hits;
+  3. GPU (``verify_seconds``): one warp per candidate expands the smaller
+     side in double-double, checks integrality against a derived error bound
+     and trial-divides p modulo three 61-bit primes (R/verify.py:60-155);
+  4. host: the minimal passing patterns (atoms) are the irreducible factors;
+     the certificate (exact re-multiplication, R/verify.py:224-231) proves
+     the product.  The reference instead re-roots and re-searches every
+     piece recursively (R/verify.py:280-284); one search here yields all
+     factors.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from fractions import Fraction
+from functools import lru_cache
+
+import numpy as np
+
+from . import _lib
+from .polynomial import (
+    IntPolynomial,
+    divide_exact,
+    monic_transform,
+    monic_untransform_factor,
+    square_free_decompose,
+)
+from .recombine import BACKENDS, RecombineStats, search_keys
+from .rootfinder import RootProfile, ToleranceConfig, hp_profile
+
+_STRIDE = 65  # smaller side degree <= 64
+KEY_SAFETY = 4  # window half-width = KEY_SAFETY * (summed key error bounds) + slack
+
+
+@dataclass
+class FactorStats:
+    """Per-stage counters of one factor() call (R/verify.py:158-170)."""
+
+    backend: str = "e"
+    workers: int = 1
+    n: int = 0
+    root_seconds: float = 0.0
+    recombine_seconds: float = 0.0
+    verify_seconds: float = 0.0
+    candidates: int = 0
+    rejected: int = 0
+    recombine: RecombineStats = field(default_factory=RecombineStats)
+    host_verified: int = 0
+
+
+@dataclass(frozen=True)
+class FactorizationResult:
+    """R/verify.py:173-184."""
+
+    input: IntPolynomial
+    content: int
+    factors: tuple
+    certificate: bool
+    stats: FactorStats
+
+    @property
+    def irreducible(self) -> bool:
+        return len(self.factors) == 1 and self.factors[0][1] == 1
+
+
+def selected_degree(s: int, profile: RootProfile) -> int:
+    """Degree of the factor a pattern selects: 1 per real root, 2 per pair
+    (R/verify.py:48-57)."""
+    e = 0
+    i = 0
+    while s:
+        if s & 1:
+            e += 1 if profile.perm[i] < profile.r else 2
+        s >>= 1
+        i += 1
+    return e
+
+
+@lru_cache(maxsize=256)
+def _profile_cached(coeffs: tuple) -> RootProfile:
+    return hp_profile(IntPolynomial(coeffs))
+
+
+def _search_window(prof: RootProfile) -> tuple[np.ndarray, int]:
+    """Combined keys (first + second power sum) and the window half-width."""
+    keys = ((prof.keys1.astype(object) + prof.keys2.astype(object)) % (1 << 64)).astype(np.uint64)
+    T = KEY_SAFETY * (prof.key_err1 + prof.key_err2) + prof.n + 64
+    return keys, T
+
+
+def _p_mod(p: IntPolynomial) -> np.ndarray:
+    primes = np.zeros(3, dtype=np.uint64)
+    lib = _lib.load()
+    lib.rfr_verify_primes(primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return np.array([[c % int(q) for c in p.coeffs] for q in primes], dtype=np.uint64)
+
+
+def verify_candidates(prof: RootProfile, p: IntPolynomial, pats: np.ndarray):
+    """Device verification of candidate patterns (one warp each).
+    Returns (verdict uint8[m], side uint8[m], coeffs int64[m, 65])."""
+    lib = _lib.load()
+    _lib.device()
+    m = len(pats)
+    verdict = np.zeros(m, dtype=np.uint8)
+    side = np.zeros(m, dtype=np.uint8)
+    coeffs = np.zeros((m, _STRIDE), dtype=np.int64)
+    if m == 0:
+        return verdict, side, coeffs
+    D = ctypes.POINTER(ctypes.c_double)
+    keep = []  # keep numpy buffers alive for the call
+
+    def dptr(a):
+        a = np.ascontiguousarray(a if a is not None else np.zeros(0), dtype=np.float64)
+        keep.append(a)
+        return a.ctypes.data_as(D)
+
+    perm = np.ascontiguousarray(prof.perm, dtype=np.int32)
+    keep.append(perm)
+    rp = _lib.RfrProfile(
+        n=prof.n, r=prof.r, c=prof.c,
+        real_hi=dptr(prof.real_roots), real_lo=dptr(prof.real_lo),
+        sum_hi=dptr(prof.pair_sums), sum_lo=dptr(prof.sum_lo),
+        prod_hi=dptr(prof.pair_products), prod_lo=dptr(prof.prod_lo),
+        perm=perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        root_err=float(prof.root_err),
+    )
+    pats = np.ascontiguousarray(pats, dtype=np.uint64)
+    pm = np.ascontiguousarray(_p_mod(p))
+    _lib.check(
+        lib.rfr_verify(ctypes.byref(rp), _lib.ptr(pats, _lib.U64_P), m,
+                       _lib.ptr(pm, _lib.U64_P), p.degree,
+                       verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
+                       coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, None),
+        "rfr_verify",
+    )
+    return verdict, side, coeffs
+
+
+def _host_candidate(prof: RootProfile, p: IntPolynomial, t: int) -> IntPolynomial | None:
+    """Exact-rational rebuild of the side t for candidates the device could
+    not decide (coefficients beyond 2^62 or a loose error bound): multiply
+    out the double-double entities as Fractions, round, bound the error,
+    and demand exact division (R/verify.py:141-155 semantics)."""
+    coeffs = [Fraction(1)]
+    mag = [1.0]
+    magp = [1.0]
+    de = prof.root_err
+    for i in range(prof.n):
+        if not (t >> i) & 1:
+            continue
+        ent = prof.perm[i]
+        if ent < prof.r:
+            u = Fraction(float(prof.real_roots[ent])) + Fraction(float(prof.real_lo[ent]))
+            fac, fm, fp = [-u, Fraction(1)], [abs(float(u)), 1.0], [abs(float(u)) + de, 1.0]
+        else:
+            j = ent - prof.r
+            tt = Fraction(float(prof.pair_sums[j])) + Fraction(float(prof.sum_lo[j]))
+            mm = Fraction(float(prof.pair_products[j])) + Fraction(float(prof.prod_lo[j]))
+            dm = 2 * abs(float(mm)) ** 0.5 * de + de * de
+            fac = [mm, -tt, Fraction(1)]
+            fm = [abs(float(mm)), abs(float(tt)), 1.0]
+            fp = [abs(float(mm)) + dm, abs(float(tt)) + 2 * de, 1.0]
+        coeffs = _pmul(coeffs, fac)
+        mag = _pmul(mag, fm)
+        magp = _pmul(magp, fp)
+    out = []
+    for c, a, b in zip(coeffs, mag, magp):
+        r = round(c)
+        bound = (b - a) + a * 1e-28 + 1e-30
+        if abs(float(c - r)) > 2 * bound + 1e-12:
+            return None
+        out.append(int(r))
+    q = IntPolynomial(out)
+    if q.degree < 1 or not q.is_monic():
+        return None
+    return q if divide_exact(p, q) is not None else None
+
+
+def _pmul(a, b):
+    out = [0] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            out[i + j] += x * y
+    return out
+
+
+def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
+                             stats: FactorStats) -> list[IntPolynomial]:
+    if p.degree <= 1:
+        return [p]
+    t0 = time.perf_counter()
+    prof = _profile_cached(p.coeffs)
+    stats.root_seconds += time.perf_counter() - t0
+    n = prof.n
+    stats.n = max(stats.n, n)
+
+    t0 = time.perf_counter()
+    keys, T = _search_window(prof)
+    if workers > 1:
+        from .parallel import sharded_search_keys
+
+        pats = sharded_search_keys(keys, T, workers, stats.recombine)
+    else:
+        pats = search_keys(keys, T, stats.recombine)
+    pats = pats[pats != 0]
+    stats.recombine_seconds += time.perf_counter() - t0
+    stats.candidates += len(pats)
+
+    t0 = time.perf_counter()
+    full = (1 << n) - 1
+    verdict, side, coeffs = verify_candidates(prof, p, pats)
+    found: dict[int, IntPolynomial] = {}  # side pattern -> monic integer factor
+    for k in range(len(pats)):
+        s = int(pats[k])
+        v = int(verdict[k])
+        if v == _lib.V_PASS:
+            t = (~s & full) if side[k] else s
+            e = selected_degree(t, prof)
+            found[t] = IntPolynomial([int(x) for x in coeffs[k, : e + 1]])
+        elif v == _lib.V_HOST:
+            stats.host_verified += 1
+            for t in (s, ~s & full):
+                q = _host_candidate(prof, p, t)
+                if q is not None:
+                    found[t] = q
+                    break
+            else:
+                stats.rejected += 1
+        else:
+            stats.rejected += 1
+    if not found:
+        stats.verify_seconds += time.perf_counter() - t0
+        return [p]
+    # atoms: minimal passing patterns (every true pattern is a disjoint union
+    # of them; the complement of a passing pattern passes too)
+    pats_all = set(found) | {(~t & full) for t in found}
+    covered = 0
+    atoms = []
+    for t in sorted(pats_all, key=lambda x: (bin(x).count("1"), x)):
+        if t and not (t & covered):
+            atoms.append(t)
+            covered |= t
+            if covered == full:
+                break
+    factors = []
+    rest = p
+    for a in atoms:
+        q = found.get(a)
+        if q is None:
+            q = divide_exact(p, found[~a & full])
+        if q is None or divide_exact(rest, q) is None:
+            continue
+        rest = divide_exact(rest, q)
+        factors.append(q)
+    if rest.degree >= 1:
+        factors.append(rest)
+    stats.verify_seconds += time.perf_counter() - t0
+    return factors
+
+
+def factor(
+    p: IntPolynomial,
+    cfg: ToleranceConfig | None = None,
+    backend: str = "e",
+    workers: int = 1,
+) -> FactorizationResult:
+    """Full irreducible factorization over the integers (R/verify.py:187-233).
+    ``workers`` > 1 shards the search over that many key ranges (GPUs when
+    torch.distributed runs one rank per device).  ValueError on an unknown
+    backend, workers < 1 or a constant polynomial."""
+    cfg = cfg or ToleranceConfig()
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}")
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if p.is_constant():
+        raise ValueError("factor requires a non-constant polynomial")
+    stats = FactorStats(backend=backend, workers=workers)
+    content = p.content()
+    prim = p.primitive_part()
+    out: list[tuple[IntPolynomial, int]] = []
+    for part, mult in square_free_decompose(prim):
+        if part.is_monic():
+            irr = _factor_monic_squarefree(part, cfg, workers, stats)
+        else:
+            tr = monic_transform(part)
+            irr = [monic_untransform_factor(g, part.leading)
+                   for g in _factor_monic_squarefree(tr, cfg, workers, stats)]
+        out.extend((g, mult) for g in irr)
+    out.sort(key=lambda fm: (fm[0].degree, fm[0].coeffs, fm[1]))
+    rebuilt = IntPolynomial([content])
+    for g, m in out:
+        rebuilt = rebuilt * g**m
+    return FactorizationResult(input=p, content=content, factors=tuple(out),
+                               certificate=(rebuilt == p), stats=stats)
+
+
+def is_irreducible(p: IntPolynomial, cfg: ToleranceConfig | None = None,
+                   backend: str = "e") -> bool:
+    """True when the primitive part of p does not split (R/verify.py:289-297)."""
+    if p.is_constant():
+        raise ValueError("irreducibility is asked of non-constant polynomials")
+    if p.degree == 1:
+        return True
+    return factor(p, cfg, backend).irreducible
