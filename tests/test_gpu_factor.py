@@ -1,0 +1,135 @@
+"""GPU parity of factor(): the same irreducible factorizations (factors,
+multiplicities, content, canonical order) as the reference on its own
+inputs (tests/golden/factor_cases.json from pkg/src/polyfactor/verify.py:
+187-233), the d = 100 benchmark inputs (C3, factors by construction), the
+d = 120 irreducible inputs (C4) and Swinnerton-Dyer f6 (C5)."""
+import random
+
+import numpy as np
+import pytest
+
+from conftest import poly_of, rho_of
+from paper_2410_15880_b200 import IntPolynomial as P
+from paper_2410_15880_b200 import RootProfile, factor, is_irreducible, verify_candidates
+from paper_2410_15880_b200 import _lib
+from paper_2410_15880_b200.errors import WidthExceeded
+
+pytestmark = pytest.mark.gpu
+
+
+def _want(c):
+    return [([int(x) for x in f], m) for f, m in c["factors"]]
+
+
+def _got(res):
+    return [(list(g.coeffs), m) for g, m in res.factors]
+
+
+def test_factor_matches_reference_on_all_golden_inputs(factor_cases):
+    for c in factor_cases:
+        res = factor(poly_of(c["input"]))
+        assert _got(res) == _want(c), c["tag"]
+        assert str(res.content) == c["content"] and res.certificate, c["tag"]
+        assert res.irreducible == c["irreducible"]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_factor_degree_100_benchmark_inputs(big_inputs, seed):
+    c = big_inputs["c3"][seed]
+    res = factor(poly_of(c["p"]))
+    assert _got(res) == _want(c) and res.certificate
+    assert res.stats.n == c["n_ref"]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_factor_degree_120_irreducible(big_inputs, seed):
+    c = big_inputs["c4"][seed]
+    res = factor(poly_of(c["p"]))
+    assert res.irreducible and res.certificate and _got(res) == _want(c)
+    assert res.stats.candidates == res.stats.rejected
+
+
+def test_factor_swinnerton_dyer_f6_irreducible(big_inputs):
+    c = big_inputs["c5"][0]
+    res = factor(poly_of(c["p"]))
+    assert res.irreducible and res.certificate
+    assert res.stats.n == 64
+
+
+def test_swinnerton_dyer_small_irreducible():
+    from paper_2410_15880_b200 import gen_swinnerton_dyer
+
+    for k in (2, 3, 4, 5):
+        res = factor(gen_swinnerton_dyer(k))
+        assert res.irreducible and res.certificate
+        assert res.stats.rejected == res.stats.candidates
+
+
+def test_factor_errors():
+    with pytest.raises(ValueError):
+        factor(P([5]))
+    with pytest.raises(ValueError):
+        factor(P([1, 1]), backend="z")
+    with pytest.raises(ValueError):
+        factor(P([1, 1]), workers=0)
+    rng = random.Random(0)
+    big = P([rng.randint(-3, 3) for _ in range(131)] + [1])
+    with pytest.raises(WidthExceeded):
+        factor(big)
+    with pytest.raises(ValueError):
+        is_irreducible(P([3]))
+    assert is_irreducible(P([7, 1])) and not is_irreducible(P([-1, 0, 1]))
+
+
+def test_factor_workers_shard_the_search(factor_cases):
+    for c in factor_cases[:30]:
+        p = poly_of(c["input"])
+        assert _got(factor(p, workers=3)) == _want(c), c["tag"]
+
+
+def test_factor_round_trips_random_products():
+    from paper_2410_15880_b200 import multiply
+
+    rng = random.Random(31)
+    for _ in range(12):
+        fs = [P([rng.randint(-30, 30) for _ in range(rng.randint(1, 9))] + [1]) for _ in range(rng.randint(2, 4))]
+        p = fs[0]
+        for f in fs[1:]:
+            p = multiply(p, f)
+        res = factor(p)
+        assert res.certificate
+        rebuilt = P([res.content])
+        for g, m in res.factors:
+            rebuilt = rebuilt * g**m
+        assert rebuilt == p
+
+
+def test_device_verification_agrees_with_reference_verdicts(verify_cases):
+    """Reference profiles (float64 roots) through the device verifier: every
+    candidate the reference accepted passes with the same integer factor, no
+    candidate the reference rejected passes."""
+    for vc in verify_cases:
+        prof = RootProfile(
+            real_roots=np.array(rho_of({"rho": vc["real_roots"]})),
+            pair_sums=np.array(rho_of({"rho": vc["pair_sums"]})),
+            pair_products=np.array(rho_of({"rho": vc["pair_products"]})),
+            rho=np.array(rho_of(vc)),
+            perm=tuple(vc["perm"]),
+            real_lo=np.zeros(len(vc["real_roots"])),
+            sum_lo=np.zeros(len(vc["pair_sums"])),
+            prod_lo=np.zeros(len(vc["pair_products"])),
+            root_err=1e-12,
+        )
+        p = poly_of(vc["p"])
+        pats = np.array([row["pattern"] for row in vc["candidates"]], dtype=np.uint64)
+        verdict, side, coeffs = verify_candidates(prof, p, pats)
+        full = (1 << prof.n) - 1
+        accepted = {row["pattern"]: row["q"] for row in vc["candidates"] if row["q"] is not None}
+        for k, row in enumerate(vc["candidates"]):
+            s = row["pattern"]
+            expect = s in accepted or (~s & full) in accepted
+            assert (verdict[k] == _lib.V_PASS) == expect, (vc["tag"], s, int(verdict[k]))
+            if expect:
+                t = (~s & full) if side[k] else s
+                q = accepted[t]
+                assert [int(x) for x in coeffs[k, : len(q)]] == [int(x) for x in q]

@@ -1,0 +1,110 @@
+"""Host preprocessing: high-precision roots, profile layout, the exact keys
+and the completeness of the key window on the benchmark inputs (CPU)."""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from conftest import poly_of
+from paper_2410_15880_b200 import IntPolynomial as P
+from paper_2410_15880_b200 import ToleranceConfig, build_profile, find_roots, hp_profile
+from paper_2410_15880_b200.rootfinder import frac, hp_roots
+from paper_2410_15880_b200.verify import KEY_SAFETY, _search_window
+
+TWO64 = 1 << 64
+
+
+def test_tolerance_config_validation():
+    with pytest.raises(ValueError):
+        ToleranceConfig(eps=0.0)
+    with pytest.raises(ValueError):
+        ToleranceConfig(eps=0.5)
+    with pytest.raises(ValueError):
+        ToleranceConfig(precision="quad")
+    assert ToleranceConfig().eps == 1e-6
+
+
+def test_frac_convention():
+    assert frac(-0.25) == 0.75 and frac(2.5) == 0.5
+
+
+def test_find_roots_layout():
+    z = find_roots(P([-2, 0, -1, 0, 1]))  # (x^2-2)(x^2+1)
+    assert np.allclose(z[:2].real, [-math.sqrt(2), math.sqrt(2)])
+    assert np.all(z[:2].imag == 0)
+    assert np.allclose(z[2:], [1j, -1j])
+
+
+def test_build_profile_kats():
+    prof = build_profile(np.array([0.5 + 0j, -0.25 + 0j, 1 + 1j, 1 - 1j]))
+    assert prof.r == 2 and prof.c == 1
+    assert prof.rho.tolist() == [0.0, 0.5, 0.75]
+    assert prof.pair_sums.tolist() == [2.0] and prof.pair_products.tolist() == pytest.approx([2.0])
+
+
+def test_hp_roots_precision_against_exact_values():
+    re_hi, re_lo, im_hi, im_lo, err = hp_roots(P([-2, 0, -1, 0, 1]))
+    for i in range(4):
+        if im_hi[i] == 0:
+            r = Fraction(re_hi[i]) + Fraction(re_lo[i])
+            assert abs(r * r - 2) < Fraction(1, 10**28)
+        else:
+            assert abs(abs(im_hi[i]) - 1) < 1e-28
+    assert err.max() < 1e-28
+
+
+def test_hp_profile_entities_and_keys():
+    prof = hp_profile(P([-2, 0, -1, 0, 1]))
+    assert prof.n == 3 and prof.r == 2 and prof.c == 1
+    # pair x^2 + 1: t = 0, m = 1 -> keys 0 and frac(t^2 - 2m) = 0
+    j = prof.perm.index(2)
+    assert int(prof.keys1[j]) in (0,) and int(prof.keys2[j]) == 0
+    # the two real roots +-sqrt(2): Tr1 = 0, Tr2 = 4 -> key sums vanish
+    ks = [i for i in range(3) if prof.perm[i] < 2]
+    s1 = sum(int(prof.keys1[i]) for i in ks) % TWO64
+    s2 = sum(int(prof.keys2[i]) for i in ks) % TWO64
+    assert min(s1, TWO64 - s1) <= prof.key_err1 and min(s2, TWO64 - s2) <= prof.key_err2
+
+
+def _factor_pattern(prof, root_values, f):
+    """rho-index pattern of the entities whose roots are roots of f."""
+    pat = 0
+    for i, ent in enumerate(prof.perm):
+        if ent < prof.r:
+            u = float(prof.real_roots[ent])
+            if abs(f.evaluate(u)) < 1e-6 * max(1.0, abs(u)) ** f.degree * 1e3:
+                pat |= 1 << i
+        else:
+            t = float(prof.pair_sums[ent - prof.r])
+            m = float(prof.pair_products[ent - prof.r])
+            # the pair is a factor of f iff f(z) ~ 0 for z = t/2 + i sqrt(m - t^2/4)
+            z = complex(t / 2, math.sqrt(max(m - t * t / 4, 0.0)))
+            if abs(f.evaluate(z)) < 1e-6 * max(1.0, abs(z)) ** f.degree * 1e3:
+                pat |= 1 << i
+    return pat
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_true_factor_keys_fall_inside_the_window_c3(big_inputs, seed):
+    case = big_inputs["c3"][seed]
+    p = poly_of(case["p"])
+    f = poly_of(case["factors"][0][0])
+    prof = hp_profile(p)
+    keys, T = _search_window(prof)
+    pat = _factor_pattern(prof, None, f)
+    full = (1 << prof.n) - 1
+    from paper_2410_15880_b200.verify import selected_degree
+
+    assert selected_degree(pat, prof) == f.degree
+    for t in (pat, pat ^ full):
+        s = sum(int(keys[i]) for i in range(prof.n) if (t >> i) & 1) % TWO64
+        assert min(s, TWO64 - s) <= T // KEY_SAFETY, (seed, s)
+    assert T < 1 << 12  # ~n rounding units: false hits ~ 2^(n-1) * 2T / 2^64
+
+
+def test_hp_profile_c4_and_sd6_certified(big_inputs):
+    prof = hp_profile(poly_of(big_inputs["c4"][0]["p"]))
+    assert prof.n == 63 and prof.root_err < 1e-20
+    sd6 = hp_profile(poly_of(big_inputs["c5"][0]["p"]))  # multiprecision path
+    assert sd6.n == 64 and sd6.r == 64 and sd6.root_err < 1e-20
