@@ -61,6 +61,7 @@ typedef struct rfr_stats {
   double ms_join;         /* device time: bucket join                               */
   double ms_post;         /* device time: recheck / verification                    */
   double ms_total;        /* device time of the whole call                          */
+  int64_t launches;       /* kernels launched by the call                            */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */

@@ -120,6 +120,8 @@ def lib():
         d_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, u64_p,
         ctypes.c_int64, i64_p,
     ]
+    L.orc_num_threads.restype = ctypes.c_int
+    L.orc_set_threads.argtypes = [ctypes.c_int]
     L.orc_divide_exact_i128.restype = ctypes.c_int
     L.orc_divide_exact_i128.argtypes = [i64_p, ctypes.c_int, i64_p, ctypes.c_int, i64_p]
     _LIB = L
@@ -172,7 +174,7 @@ def c_recombine_e_port(vals, eps: float, q_lo: int = 0, q_hi: int | None = None)
     na = n // 2
     if q_hi is None:
         q_hi = 1 << na
-    st = np.zeros(4, dtype=np.int64)
+    st = np.zeros(6, dtype=np.int64)
     cap = 1 << 16
     while True:
         out = np.zeros(cap, dtype=np.uint64)
@@ -184,7 +186,8 @@ def c_recombine_e_port(vals, eps: float, q_lo: int = 0, q_hi: int | None = None)
             raise RuntimeError("orc_recombine_e_port: allocation failure")
         if cnt <= cap:
             stats = dict(inserts=int(st[0]), insert_probes=int(st[1]),
-                         queries=int(st[2]), query_probes=int(st[3]))
+                         queries=int(st[2]), query_probes=int(st[3]),
+                         splat_s=st[4] * 1e-9, query_s=st[5] * 1e-9)
             return out[:cnt].copy(), stats
         cap = max(cap * 4, int(cnt))
 

@@ -34,6 +34,15 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <pthread.h>
+#include <time.h>
+#include <unistd.h>
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
 
 #define GUARD 1e-12 /* R/recombine.py:28-30 */
 
@@ -195,38 +204,85 @@ static double pymod1(double x) { /* Python's float % 1.0 for the values used */
     return r;
 }
 
-/* _stream_merged_raw (:328-358) over the A-half values xs[lo..hi). */
+/* _stream_merged_raw (:328-358) over the A-half values xs[lo..hi).  The
+ * query loop is read-only over the table, so it runs on all host threads
+ * (the partitioned query sweep of R/parallel.py:195-252); hits are appended
+ * with an atomic cursor. */
+typedef struct {
+  const double *xs, *merged;
+  int64_t lo_q, hi_q, k, cap;
+  int na;
+  double eps;
+  uint64_t *out;
+  int64_t *nout;
+  int64_t probes;
+} stream_job;
+
+static void *stream_worker(void *arg) {
+  stream_job *J = (stream_job *)arg;
+  const int64_t k = J->k;
+  int64_t probes = 0;
+  for (int64_t s_a = J->lo_q; s_a < J->hi_q; s_a++) {
+    double t = pymod1(1.0 - J->xs[s_a]);
+    double lo = pymod1(t - J->eps);
+    int64_t start = (int64_t)(k * lo);
+    if (start >= k) start -= k; /* lo == 1.0 would index past the table */
+    int64_t span = ((int64_t)(k * pymod1(t + J->eps)) - start) % k;
+    if (span < 0) span += k;
+    int64_t i = start, off = 0;
+    while (off <= k) {
+      double v = J->merged[2 * i];
+      probes++;
+      if (v < 0.0) {
+        if (off >= span) break;
+      } else {
+        double delta = pymod1(v - t);
+        if (delta < J->eps || delta > 1.0 - J->eps) {
+          int64_t slot = __atomic_fetch_add(J->nout, 1, __ATOMIC_RELAXED);
+          if (slot < J->cap) J->out[slot] = (uint64_t)s_a | ((uint64_t)J->merged[2 * i + 1] << J->na);
+        }
+      }
+      off++;
+      i++;
+      if (i == k) i = 0;
+    }
+  }
+  J->probes = probes;
+  return NULL;
+}
+
+static int g_threads = 0; /* 0 = all online cores */
+
+int orc_num_threads(void) {
+  long c = sysconf(_SC_NPROCESSORS_ONLN);
+  if (g_threads > 0) return g_threads;
+  return c > 0 ? (int)c : 1;
+}
+
+void orc_set_threads(int t) { g_threads = t; }
+
 static int64_t stream_merged(const double *xs, int64_t lo_q, int64_t hi_q, const double *merged,
                              int64_t k, int na, double eps, uint64_t *out, int64_t cap,
                              int64_t *probes_out) {
-    int64_t probes = 0, nout = 0;
-    for (int64_t s_a = lo_q; s_a < hi_q; s_a++) {
-        double t = pymod1(1.0 - xs[s_a]);
-        double lo = pymod1(t - eps);
-        int64_t start = (int64_t)(k * lo);
-        if (start >= k) start -= k; /* lo == 1.0 would index past the table */
-        int64_t span = ((int64_t)(k * pymod1(t + eps)) - start) % k;
-        if (span < 0) span += k;
-        int64_t i = start, off = 0;
-        while (off <= k) {
-            double v = merged[2 * i];
-            probes++;
-            if (v < 0.0) {
-                if (off >= span) break;
-            } else {
-                double delta = pymod1(v - t);
-                if (delta < eps || delta > 1.0 - eps) {
-                    if (nout < cap) out[nout] = (uint64_t)s_a | ((uint64_t)merged[2 * i + 1] << na);
-                    nout++;
-                }
-            }
-            off++;
-            i++;
-            if (i == k) i = 0;
-        }
-    }
-    *probes_out = probes;
-    return nout;
+  int T = orc_num_threads();
+  if (T > 256) T = 256;
+  if (hi_q - lo_q < 4096) T = 1;
+  pthread_t th[256];
+  stream_job jobs[256];
+  int64_t nout = 0;
+  for (int w = 0; w < T; w++) {
+    jobs[w] = (stream_job){xs, merged, lo_q + (hi_q - lo_q) * w / T, lo_q + (hi_q - lo_q) * (w + 1) / T,
+                           k, cap, na, eps, out, &nout, 0};
+    if (T == 1) stream_worker(&jobs[w]);
+    else pthread_create(&th[w], NULL, stream_worker, &jobs[w]);
+  }
+  int64_t probes = 0;
+  for (int w = 0; w < T; w++) {
+    if (T > 1) pthread_join(th[w], NULL);
+    probes += jobs[w].probes;
+  }
+  *probes_out = probes;
+  return nout;
 }
 
 /*
@@ -234,7 +290,8 @@ static int64_t stream_merged(const double *xs, int64_t lo_q, int64_t hi_q, const
  * by the caller on the raw output: builds the splat table of the high half,
  * then streams the A-queries with index in [q_lo, q_hi) (a bounded sample
  * when the caller asks for less than 2^na).  Returns the raw hit count;
- * stats[0..3] = inserts, insert_probes, queries, query_probes.
+ * stats[0..3] = inserts, insert_probes, queries, query_probes,
+ * stats[4..5] = splat and query wall time in nanoseconds.
  * -1: allocation failure.
  */
 int64_t orc_recombine_e_port(const double *rho, int n, double eps, int64_t q_lo, int64_t q_hi,
@@ -259,16 +316,21 @@ int64_t orc_recombine_e_port(const double *rho, int n, double eps, int64_t q_lo,
         return -1;
     }
     for (int64_t i = 0; i < k; i++) merged[2 * i] = -1.0;
+    double t0 = now_s();
     int64_t ip = splat_merged(bsums, nbv, merged, k);
+    double t1 = now_s();
     if (q_hi > nav) q_hi = nav;
     if (q_lo < 0) q_lo = 0;
     int64_t qp = 0;
     int64_t nout = stream_merged(asums, q_lo, q_hi, merged, k, na, eps_d, out, cap, &qp);
+    double t2 = now_s();
     if (stats) {
         stats[0] = nbv;
         stats[1] = ip;
         stats[2] = q_hi - q_lo;
         stats[3] = qp;
+        stats[4] = (int64_t)((t1 - t0) * 1e9);
+        stats[5] = (int64_t)((t2 - t1) * 1e9);
     }
     free(merged);
     free(bsums);

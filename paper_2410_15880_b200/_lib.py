@@ -56,6 +56,7 @@ class RfrStats(ctypes.Structure):
         ("ms_join", ctypes.c_double),
         ("ms_post", ctypes.c_double),
         ("ms_total", ctypes.c_double),
+        ("launches", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -208,9 +208,12 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 // Core search on device-resident keys.  d_out/cap: raw output; d_count: out
 // counter lives in g.ctr (DevCounters.out_count).  Leaves counters on device.
+int g_launches = 0;  // kernels launched by the last search_core call
+
 int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard, int nshards,
                 uint64_t* d_out, unsigned long long cap, cudaStream_t s, int* r_bits,
                 int* nwin, bool time_it) {
+  g_launches = 0;
   std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
   *nwin = (int)wins.size();
   JoinPlan P0;
@@ -221,6 +224,11 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   if (rc) return rc;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
   RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), s));
+  {
+    int maxbits = 0;
+    for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
+    g_launches += 1 + (maxbits > kBaseBits ? maxbits - kBaseBits : 0);
+  }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
   for (auto& w : wins) {
     // every piece reuses the geometry planned for the widest (first) piece
@@ -236,6 +244,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     if (span == 0) continue;
     int grid = (int)(span < (uint64_t)g.nsm ? span : (uint64_t)g.nsm);
     RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
+    g_launches += 1;
   }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
   return RFR_OK;
@@ -256,6 +265,7 @@ void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin
   st->chunks = (int64_t)c.chunks;
   st->r_bits = r_bits;
   st->windows = nwin;
+  st->launches = g_launches;
 }
 
 int check_n(int n) {
@@ -373,6 +383,7 @@ static int run_search_host(const uint64_t* h_keys, const double* h_rho, int n, u
   unsigned long long count = c.out_count;
   if (parity) {
     RFR_CUDA_OK(g.post.ensure((count ? count : 1) * sizeof(uint64_t)));
+    g_launches += 1;
     RFR_CUDA_OK(launch_recheck((const double*)g.rho.p, (const uint64_t*)g.raw.p, &d_ctr->out_count,
                                raw_cap, eps, (uint64_t*)g.post.p,
                                g.post.bytes / sizeof(uint64_t), d_ctr, g.nsm, s));
@@ -546,6 +557,7 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
     memset(st, 0, sizeof *st);
     st->ms_post = ev_ms(g.ev[2], g.ev[3]);
     st->ms_total = st->ms_post;
+    st->launches = 1;
   }
   return RFR_OK;
 }
