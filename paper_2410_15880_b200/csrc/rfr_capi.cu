@@ -111,7 +111,7 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   memset(P, 0, sizeof *P);
   const int m = n - 1;
   const int alpha = (m + 1) / 2, beta = m - alpha;
-  int r = alpha - 12;
+  int r = alpha - 12;  // ~4096 A records per bucket
   if (r < 2) r = 2;
   const uint64_t half = (width >> 1) + (width & 1);
   const int hb = bit_length(half);
@@ -123,7 +123,7 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   static int lam = -1;
   if (lam < 0) {
     const char* e = getenv("RFR_LAMBDA_LOG");
-    lam = e ? atoi(e) : 2;
+    lam = e ? atoi(e) : 3;
   }
   const int ao = clampi(alpha - r - lam, alpha > kMaxInnerBits ? alpha - kMaxInnerBits : 0, kMaxOuterBits);
   const int bo = clampi(beta - r - lam, beta > kMaxInnerBits ? beta - kMaxInnerBits : 0, kMaxOuterBits);
@@ -242,7 +242,8 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     P.bucket_end = nb * (uint64_t)(shard + 1) / (uint64_t)nshards;
     uint64_t span = P.bucket_end - P.bucket_begin;
     if (span == 0) continue;
-    int grid = (int)(span < (uint64_t)g.nsm ? span : (uint64_t)g.nsm);
+    const uint64_t ctas = (uint64_t)g.nsm;  // one join CTA per SM
+    int grid = (int)(span < ctas ? span : ctas);
     RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
     g_launches += 1;
   }

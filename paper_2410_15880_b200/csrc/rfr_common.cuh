@@ -12,7 +12,7 @@ namespace rfr {
 // Largest quarter list walked by the join (2^23 entries = 64 MB of keys).
 constexpr int kMaxInnerBits = 23;
 // Outer lists live in shared memory of the join kernel.
-constexpr int kMaxOuterBits = 10;
+constexpr int kMaxOuterBits = 9;
 // Sorted base block built in shared memory by the list builder.
 constexpr int kBaseBits = 12;
 

@@ -33,13 +33,16 @@
 
 constexpr int kJoinThreads = 512;
 constexpr int kJoinWarps = kJoinThreads / 32;
+constexpr int kJoinCtasPerSm = 1;
 constexpr int kL1Log = 15, kL2Log = 13, kL3Log = 11;  // index levels (slots)
 constexpr int kPart = 384;                            // A records per warp partition
 constexpr int kCapRec = kPart * kJoinWarps;           // 6144 A records per chunk
 constexpr int kLose = 128;                            // per-warp level-1 loser list
 constexpr int kList4 = 256;                           // level-3 losers (CTA list)
 constexpr int kMaxOuter = 1 << kMaxOuterBits;
-constexpr int kU = 8;                                 // windows in flight per lane
+constexpr int kU = 8;                                 // A windows in flight per lane
+constexpr int kUB = 4;                                // B windows in flight per lane
+constexpr int kStageB = kUB * 32;                     // staged B records per warp
 constexpr uint16_t kNone = 0xffffu;
 constexpr uint32_t kFlagCont = 0x80000000u;
 
@@ -51,9 +54,9 @@ struct JoinSmem {
   uint16_t t3[1 << kL3Log];
   uint16_t lose[kJoinWarps][kLose];  // per-warp level-1 losers, then level-2 losers
   uint16_t list4[kList4];
-  uint64_t qK[kJoinWarps][64];  // B candidates: key
-  uint32_t qJ[kJoinWarps][64];  // B candidates: halo flag << 31 | inner index
-  uint16_t qB[kJoinWarps][64];  // B candidates: outer index
+  uint64_t qK[kJoinWarps][kStageB];  // staged B records: key
+  uint32_t qJ[kJoinWarps][kStageB];  // staged B records: halo flag << 31 | inner index
+  uint16_t qB[kJoinWarps][kStageB];  // staged B records: outer index
   uint64_t ax[kMaxOuter];
   uint32_t arot[kMaxOuter];
   uint32_t apos[kMaxOuter];
@@ -72,6 +75,21 @@ __device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
   return (uint32_t)(rel >> shift) & ((1u << lg) - 1u);
 }
 
+// Emit the full pattern of a matching (A record r, B record) pair.
+__device__ __noinline__ void emit_match(const JoinSmem& S, const JoinArgs& a, uint32_t r,
+                                        uint32_t ib, uint32_t jb) {
+  const JoinPlan& P = a.P;
+  const uint32_t id = S.recI[r];
+  const int aib = P.list[1].bits;
+  const uint32_t ia = id >> aib, ja = id & ((1u << aib) - 1u);
+  const uint64_t pa = (uint64_t)__ldg(a.pat[0] + ia) |
+                      ((uint64_t)__ldg(a.pat[1] + ja) << P.list[1].pat_shift);
+  const uint64_t pb = ((uint64_t)__ldg(a.pat[2] + ib) << P.list[2].pat_shift) |
+                      ((uint64_t)__ldg(a.pat[3] + jb) << P.list[3].pat_shift);
+  const unsigned long long k = atomicAdd(&a.ctr->out_count, 1ull);
+  if (k < a.cap) a.out[k] = pa | pb;
+}
+
 // Exact check of A record r against B key s; emits the pattern on a match.
 __device__ __forceinline__ void check_pair(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
                                            uint32_t r, uint64_t s, bool bghost, uint32_t ib,
@@ -81,17 +99,7 @@ __device__ __forceinline__ void check_pair(const JoinSmem& S, const JoinArgs& a,
   n_qprobe++;
   const uint64_t ka = S.recK[r];
   if (bghost && (ka - cW >= W)) return;  // halo x halo belongs to bucket c+1
-  if (ka - s + (P.width >> 1) <= P.width) {
-    const uint32_t id = S.recI[r];
-    const int aib = P.list[1].bits;
-    const uint32_t ia = id >> aib, ja = id & ((1u << aib) - 1u);
-    const uint64_t pa = (uint64_t)__ldg(a.pat[0] + ia) |
-                        ((uint64_t)__ldg(a.pat[1] + ja) << P.list[1].pat_shift);
-    const uint64_t pb = ((uint64_t)__ldg(a.pat[2] + ib) << P.list[2].pat_shift) |
-                        ((uint64_t)__ldg(a.pat[3] + jb) << P.list[3].pat_shift);
-    const unsigned long long k = atomicAdd(&a.ctr->out_count, 1ull);
-    if (k < a.cap) a.out[k] = pa | pb;
-  }
+  if (ka - s + (P.width >> 1) <= P.width) emit_match(S, a, r, ib, jb);
 }
 
 // Probe one level of the index over the homes of [lo_rel, hi_rel].
@@ -110,80 +118,91 @@ __device__ __forceinline__ void probe_level(const JoinSmem& S, const JoinArgs& a
   }
 }
 
-__device__ __forceinline__ void probe_b(const JoinSmem& S, const JoinArgs& a, uint64_t cW, uint64_t s,
-                                     bool bghost, uint32_t ib, uint32_t jb, uint32_t& n_qprobe) {
+// Deep probe for a B record whose level-1 home(s) carry the collision flag:
+// levels 2 and 3 and the short list (level 1 was checked in place).
+__device__ __noinline__ uint32_t probe_b(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                         uint64_t s, bool bghost, uint32_t ib, uint32_t jb) {
+  uint32_t n_qprobe = 0;
   const uint64_t H = a.P.half;
   const uint64_t rel = s - cW;  // main: [0, W); halo: [W, W + H)
   const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
   const uint64_t hi_rel = rel + H;
-  probe_level(S, a, cW, S.t1, kL1Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
   probe_level(S, a, cW, S.t2, kL2Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
   probe_level(S, a, cW, S.t3, kL3Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
   const uint32_t n4 = S.n4 < (unsigned)kList4 ? S.n4 : (unsigned)kList4;
   for (uint32_t e = 0; e < n4; e++) check_pair(S, a, cW, S.list4[e], s, bghost, ib, jb, n_qprobe);
+  return n_qprobe;
 }
 
-// Fast B screen.  Every A record's level-1 home is occupied (by it or by the
-// record that won the slot), so empty level-1 homes over the window prove
-// that no A record is within +-H: one shared load for ~88% of B records.
-__device__ __forceinline__ bool b_may_hit(const JoinSmem& S, const JoinPlan& P, uint64_t cW,
-                                          uint64_t s, uint32_t n4) {
+// Full probe (all levels) for B records whose window spans many level-1
+// homes (wide parity-mode windows).
+__device__ __noinline__ uint32_t probe_b_wide(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                              uint64_t s, bool bghost, uint32_t ib, uint32_t jb) {
+  uint32_t n_qprobe = 0;
+  const uint64_t H = a.P.half;
+  const uint64_t rel = s - cW;
+  const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
+  const uint64_t hi_rel = rel + H;
+  const int shift = 64 - a.P.r - kL1Log;
+  const uint32_t h0 = (uint32_t)(lo_rel >> shift);
+  const uint32_t hn = (uint32_t)(hi_rel >> shift) - h0;
+  const uint32_t m = (1u << kL1Log) - 1u;
+  const uint32_t lim = hn < m ? hn : m;
+  for (uint32_t d = 0; d <= lim; d++) {
+    const uint32_t e = S.t1[(h0 + d) & m];
+    if (e != kNone) check_pair(S, a, cW, e & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+  }
+  return n_qprobe + probe_b(S, a, cW, s, bghost, ib, jb);
+}
+
+// In-place level-1 check for one B record: the occupants of its level-1
+// home(s) are compared exactly.  Returns 1 when a deep probe of levels 2-3
+// is still needed (flagged collision slot), 2 for a wide window.
+__device__ __forceinline__ int probe_b_l1(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                          uint64_t s, bool bghost, uint32_t ib, uint32_t jb,
+                                          uint32_t& n_qprobe) {
+  const JoinPlan& P = a.P;
   const uint64_t H = P.half;
   const uint64_t rel = s - cW;
   const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
   const int sh1 = 64 - P.r - kL1Log;
   const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
   const uint32_t hn = (uint32_t)((rel + H) >> sh1) - h0;
-  if (hn > 1 || n4 > 0) return true;
+  if (hn > 1) return 2;
   const uint32_t m1 = (1u << kL1Log) - 1u;
-  return S.t1[h0 & m1] != kNone || (hn && S.t1[(h0 + 1) & m1] != kNone);
+  int deep = 0;
+  const uint32_t e0 = S.t1[h0 & m1];
+  if (e0 != kNone) {
+    check_pair(S, a, cW, e0 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+    deep |= (e0 >> 15) & 1;
+  }
+  if (hn) {
+    const uint32_t e1 = S.t1[(h0 + 1) & m1];
+    if (e1 != kNone) {
+      check_pair(S, a, cW, e1 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+      deep |= (e1 >> 15) & 1;
+    }
+  }
+  return deep;
 }
 
-// Probe one full batch of 32 queued B candidates (one lane each) and shift
-// the remainder down.  Out of line: one copy of the probe code.
-__device__ __noinline__ void drain_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, uint32_t& nq,
-                                     uint32_t& n_qprobe) {
+// Deep-probe the staged B records of this warp (rare: flagged level-1
+// collisions or wide windows), one lane per record, from one code site.
+__device__ __noinline__ uint32_t process_staged(JoinSmem& S, const JoinArgs& a, uint64_t cW,
+                                                uint32_t nst) {
+  uint32_t n_qprobe = 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncwarp();
-  probe_b(S, a, cW, S.qK[wid][lane], S.qJ[wid][lane] >> 31, S.qB[wid][lane],
-          S.qJ[wid][lane] & 0x7fffffffu, n_qprobe);
-  __syncwarp();
-  nq -= 32;
-  if ((uint32_t)lane < nq) {
-    S.qK[wid][lane] = S.qK[wid][32 + lane];
-    S.qJ[wid][lane] = S.qJ[wid][32 + lane];
-    S.qB[wid][lane] = S.qB[wid][32 + lane];
+  for (uint32_t e = lane; e < nst; e += 32) {
+    const uint64_t s = S.qK[wid][e];
+    const uint32_t meta = S.qJ[wid][e];
+    if ((meta >> 30) & 1u)
+      n_qprobe += probe_b_wide(S, a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
+    else
+      n_qprobe += probe_b(S, a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
   }
   __syncwarp();
-}
-
-// Append this lane's B candidate (if any) to the warp queue; probe full
-// batches of 32 from a single code site (one lane per candidate).
-__device__ __forceinline__ void queue_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, bool cand,
-                                        uint64_t s, bool bghost, uint32_t ib, uint32_t jb,
-                                        uint32_t& nq, uint32_t& n_qprobe) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned FULL = 0xffffffffu;
-  const uint32_t cm = __ballot_sync(FULL, cand);
-  if (cand) {
-    const uint32_t k = nq + __popc(cm & ((1u << lane) - 1u));
-    S.qK[wid][k] = s;
-    S.qJ[wid][k] = (bghost ? 0x80000000u : 0u) | jb;
-    S.qB[wid][k] = (uint16_t)ib;
-  }
-  nq += __popc(cm);
-  if (nq >= 32) drain_b(S, a, cW, nq, n_qprobe);
-}
-
-__device__ __noinline__ void flush_b(JoinSmem& S, const JoinArgs& a, uint64_t cW, uint32_t& nq,
-                                        uint32_t& n_qprobe) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncwarp();
-  if ((uint32_t)lane < nq)
-    probe_b(S, a, cW, S.qK[wid][lane], S.qJ[wid][lane] >> 31, S.qB[wid][lane],
-            S.qJ[wid][lane] & 0x7fffffffu, n_qprobe);
-  nq = 0;
-  __syncwarp();
+  return n_qprobe;
 }
 
 // Windowed walk of one side: lane-group layout, kU windows in flight.  Side A
@@ -191,8 +210,11 @@ __device__ __noinline__ void flush_b(JoinSmem& S, const JoinArgs& a, uint64_t cW
 // probes.  Saturated runs are flagged in the main-count array.
 template <bool SIDE_A>
 __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
-                                            uint32_t lo, uint32_t hi, int gs, uint32_t& wfill,
-                                            uint32_t& n_stat, uint32_t& n_qprobe, bool& overflow) {
+                                            uint32_t lo, uint32_t hi, int gs, uint32_t& wfill_r,
+                                            uint32_t& n_stat_r, uint32_t& n_qprobe_r, bool& overflow_r) {
+  // register copies of the by-reference counters (written back once)
+  uint32_t wfill = wfill_r, n_stat = n_stat_r, n_qprobe = n_qprobe_r;
+  bool overflow = overflow_r;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -208,32 +230,60 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
   const int sh = 64 - P.r;
   const uint64_t W = 1ull << sh, H = P.half;
   const int aib = P.list[1].bits;
-  const uint32_t n4 = SIDE_A ? 0u : S.n4;
   uint32_t nq = 0;
-  for (uint32_t base = lo; base < hi; base += kU * gpw) {
-    uint64_t sv[kU];
-    uint32_t jv[kU];
-    bool mv[kU], ev[kU];
+  constexpr int U = SIDE_A ? kU : kUB;
+  unsigned long long* tr = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 128 + (SIDE_A ? 0 : 64) : nullptr;
+  int trn = 0;
+  // Software pipeline: the U window keys of round k+1 are loaded while round
+  // k is processed, so the L2 round trips overlap the processing and each
+  // other (issued back to back, consumed only after the loop back-edge).
+  uint64_t kn[U];
+  auto issue = [&](uint32_t b0) {
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
+    for (int u = 0; u < U; u++) {
+      const uint32_t i = b0 + u * gpw + g;
+      const bool valid = i < hi && (uint32_t)l < Mi;
+      const uint32_t ic = i < hi ? i : lo;
+      const uint32_t j = (rots[ic] + poss[ic] + l) & (Mi - 1);
+      kn[u] = __ldg(kin + (valid ? j : 0u));
+    }
+  };
+  if (lo < hi) issue(lo);
+  for (uint32_t base = lo; base < hi; base += U * gpw) {
+    if (tr && trn < 60) tr[trn++] = clock64();
+    uint64_t kv[U];
+    uint32_t jv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) kv[u] = kn[u];
+    if (base + U * gpw < hi) issue(base + U * gpw);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t i = base + u * gpw + g;
+      const uint32_t ic = i < hi ? i : lo;
+      jv[u] = (rots[ic] + poss[ic] + l) & (Mi - 1);
+    }
+    // phase 2: classify (main / halo) from the loaded keys
+    uint64_t sv[U];
+    bool mv[U], ev[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
       const uint32_t i = base + u * gpw + g;
       const bool valid = i < hi && (uint32_t)l < Mi;
-      uint32_t pos = 0, rot = 0;
+      uint32_t pos = 0;
       uint64_t x = 0;
       if (i < hi) {
         pos = poss[i];
-        rot = rots[i];
         x = xs[i];
       }
       const uint32_t o = pos + l;
-      jv[u] = (rot + o) & (Mi - 1);
-      sv[u] = x + (valid ? __ldg(kin + jv[u]) : 0ull);
+      sv[u] = x + kv[u];
       const uint64_t rel = sv[u] - cW;
       mv[u] = valid && o < Mi && rel < W;
       ev[u] = mv[u] || (valid && (rel - W) < H);
     }
+    if (tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
+    for (int u = 0; u < U; u++) {
       const uint32_t i = base + u * gpw + g;
       const uint32_t em = __ballot_sync(FULL, ev[u]);
       const uint32_t mm = __ballot_sync(FULL, mv[u]);
@@ -252,24 +302,42 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
         n_stat += ev[u] ? 1u : 0u;
       } else {
         n_stat += ev[u] ? 1u : 0u;
-        const bool cand = ev[u] && b_may_hit(S, P, cW, sv[u], n4);
-        queue_b(S, a, cW, cand, sv[u], !mv[u], i, jv[u], nq, n_qprobe);
+        int deep = 0;
+        if (ev[u]) deep = probe_b_l1(S, a, cW, sv[u], !mv[u], i, jv[u], n_qprobe);
+        const uint32_t dm = __ballot_sync(FULL, deep != 0);
+        if (deep) {
+          const uint32_t k = nq + __popc(dm & lt_mask);
+          S.qK[wid][k] = sv[u];
+          S.qJ[wid][k] = (mv[u] ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | jv[u];
+          S.qB[wid][k] = (uint16_t)i;
+        }
+        nq += __popc(dm);
       }
       if (l == 0 && i < hi) {
         const bool sat = ((em >> gb) & gmask) == gmask && (uint32_t)gs < Mi;
         mainv[i] = (uint32_t)__popc((mm >> gb) & gmask) | (sat ? kFlagCont : 0u);
       }
     }
+    if (!SIDE_A && nq) {
+      n_qprobe += process_staged(S, a, cW, nq);
+      nq = 0;
+    }
   }
-  if (!SIDE_A) flush_b(S, a, cW, nq, n_qprobe);
+  wfill_r = wfill;
+  n_stat_r = n_stat;
+  n_qprobe_r = n_qprobe;
+  overflow_r = overflow;
 }
 
 // Continue the saturated runs of one side, one outer at a time, 32 lanes.
 template <bool SIDE_A>
 __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
-                                              uint32_t lo, uint32_t hi, int gs, uint32_t& wfill,
-                                              uint32_t& n_stat, uint32_t& n_qprobe,
-                                              bool& overflow) {
+                                              uint32_t lo, uint32_t hi, int gs, uint32_t& wfill_r,
+                                              uint32_t& n_stat_r, uint32_t& n_qprobe_r,
+                                              bool& overflow_r) {
+  // register copies of the by-reference counters (written back once)
+  uint32_t wfill = wfill_r, n_stat = n_stat_r, n_qprobe = n_qprobe_r;
+  bool overflow = overflow_r;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -280,8 +348,6 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
   const int sh = 64 - P.r;
   const uint64_t W = 1ull << sh, H = P.half;
   const int aib = P.list[1].bits;
-  const uint32_t n4 = SIDE_A ? 0u : S.n4;
-  uint32_t nq = 0;
   for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
     const uint32_t ii = c0 + lane;
     const bool flag = ii < hi && (mainv[ii] & kFlagCont);
@@ -320,8 +386,16 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
           n_stat += e ? 1u : 0u;
         } else {
           n_stat += e ? 1u : 0u;
-          const bool cand = e && b_may_hit(S, P, cW, s, n4);
-          queue_b(S, a, cW, cand, s, !m, i, j, nq, n_qprobe);
+          int deep = 0;
+          if (e) deep = probe_b_l1(S, a, cW, s, !m, i, j, n_qprobe);
+          const uint32_t dm = __ballot_sync(FULL, deep != 0);
+          if (deep) {
+            const uint32_t k = __popc(dm & lt_mask);
+            S.qK[wid][k] = s;
+            S.qJ[wid][k] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
+            S.qB[wid][k] = (uint16_t)i;
+          }
+          if (dm) n_qprobe += process_staged(S, a, cW, __popc(dm));
         }
         mainc += __popc(__ballot_sync(FULL, m));
         off += ne;
@@ -330,7 +404,10 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
       if (lane == 0) mainv[i] = mainc;
     }
   }
-  if (!SIDE_A) flush_b(S, a, cW, nq, n_qprobe);
+  wfill_r = wfill;
+  n_stat_r = n_stat;
+  n_qprobe_r = n_qprobe;
+  overflow_r = overflow;
 }
 
 // Build levels 2 and 3 from the level-1 losers (plain stores + read-back).
@@ -350,15 +427,19 @@ __device__ __forceinline__ void build_index_levels(JoinSmem& S, const JoinPlan& 
     const uint32_t r = wid * kPart + e;
     bool lost = false;
     uint64_t rel = 0;
+    uint32_t h1 = 0, occ = 0;
     if (e < nw) {
       rel = S.recK[r] - cW;
-      lost = S.t1[home_of(rel, sh - kL1Log, kL1Log)] != (uint16_t)r;
+      h1 = home_of(rel, sh - kL1Log, kL1Log);
+      occ = S.t1[h1];
+      lost = (occ & 0x7fffu) != r;
     }
     const uint32_t lm = __ballot_sync(FULL, lost);
     if (lost) {
       const uint32_t k = nl + __popc(lm & lt_mask);
       if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
       S.t2[home_of(rel, sh - kL2Log, kL2Log)] = (uint16_t)r;
+      S.t1[h1] = (uint16_t)(occ | 0x8000u);  // collision flag: B also probes levels 2-3
     }
     nl += __popc(lm);
   }
@@ -411,7 +492,7 @@ __device__ __forceinline__ void clear_index(JoinSmem& S) {
   for (int i = threadIdx.x; i < (1 << kL3Log) / 8; i += kJoinThreads) p3[i] = f4;
 }
 
-__global__ void __launch_bounds__(kJoinThreads, 1)
+__global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     join_kernel(const __grid_constant__ JoinArgs a, int gsA, int gsB) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   JoinSmem& S = *reinterpret_cast<JoinSmem*>(smem_raw);

@@ -277,6 +277,13 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
     fprintf(stderr, "[rfr trace] gsA=%d gsB=%d r=%d MoA=%d MiA=%d MoB=%d MiB=%d init=%llu\n", gsA, gsB,
             P.r, 1 << P.list[0].bits, 1 << P.list[1].bits, 1 << P.list[2].bits,
             1 << P.list[3].bits, h[1] - h[0]);
+    for (int side = 0; side < 2; side++) {
+      fprintf(stderr, "[rfr trace] %s rounds (issue -> after loads+classify, -> next round):", side ? "B" : "A");
+      const unsigned long long* t = h + 128 + side * 64;
+      for (int k = 0; k + 2 < 64 && t[k + 2]; k += 2)
+        fprintf(stderr, " %llu/%llu", (t[k + 1] & ~(1ull << 63)) - t[k], t[k + 2] - (t[k + 1] & ~(1ull << 63)));
+      fprintf(stderr, "\n");
+    }
     for (int b = 0; b < 6; b++) {  // marks: bucket start, A gen, A index, B pass, end barrier
       const unsigned long long* q = h + 1 + b * 5;
       if (!q[4]) break;
