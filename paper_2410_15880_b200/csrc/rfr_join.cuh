@@ -31,6 +31,12 @@
 // overflow is known, so no pair is duplicated.
 #pragma once
 
+// Clock64 phase trace of CTA 0 (RFR_TRACE=1 at run time, needs a build with
+// `make TRACE=1`); compiled out of the production kernel.
+#ifndef RFR_JOIN_TRACE
+#define RFR_JOIN_TRACE 0
+#endif
+
 constexpr int kJoinThreads = 512;
 constexpr int kJoinWarps = kJoinThreads / 32;
 constexpr int kJoinCtasPerSm = 1;
@@ -71,13 +77,22 @@ struct JoinSmem {
   uint32_t cur_i, cur_t;  // slow path cursor
 };
 
+// The join's shared memory, addressed from the extern symbol inside every
+// (noinline) function so the compiler emits direct shared-window accesses
+// instead of re-deriving them from a generic reference.
+__device__ __forceinline__ JoinSmem& join_smem() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return *reinterpret_cast<JoinSmem*>(smem_raw);
+}
+
 __device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
   return (uint32_t)(rel >> shift) & ((1u << lg) - 1u);
 }
 
 // Emit the full pattern of a matching (A record r, B record) pair.
-__device__ __noinline__ void emit_match(const JoinSmem& S, const JoinArgs& a, uint32_t r,
+__device__ __noinline__ void emit_match(const JoinArgs& a, uint32_t r,
                                         uint32_t ib, uint32_t jb) {
+  JoinSmem& S = join_smem();
   const JoinPlan& P = a.P;
   const uint32_t id = S.recI[r];
   const int aib = P.list[1].bits;
@@ -90,82 +105,109 @@ __device__ __noinline__ void emit_match(const JoinSmem& S, const JoinArgs& a, ui
   if (k < a.cap) a.out[k] = pa | pb;
 }
 
+// Running counters of one warp threaded through the passes by value (by
+// reference they would live in local memory across every call).
+struct PassSt {
+  uint32_t wfill;     // records in the warp's A partition
+  uint32_t n_stat;    // records streamed (inserts for A, queries for B)
+  uint32_t n_qprobe;  // A records compared against B records
+  bool overflow;      // the A partition overflowed
+};
+
+// Per-bucket constants, built once per pass into registers (reading them
+// through the JoinArgs reference inside the loops costs a generic load each).
+struct JoinK {
+  uint64_t cW, W, H, width, hw;  // bucket base, bucket width, halo, window, window / 2
+  int sh;                        // bucket = key >> sh
+};
+__device__ __forceinline__ JoinK make_k(const JoinArgs& a, uint64_t cW) {
+  JoinK K;
+  K.sh = 64 - a.P.r;
+  K.cW = cW;
+  K.W = 1ull << K.sh;
+  K.H = a.P.half;
+  K.width = a.P.width;
+  K.hw = a.P.width >> 1;
+  return K;
+}
+
 // Exact check of A record r against B key s; emits the pattern on a match.
-__device__ __forceinline__ void check_pair(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __forceinline__ void check_pair(const JoinSmem& S, const JoinArgs& a, const JoinK& K,
                                            uint32_t r, uint64_t s, bool bghost, uint32_t ib,
                                            uint32_t jb, uint32_t& n_qprobe) {
-  const JoinPlan& P = a.P;
-  const uint64_t W = 1ull << (64 - P.r);
   n_qprobe++;
   const uint64_t ka = S.recK[r];
-  if (bghost && (ka - cW >= W)) return;  // halo x halo belongs to bucket c+1
-  if (ka - s + (P.width >> 1) <= P.width) emit_match(S, a, r, ib, jb);
+  if (bghost && (ka - K.cW >= K.W)) return;  // halo x halo belongs to bucket c+1
+  if (ka - s + K.hw <= K.width) emit_match(a, r, ib, jb);
 }
 
 // Probe one level of the index over the homes of [lo_rel, hi_rel].
-__device__ __forceinline__ void probe_level(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __forceinline__ void probe_level(const JoinSmem& S, const JoinArgs& a, const JoinK& K,
                                             const uint16_t* t, int lg, uint64_t lo_rel,
                                             uint64_t hi_rel, uint64_t s, bool bghost, uint32_t ib,
                                             uint32_t jb, uint32_t& n_qprobe) {
-  const int shift = 64 - a.P.r - lg;
+  const int shift = K.sh - lg;
   const uint32_t h0 = (uint32_t)(lo_rel >> shift);
   const uint32_t hn = (uint32_t)(hi_rel >> shift) - h0;
   const uint32_t m = (1u << lg) - 1u;
   const uint32_t lim = hn < m ? hn : m;
   for (uint32_t d = 0; d <= lim; d++) {
     const uint32_t r = t[(h0 + d) & m];
-    if (r != kNone) check_pair(S, a, cW, r, s, bghost, ib, jb, n_qprobe);
+    if (r != kNone) check_pair(S, a, K, r, s, bghost, ib, jb, n_qprobe);
   }
 }
 
 // Deep probe for a B record whose level-1 home(s) carry the collision flag:
 // levels 2 and 3 and the short list (level 1 was checked in place).
-__device__ __noinline__ uint32_t probe_b(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __noinline__ uint32_t probe_b(const JoinArgs& a, uint64_t cW,
                                          uint64_t s, bool bghost, uint32_t ib, uint32_t jb) {
+  JoinSmem& S = join_smem();
   uint32_t n_qprobe = 0;
-  const uint64_t H = a.P.half;
+  const JoinK K = make_k(a, cW);
+  const uint64_t H = K.H;
   const uint64_t rel = s - cW;  // main: [0, W); halo: [W, W + H)
   const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
   const uint64_t hi_rel = rel + H;
-  probe_level(S, a, cW, S.t2, kL2Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
-  probe_level(S, a, cW, S.t3, kL3Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
+  probe_level(S, a, K, S.t2, kL2Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
+  probe_level(S, a, K, S.t3, kL3Log, lo_rel, hi_rel, s, bghost, ib, jb, n_qprobe);
   const uint32_t n4 = S.n4 < (unsigned)kList4 ? S.n4 : (unsigned)kList4;
-  for (uint32_t e = 0; e < n4; e++) check_pair(S, a, cW, S.list4[e], s, bghost, ib, jb, n_qprobe);
+  for (uint32_t e = 0; e < n4; e++) check_pair(S, a, K, S.list4[e], s, bghost, ib, jb, n_qprobe);
   return n_qprobe;
 }
 
 // Full probe (all levels) for B records whose window spans many level-1
 // homes (wide parity-mode windows).
-__device__ __noinline__ uint32_t probe_b_wide(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __noinline__ uint32_t probe_b_wide(const JoinArgs& a, uint64_t cW,
                                               uint64_t s, bool bghost, uint32_t ib, uint32_t jb) {
+  JoinSmem& S = join_smem();
   uint32_t n_qprobe = 0;
-  const uint64_t H = a.P.half;
+  const JoinK K = make_k(a, cW);
+  const uint64_t H = K.H;
   const uint64_t rel = s - cW;
   const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
   const uint64_t hi_rel = rel + H;
-  const int shift = 64 - a.P.r - kL1Log;
+  const int shift = K.sh - kL1Log;
   const uint32_t h0 = (uint32_t)(lo_rel >> shift);
   const uint32_t hn = (uint32_t)(hi_rel >> shift) - h0;
   const uint32_t m = (1u << kL1Log) - 1u;
   const uint32_t lim = hn < m ? hn : m;
   for (uint32_t d = 0; d <= lim; d++) {
     const uint32_t e = S.t1[(h0 + d) & m];
-    if (e != kNone) check_pair(S, a, cW, e & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+    if (e != kNone) check_pair(S, a, K, e & 0x7fffu, s, bghost, ib, jb, n_qprobe);
   }
-  return n_qprobe + probe_b(S, a, cW, s, bghost, ib, jb);
+  return n_qprobe + probe_b(a, cW, s, bghost, ib, jb);
 }
 
 // In-place level-1 check for one B record: the occupants of its level-1
 // home(s) are compared exactly.  Returns 1 when a deep probe of levels 2-3
 // is still needed (flagged collision slot), 2 for a wide window.
-__device__ __forceinline__ int probe_b_l1(const JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __forceinline__ int probe_b_l1(const JoinSmem& S, const JoinArgs& a, const JoinK& K,
                                           uint64_t s, bool bghost, uint32_t ib, uint32_t jb,
                                           uint32_t& n_qprobe) {
-  const JoinPlan& P = a.P;
-  const uint64_t H = P.half;
-  const uint64_t rel = s - cW;
+  const uint64_t H = K.H;
+  const uint64_t rel = s - K.cW;
   const uint64_t lo_rel = rel >= H ? rel - H : 0ull;
-  const int sh1 = 64 - P.r - kL1Log;
+  const int sh1 = K.sh - kL1Log;
   const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
   const uint32_t hn = (uint32_t)((rel + H) >> sh1) - h0;
   if (hn > 1) return 2;
@@ -173,13 +215,13 @@ __device__ __forceinline__ int probe_b_l1(const JoinSmem& S, const JoinArgs& a, 
   int deep = 0;
   const uint32_t e0 = S.t1[h0 & m1];
   if (e0 != kNone) {
-    check_pair(S, a, cW, e0 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+    check_pair(S, a, K, e0 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
     deep |= (e0 >> 15) & 1;
   }
   if (hn) {
     const uint32_t e1 = S.t1[(h0 + 1) & m1];
     if (e1 != kNone) {
-      check_pair(S, a, cW, e1 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
+      check_pair(S, a, K, e1 & 0x7fffu, s, bghost, ib, jb, n_qprobe);
       deep |= (e1 >> 15) & 1;
     }
   }
@@ -188,8 +230,9 @@ __device__ __forceinline__ int probe_b_l1(const JoinSmem& S, const JoinArgs& a, 
 
 // Deep-probe the staged B records of this warp (rare: flagged level-1
 // collisions or wide windows), one lane per record, from one code site.
-__device__ __noinline__ uint32_t process_staged(JoinSmem& S, const JoinArgs& a, uint64_t cW,
+__device__ __noinline__ uint32_t process_staged(const JoinArgs& a, uint64_t cW,
                                                 uint32_t nst) {
+  JoinSmem& S = join_smem();
   uint32_t n_qprobe = 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncwarp();
@@ -197,9 +240,9 @@ __device__ __noinline__ uint32_t process_staged(JoinSmem& S, const JoinArgs& a, 
     const uint64_t s = S.qK[wid][e];
     const uint32_t meta = S.qJ[wid][e];
     if ((meta >> 30) & 1u)
-      n_qprobe += probe_b_wide(S, a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
+      n_qprobe += probe_b_wide(a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
     else
-      n_qprobe += probe_b(S, a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
+      n_qprobe += probe_b(a, cW, s, meta >> 31, S.qB[wid][e], meta & 0x3fffffffu);
   }
   __syncwarp();
   return n_qprobe;
@@ -209,12 +252,12 @@ __device__ __noinline__ uint32_t process_staged(JoinSmem& S, const JoinArgs& a, 
 // appends records to the warp partition and claims level-1 homes; side B
 // probes.  Saturated runs are flagged in the main-count array.
 template <bool SIDE_A>
-__device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
-                                            uint32_t lo, uint32_t hi, int gs, uint32_t& wfill_r,
-                                            uint32_t& n_stat_r, uint32_t& n_qprobe_r, bool& overflow_r) {
+__device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
+                                            uint32_t lo, uint32_t hi, int gs, PassSt st) {
+  JoinSmem& S = join_smem();
   // register copies of the by-reference counters (written back once)
-  uint32_t wfill = wfill_r, n_stat = n_stat_r, n_qprobe = n_qprobe_r;
-  bool overflow = overflow_r;
+  uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
+  bool overflow = st.overflow;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -229,10 +272,11 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
   uint32_t* mainv = SIDE_A ? S.amain : S.bmain;
   const int sh = 64 - P.r;
   const uint64_t W = 1ull << sh, H = P.half;
+  const JoinK K = make_k(a, cW);
   const int aib = P.list[1].bits;
   uint32_t nq = 0;
   constexpr int U = SIDE_A ? kU : kUB;
-  unsigned long long* tr = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 128 + (SIDE_A ? 0 : 64) : nullptr;
+  unsigned long long* tr = (RFR_JOIN_TRACE && a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 128 + (SIDE_A ? 0 : 64) : nullptr;
   int trn = 0;
   // Software pipeline: the U window keys of round k+1 are loaded while round
   // k is processed, so the L2 round trips overlap the processing and each
@@ -250,7 +294,7 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
   };
   if (lo < hi) issue(lo);
   for (uint32_t base = lo; base < hi; base += U * gpw) {
-    if (tr && trn < 60) tr[trn++] = clock64();
+    if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64();
     uint64_t kv[U];
     uint32_t jv[U];
 #pragma unroll
@@ -281,7 +325,7 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
       mv[u] = valid && o < Mi && rel < W;
       ev[u] = mv[u] || (valid && (rel - W) < H);
     }
-    if (tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
+    if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const uint32_t i = base + u * gpw + g;
@@ -303,7 +347,7 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
       } else {
         n_stat += ev[u] ? 1u : 0u;
         int deep = 0;
-        if (ev[u]) deep = probe_b_l1(S, a, cW, sv[u], !mv[u], i, jv[u], n_qprobe);
+        if (ev[u]) deep = probe_b_l1(S, a, K, sv[u], !mv[u], i, jv[u], n_qprobe);
         const uint32_t dm = __ballot_sync(FULL, deep != 0);
         if (deep) {
           const uint32_t k = nq + __popc(dm & lt_mask);
@@ -319,25 +363,21 @@ __device__ __noinline__ void window_pass(JoinSmem& S, const JoinArgs& a, uint64_
       }
     }
     if (!SIDE_A && nq) {
-      n_qprobe += process_staged(S, a, cW, nq);
+      n_qprobe += process_staged(a, cW, nq);
       nq = 0;
     }
   }
-  wfill_r = wfill;
-  n_stat_r = n_stat;
-  n_qprobe_r = n_qprobe;
-  overflow_r = overflow;
+  return PassSt{wfill, n_stat, n_qprobe, overflow};
 }
 
 // Continue the saturated runs of one side, one outer at a time, 32 lanes.
 template <bool SIDE_A>
-__device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint64_t cW,
-                                              uint32_t lo, uint32_t hi, int gs, uint32_t& wfill_r,
-                                              uint32_t& n_stat_r, uint32_t& n_qprobe_r,
-                                              bool& overflow_r) {
+__device__ __noinline__ PassSt continue_pass(const JoinArgs& a, uint64_t cW,
+                                              uint32_t lo, uint32_t hi, int gs, PassSt st) {
+  JoinSmem& S = join_smem();
   // register copies of the by-reference counters (written back once)
-  uint32_t wfill = wfill_r, n_stat = n_stat_r, n_qprobe = n_qprobe_r;
-  bool overflow = overflow_r;
+  uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
+  bool overflow = st.overflow;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -347,6 +387,7 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
   uint32_t* mainv = SIDE_A ? S.amain : S.bmain;
   const int sh = 64 - P.r;
   const uint64_t W = 1ull << sh, H = P.half;
+  const JoinK K = make_k(a, cW);
   const int aib = P.list[1].bits;
   for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
     const uint32_t ii = c0 + lane;
@@ -387,7 +428,7 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
         } else {
           n_stat += e ? 1u : 0u;
           int deep = 0;
-          if (e) deep = probe_b_l1(S, a, cW, s, !m, i, j, n_qprobe);
+          if (e) deep = probe_b_l1(S, a, K, s, !m, i, j, n_qprobe);
           const uint32_t dm = __ballot_sync(FULL, deep != 0);
           if (deep) {
             const uint32_t k = __popc(dm & lt_mask);
@@ -395,7 +436,7 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
             S.qJ[wid][k] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
             S.qB[wid][k] = (uint16_t)i;
           }
-          if (dm) n_qprobe += process_staged(S, a, cW, __popc(dm));
+          if (dm) n_qprobe += process_staged(a, cW, __popc(dm));
         }
         mainc += __popc(__ballot_sync(FULL, m));
         off += ne;
@@ -404,16 +445,131 @@ __device__ __noinline__ void continue_pass(JoinSmem& S, const JoinArgs& a, uint6
       if (lane == 0) mainv[i] = mainc;
     }
   }
-  wfill_r = wfill;
-  n_stat_r = n_stat;
-  n_qprobe_r = n_qprobe;
-  overflow_r = overflow;
+  return PassSt{wfill, n_stat, n_qprobe, overflow};
+}
+
+// Branch-light level-1 probe of one B record (run_pass): the slot(s) and
+// the records they name are read unconditionally, the exact checks are
+// predicated, and only a hit branches (to emit_match).  Returns 0, 1 (a
+// flagged slot: levels 2-3 still to probe) or 2 (window spans > 2 homes).
+__device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs& a,
+                                               const JoinK& K, bool e, uint64_t s, bool bghost,
+                                               uint32_t ib, uint32_t jb, uint32_t& n_qprobe) {
+  const uint64_t rel = s - K.cW;
+  const uint64_t lo_rel = rel >= K.H ? rel - K.H : 0ull;
+  const int sh1 = K.sh - kL1Log;
+  const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
+  const uint32_t hn = (uint32_t)((rel + K.H) >> sh1) - h0;
+  const uint32_t m1 = (1u << kL1Log) - 1u;
+  const bool narrow = e && hn <= 1;  // wide windows go to probe_b_wide whole
+  const uint32_t e0 = narrow ? (uint32_t)S.t1[h0 & m1] : (uint32_t)kNone;
+  const uint32_t e1 = (narrow && hn == 1) ? (uint32_t)S.t1[(h0 + 1) & m1] : (uint32_t)kNone;
+  const uint32_t r0 = min(e0 & 0x7fffu, (uint32_t)kCapRec - 1u);
+  const uint32_t r1 = min(e1 & 0x7fffu, (uint32_t)kCapRec - 1u);
+  const uint64_t k0 = S.recK[r0], k1 = S.recK[r1];
+  const bool o0 = e0 != kNone, o1 = e1 != kNone;
+  const bool hit0 = o0 && !(bghost && (k0 - K.cW >= K.W)) && (k0 - s + K.hw <= K.width);
+  const bool hit1 = o1 && !(bghost && (k1 - K.cW >= K.W)) && (k1 - s + K.hw <= K.width);
+  n_qprobe += (o0 ? 1u : 0u) + (o1 ? 1u : 0u);
+  if (hit0) emit_match(a, r0, ib, jb);
+  if (hit1) emit_match(a, r1, ib, jb);
+  const int deep = ((o0 && (e0 >> 15)) || (o1 && (e1 >> 15))) ? 1 : 0;
+  return (e && hn > 1) ? 2 : deep;
+}
+
+// Warp-wide walk for long runs (expected run >= 32 records per outer per
+// bucket): each warp takes its outers one at a time, with the outer's state
+// in registers, and loads all nch chunks of its run at once (chunk k = window
+// offsets [32k, 32k + 32)); nch covers the expected run plus ~3 sigma.  An
+// outer whose last chunk is still full is flagged for continue_pass
+// (off = 32 * nch).  Same record semantics as window_pass.
+constexpr int kMaxCh = 12;
+template <bool SIDE_A>
+__device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t lo, uint32_t hi,
+                                      int nch, PassSt st) {
+  JoinSmem& S = join_smem();
+  uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
+  bool overflow = st.overflow;
+  const JoinPlan& P = a.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t Mi = 1u << P.list[SIDE_A ? 1 : 3].bits;
+  const uint64_t* __restrict__ kin = a.key[SIDE_A ? 1 : 3];
+  const int aib = P.list[1].bits;
+  const JoinK K = make_k(a, cW);
+  const bool can_cont = (uint32_t)(32 * nch) < Mi;
+  unsigned long long* tr = (RFR_JOIN_TRACE && a.dbg && blockIdx.x == 0 && threadIdx.x == 0 &&
+                            cW == ((P.bucket_begin + 1) << K.sh))
+                               ? a.dbg + 128 + (SIDE_A ? 0 : 64)
+                               : nullptr;
+  int trn = 0;
+  for (uint32_t i = lo; i < hi; i++) {
+    const uint32_t pos = (SIDE_A ? S.apos : S.bpos)[i];
+    const uint32_t rot = (SIDE_A ? S.arot : S.brot)[i];
+    const uint64_t x = (SIDE_A ? S.ax : S.bx)[i];
+    if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64();
+    uint64_t kv[kMaxCh];
+#pragma unroll
+    for (int k = 0; k < kMaxCh; k++) {
+      const uint32_t q = (uint32_t)(k * 32 + lane);
+      kv[k] = (k < nch && q < Mi) ? __ldg(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
+    }
+    if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
+    uint32_t mc = 0, nq = 0, em = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxCh; k++) {
+      if (k < nch) {
+        const uint32_t q = (uint32_t)(k * 32 + lane);
+        const uint32_t o = pos + q;
+        const uint32_t j = (rot + o) & (Mi - 1);
+        const uint64_t sv = x + kv[k];
+        const uint64_t rel = sv - cW;
+        const bool valid = q < Mi;
+        const bool m = valid && o < Mi && rel < K.W;
+        const bool e = m || (valid && (rel - K.W) < K.H);
+        em = __ballot_sync(FULL, e);
+        mc += __popc(__ballot_sync(FULL, m));
+        n_stat += e ? 1u : 0u;
+        if (SIDE_A) {
+          const uint32_t ne = __popc(em);
+          if (wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
+          if (!overflow && e) {
+            const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
+            S.recK[r] = sv;
+            S.recI[r] = (i << aib) | j;
+            S.t1[home_of(rel, K.sh - kL1Log, kL1Log)] = (uint16_t)r;
+          }
+          if (!overflow) wfill += ne;
+        } else {
+          const int deep = probe_b_l1_fast(S, a, K, e, sv, !m, i, j, n_qprobe);
+          const uint32_t dm = __ballot_sync(FULL, deep != 0);
+          if (deep) {
+            const uint32_t kk = nq + __popc(dm & lt_mask);
+            S.qK[wid][kk] = sv;
+            S.qJ[wid][kk] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
+            S.qB[wid][kk] = (uint16_t)i;
+          }
+          nq += __popc(dm);
+          if (nq > (uint32_t)(kStageB - 32)) {  // keep room for one more chunk
+            n_qprobe += process_staged(a, cW, nq);
+            nq = 0;
+          }
+        }
+      }
+    }
+    if (!SIDE_A && nq) n_qprobe += process_staged(a, cW, nq);
+    if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | ((em == FULL && can_cont) ? kFlagCont : 0u);
+  }
+  if (RFR_JOIN_TRACE && tr && trn < 63) tr[trn++] = clock64();
+  return PassSt{wfill, n_stat, n_qprobe, overflow};
 }
 
 // Build levels 2 and 3 from the level-1 losers (plain stores + read-back).
 // Called by every thread after the barrier that follows the level-1 stores;
 // returns after a barrier with S.n4 / S.ovf valid.
-__device__ __forceinline__ void build_index_levels(JoinSmem& S, const JoinPlan& P, uint64_t cW) {
+__device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) {
+  JoinSmem& S = join_smem();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -492,6 +648,140 @@ __device__ __forceinline__ void clear_index(JoinSmem& S) {
   for (int i = threadIdx.x; i < (1 << kL3Log) / 8; i += kJoinThreads) p3[i] = f4;
 }
 
+// Slow path for a skewed bucket whose A side overflowed the warp partitions:
+// warp 0 fills chunks of at most kCapRec records (halving the chunk when the
+// index overflows), and every chunk re-streams B.  Out of line: rare, and it
+// keeps the fast loop's register allocation small.
+__device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_t aLo, uint32_t aHi,
+                                         uint32_t bLo, uint32_t bHi, int gsB, uint32_t& n_ins_r,
+                                         uint32_t& n_q_r, uint32_t& n_qprobe_r,
+                                         uint32_t& n_chunks_r) {
+  JoinSmem& S = join_smem();
+  const JoinPlan& P = a.P;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t MoA = 1u << P.list[0].bits, MiA = 1u << P.list[1].bits;
+  const uint64_t* __restrict__ kA = a.key[1];
+  const int sh = 64 - P.r;
+  const uint64_t W = 1ull << sh;
+  const uint64_t H = P.half;
+  uint32_t n_ins = n_ins_r, n_q = n_q_r, n_qprobe = n_qprobe_r, n_chunks = n_chunks_r;
+  // ---- slow path (skewed bucket): chunks of kCapRec records filled by warp 0
+  __syncthreads();
+  if (tid == 0) {
+    S.cur_i = 0;
+    S.cur_t = 0;
+  }
+  for (uint32_t i = tid; i < MoA; i += kJoinThreads) S.amain[i] = 0;
+  __syncthreads();
+  uint32_t chunk_cap = (uint32_t)kCapRec;  // halves when a chunk overflows the index
+  while (true) {
+    n_chunks++;
+    clear_index(S);
+    const uint32_t save_i = S.cur_i, save_t = S.cur_t;
+    __syncthreads();
+    if (tid == 0) {
+      S.n4 = 0;
+      S.ovf = 0;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t i = S.cur_i, t = S.cur_t, fill = 0;
+      while (i < MoA) {
+        const uint32_t pos = S.apos[i], rot = S.arot[i];
+        const uint64_t x = S.ax[i];
+        bool full = false;
+        while (true) {
+          const uint32_t q = t + lane;
+          const bool valid = q < MiA;
+          const uint32_t o = pos + q;
+          const uint32_t j = (rot + o) & (MiA - 1);
+          const uint64_t s = x + (valid ? __ldg(kA + j) : 0ull);
+          const uint64_t rel = s - cW;
+          const bool m = valid && o < MiA && rel < W;
+          const bool e = m || (valid && (rel - W) < H);
+          const uint32_t em = __ballot_sync(FULL, e);
+          const uint32_t ne_all = __popc(em);
+          const uint32_t room = chunk_cap - fill;
+          const uint32_t take = ne_all < room ? ne_all : room;  // emitted lanes are a prefix
+          if ((uint32_t)lane < take) {
+            // spread the chunk round-robin over the warp partitions
+            const uint32_t idx = fill + lane;
+            const uint32_t r = (idx % kJoinWarps) * kPart + idx / kJoinWarps;
+            S.recK[r] = s;
+            S.recI[r] = (i << P.list[1].bits) | j;
+          }
+          const uint32_t mm = __ballot_sync(FULL, m) & (take >= 32 ? FULL : ((1u << take) - 1u));
+          if (lane == 0) S.amain[i] += __popc(mm);
+          fill += take;
+          t += take;
+          n_ins += ((uint32_t)lane < take) ? 1u : 0u;
+          if (take < ne_all) {  // chunk full inside this run
+            full = true;
+            break;
+          }
+          if (ne_all < 32 || t >= MiA) break;
+        }
+        if (full) break;
+        i++;
+        t = 0;
+      }
+      if (lane == 0) {
+        S.cur_i = i;
+        S.cur_t = t;
+      }
+      if (lane < kJoinWarps)
+        S.wcnt[lane] = fill / kJoinWarps + ((uint32_t)lane < fill % kJoinWarps ? 1u : 0u);
+    }
+    __syncthreads();
+    {  // every warp claims level-1 homes for its partition, then the levels
+      const uint32_t nw = S.wcnt[wid];
+      for (uint32_t e = lane; e < nw; e += 32) {
+        const uint32_t r = wid * kPart + e;
+        S.t1[home_of(S.recK[r] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
+      }
+    }
+    __syncthreads();
+    build_index_levels(P, cW);
+    if (S.ovf) {  // too many colliding records: redo this chunk with half the records
+      __syncthreads();
+      if (tid == 0) {
+        S.cur_i = save_i;
+        S.cur_t = save_t;
+      }
+      for (uint32_t i = tid; i < MoA; i += kJoinThreads)
+        if (i >= save_i) S.amain[i] = 0;  // recounted by the smaller chunks
+      chunk_cap = chunk_cap > 64u ? chunk_cap / 2 : 64u;
+      __syncthreads();
+      continue;
+    }
+    const bool done = S.cur_i >= MoA;
+    uint32_t dummy_fill = 0;
+    bool dummy_ovf = false;
+    if (gsB > 32)
+      {
+      const PassSt o_ = run_pass<false>(a, cW, bLo, bHi, gsB >> 5, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
+    else
+      {
+      const PassSt o_ = window_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
+    __syncwarp();
+    {
+      const PassSt o_ = continue_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
+    __syncthreads();
+    if (done) break;
+  }
+  n_ins_r = n_ins;
+  n_q_r = n_q;
+  n_qprobe_r = n_qprobe;
+  n_chunks_r = n_chunks;
+}
+
 __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     join_kernel(const __grid_constant__ JoinArgs a, int gsA, int gsB) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -512,11 +802,11 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   const uint64_t c_begin = P.bucket_begin + nbk * blockIdx.x / gridDim.x;
   const uint64_t c_end = P.bucket_begin + nbk * (blockIdx.x + 1) / gridDim.x;
   if (c_begin >= c_end) return;
-  unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && tid == 0) ? a.dbg : nullptr;
+  unsigned long long* dbg = (RFR_JOIN_TRACE && a.dbg && blockIdx.x == 0 && tid == 0) ? a.dbg : nullptr;
   int dbg_n = 0;
 #define RFR_MARK()                                   \
   do {                                               \
-    if (dbg && dbg_n < 256) dbg[dbg_n++] = clock64(); \
+    if (RFR_JOIN_TRACE && dbg && dbg_n < 120) dbg[dbg_n++] = clock64(); \
   } while (0)
   RFR_MARK();
 
@@ -552,9 +842,21 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     // ---- fast path: A windows + continuations into the warp partitions
     bool wovf = false;
     uint32_t wfill = 0;
-    window_pass<true>(S, a, cW, aLo, aHi, gsA, wfill, n_ins, n_qprobe, wovf);
+    if (gsA > 32)
+      {
+      const PassSt o_ = run_pass<true>(a, cW, aLo, aHi, gsA >> 5, PassSt{wfill, n_ins, n_qprobe, wovf});
+      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
+    }
+    else
+      {
+      const PassSt o_ = window_pass<true>(a, cW, aLo, aHi, gsA, PassSt{wfill, n_ins, n_qprobe, wovf});
+      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
+    }
     __syncwarp();
-    continue_pass<true>(S, a, cW, aLo, aHi, gsA, wfill, n_ins, n_qprobe, wovf);
+    {
+      const PassSt o_ = continue_pass<true>(a, cW, aLo, aHi, gsA, PassSt{wfill, n_ins, n_qprobe, wovf});
+      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
+    }
     if (lane == 0) {
       S.wcnt[wid] = wfill;
       if (wovf) S.ovf = 1;
@@ -563,16 +865,28 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     __syncthreads();
     bool overflowed = S.ovf != 0;
     if (!overflowed) {
-      build_index_levels(S, P, cW);
+      build_index_levels(P, cW);
       overflowed = S.ovf != 0;
     }
     RFR_MARK();
     if (!overflowed) {
       uint32_t dummy_fill = 0;
       bool dummy_ovf = false;
-      window_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      if (gsB > 32)
+        {
+      const PassSt o_ = run_pass<false>(a, cW, bLo, bHi, gsB >> 5, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
+      else
+        {
+      const PassSt o_ = window_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
       __syncwarp();
-      continue_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
+      {
+      const PassSt o_ = continue_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
+      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
+    }
       __syncwarp();
       for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
       for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
@@ -582,104 +896,8 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       continue;
     }
 
-    // ---- slow path (skewed bucket): chunks of kCapRec records filled by warp 0
-    __syncthreads();
-    if (tid == 0) {
-      S.cur_i = 0;
-      S.cur_t = 0;
-    }
-    for (uint32_t i = tid; i < MoA; i += kJoinThreads) S.amain[i] = 0;
-    __syncthreads();
-    uint32_t chunk_cap = (uint32_t)kCapRec;  // halves when a chunk overflows the index
-    while (true) {
-      n_chunks++;
-      clear_index(S);
-      const uint32_t save_i = S.cur_i, save_t = S.cur_t;
-      __syncthreads();
-      if (tid == 0) {
-        S.n4 = 0;
-        S.ovf = 0;
-      }
-      __syncthreads();
-      if (wid == 0) {
-        uint32_t i = S.cur_i, t = S.cur_t, fill = 0;
-        while (i < MoA) {
-          const uint32_t pos = S.apos[i], rot = S.arot[i];
-          const uint64_t x = S.ax[i];
-          bool full = false;
-          while (true) {
-            const uint32_t q = t + lane;
-            const bool valid = q < MiA;
-            const uint32_t o = pos + q;
-            const uint32_t j = (rot + o) & (MiA - 1);
-            const uint64_t s = x + (valid ? __ldg(kA + j) : 0ull);
-            const uint64_t rel = s - cW;
-            const bool m = valid && o < MiA && rel < W;
-            const bool e = m || (valid && (rel - W) < H);
-            const uint32_t em = __ballot_sync(FULL, e);
-            const uint32_t ne_all = __popc(em);
-            const uint32_t room = chunk_cap - fill;
-            const uint32_t take = ne_all < room ? ne_all : room;  // emitted lanes are a prefix
-            if ((uint32_t)lane < take) {
-              // spread the chunk round-robin over the warp partitions
-              const uint32_t idx = fill + lane;
-              const uint32_t r = (idx % kJoinWarps) * kPart + idx / kJoinWarps;
-              S.recK[r] = s;
-              S.recI[r] = (i << P.list[1].bits) | j;
-            }
-            const uint32_t mm = __ballot_sync(FULL, m) & (take >= 32 ? FULL : ((1u << take) - 1u));
-            if (lane == 0) S.amain[i] += __popc(mm);
-            fill += take;
-            t += take;
-            n_ins += ((uint32_t)lane < take) ? 1u : 0u;
-            if (take < ne_all) {  // chunk full inside this run
-              full = true;
-              break;
-            }
-            if (ne_all < 32 || t >= MiA) break;
-          }
-          if (full) break;
-          i++;
-          t = 0;
-        }
-        if (lane == 0) {
-          S.cur_i = i;
-          S.cur_t = t;
-        }
-        if (lane < kJoinWarps)
-          S.wcnt[lane] = fill / kJoinWarps + ((uint32_t)lane < fill % kJoinWarps ? 1u : 0u);
-      }
-      __syncthreads();
-      {  // every warp claims level-1 homes for its partition, then the levels
-        const uint32_t nw = S.wcnt[wid];
-        for (uint32_t e = lane; e < nw; e += 32) {
-          const uint32_t r = wid * kPart + e;
-          S.t1[home_of(S.recK[r] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
-        }
-      }
-      __syncthreads();
-      build_index_levels(S, P, cW);
-      if (S.ovf) {  // too many colliding records: redo this chunk with half the records
-        __syncthreads();
-        if (tid == 0) {
-          S.cur_i = save_i;
-          S.cur_t = save_t;
-        }
-        for (uint32_t i = tid; i < MoA; i += kJoinThreads)
-          if (i >= save_i) S.amain[i] = 0;  // recounted by the smaller chunks
-        chunk_cap = chunk_cap > 64u ? chunk_cap / 2 : 64u;
-        __syncthreads();
-        continue;
-      }
-      const bool done = S.cur_i >= MoA;
-      uint32_t dummy_fill = 0;
-      bool dummy_ovf = false;
-      window_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
-      __syncwarp();
-      continue_pass<false>(S, a, cW, bLo, bHi, gsB, dummy_fill, n_q, n_qprobe, dummy_ovf);
-      __syncthreads();
-      if (done) break;
-    }
+    // ---- slow path (skewed bucket)
+    slow_bucket(a, cW, aLo, aHi, bLo, bHi, gsB, n_ins, n_q, n_qprobe, n_chunks);
     for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
     for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
     __syncthreads();

@@ -1,3 +1,4 @@
+#include <cmath>
 // rfr_search.cu -- the recombination search (meet in the middle) on sm_100a.
 //
 // Replaces the reference's backend e hot loops (pkg/src/polyfactor/
@@ -262,8 +263,18 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
     a.dbg = dbg;
   }
   // lane groups: about twice the expected run of one outer in one bucket
+  // Lanes per outer window: a lane group of 2 * lambda lanes for short runs
+  // (lambda = expected records per outer per bucket); for lambda >= 32 the
+  // warp-wide run pass with ceil((lambda + 3 sqrt(lambda) + 8) / 32) chunks
+  // (encoded as gs = 32 * chunks > 32).
   auto gs_for = [&](int inner_bits) {
     int run_log = inner_bits - P.r;  // log2 expected records per outer per bucket
+    if (run_log >= 5) {
+      const double lam = std::ldexp(1.0, run_log);
+      int nch = (int)std::ceil((lam + 3.0 * std::sqrt(lam) + 8.0) / 32.0);
+      if (nch > kMaxCh) nch = kMaxCh;  // longer runs continue in continue_pass
+      return 32 * nch;
+    }
     int g = run_log + 1;
     g = g < 3 ? 3 : (g > 5 ? 5 : g);
     return 1 << g;
@@ -278,10 +289,11 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
             P.r, 1 << P.list[0].bits, 1 << P.list[1].bits, 1 << P.list[2].bits,
             1 << P.list[3].bits, h[1] - h[0]);
     for (int side = 0; side < 2; side++) {
-      fprintf(stderr, "[rfr trace] %s rounds (issue -> after loads+classify, -> next round):", side ? "B" : "A");
+      fprintf(stderr, "[rfr trace] %s marks (cycles between marks; p = before processing):", side ? "B" : "A");
       const unsigned long long* t = h + 128 + side * 64;
-      for (int k = 0; k + 2 < 64 && t[k + 2]; k += 2)
-        fprintf(stderr, " %llu/%llu", (t[k + 1] & ~(1ull << 63)) - t[k], t[k + 2] - (t[k + 1] & ~(1ull << 63)));
+      for (int k = 0; k + 1 < 64 && t[k + 1]; k++)
+        fprintf(stderr, " %llu%s", (t[k + 1] & ~(1ull << 63)) - (t[k] & ~(1ull << 63)),
+                (t[k + 1] >> 63) ? "p" : "");
       fprintf(stderr, "\n");
     }
     for (int b = 0; b < 6; b++) {  // marks: bucket start, A gen, A index, B pass, end barrier
