@@ -74,7 +74,7 @@ struct Ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  DevVec keys, rho, raw, post, ctr;
+  DevVec keys, rho, raw, post, ctr, rotc, splits;
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
@@ -118,12 +118,13 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   if (r > 61 - hb) r = 61 - hb;  // keep the window radius <= W / 8
   if (r < 2) return rfr_fail(RFR_E_ARG, "window too wide for one plan (internal)");
   auto clampi = [](int v, int lo_, int hi_) { return v < lo_ ? lo_ : (v > hi_ ? hi_ : v); };
-  // outer lists sized so each outer contributes ~2^lam records per bucket,
-  // inner lists capped at 2^kMaxInnerBits (L2 resident)
+  // outer lists sized so each outer contributes ~2^lam records per bucket
+  // (long runs: the join's warp-wide run pass), inner lists
+  // capped at 2^kMaxInnerBits entries (streamed, so they need not fit L2)
   static int lam = -1;
   if (lam < 0) {
     const char* e = getenv("RFR_LAMBDA_LOG");
-    lam = e ? atoi(e) : 3;
+    lam = e ? atoi(e) : 8;
   }
   const int ao = clampi(alpha - r - lam, alpha > kMaxInnerBits ? alpha - kMaxInnerBits : 0, kMaxOuterBits);
   const int bo = clampi(beta - r - lam, beta > kMaxInnerBits ? beta - kMaxInnerBits : 0, kMaxOuterBits);
@@ -223,11 +224,14 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   rc = ensure_list_buffers(P0);
   if (rc) return rc;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
-  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), s));
+  RFR_CUDA_OK(g.rotc.ensure(4 * kRotSlots * sizeof(uint32_t)));
+  RFR_CUDA_OK(g.splits.ensure(lists_split_words(P0) * sizeof(uint32_t)));
+  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p,
+                           (uint32_t*)g.splits.p, s));
   {
     int maxbits = 0;
     for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
-    g_launches += 1 + (maxbits > kBaseBits ? maxbits - kBaseBits : 0);
+    g_launches += 1 + (maxbits > kBaseBits ? 2 * (maxbits - kBaseBits) : 0);
   }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
   for (auto& w : wins) {
@@ -321,6 +325,8 @@ int rfr_shutdown(void) {
   g.rho.release();
   g.raw.release();
   g.post.release();
+  g.rotc.release();
+  g.splits.release();
   g.vprof.release();
   g.vpats.release();
   g.vpmod.release();

@@ -10,11 +10,12 @@
 namespace rfr {
 
 // Largest quarter list walked by the join (2^23 entries = 64 MB of keys).
-constexpr int kMaxInnerBits = 23;
+constexpr int kMaxInnerBits = 28;  // inner lists up to 2^28 entries (12 B each, x2 ping-pong)
 // Outer lists live in shared memory of the join kernel.
 constexpr int kMaxOuterBits = 9;
 // Sorted base block built in shared memory by the list builder.
 constexpr int kBaseBits = 12;
+constexpr int kRotSlots = 64;  // per-list rotation counters of the merge levels
 
 // One quarter list of the folded pattern space: subset sums of
 // keys[first, first + bits) (negated for the B half), sorted ascending.

@@ -6,8 +6,9 @@
 
 namespace rfr {
 size_t join_smem_bytes();
+size_t lists_split_words(const JoinPlan& P);
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
-                         cudaStream_t s);
+                         uint32_t* d_rot, uint32_t* d_split, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,

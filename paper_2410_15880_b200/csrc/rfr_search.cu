@@ -33,49 +33,116 @@ __device__ __forceinline__ uint64_t elem_key(const uint64_t* keys, const ListSpe
   return L.negate ? (0ull - k) : k;
 }
 
-// One CTA per list: all 2^b subset sums (b = min(bits, kBaseBits)) of the
-// list's first b elements, bitonic-sorted in shared memory.
+// Select element i of a 4-array held in kernel parameters without dynamic
+// indexing (which would copy the whole parameter struct to local memory).
+template <class T>
+__device__ __forceinline__ T pick4(const T (&v)[4], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : (i == 2 ? v[2] : v[3]));
+}
+__device__ __forceinline__ ListSpec pick_list(const JoinPlan& P, int i) {
+  ListSpec L;
+  L.first = i == 0 ? P.list[0].first : (i == 1 ? P.list[1].first : (i == 2 ? P.list[2].first : P.list[3].first));
+  L.bits = i == 0 ? P.list[0].bits : (i == 1 ? P.list[1].bits : (i == 2 ? P.list[2].bits : P.list[3].bits));
+  L.negate = i == 0 ? P.list[0].negate : (i == 1 ? P.list[1].negate : (i == 2 ? P.list[2].negate : P.list[3].negate));
+  L.pat_shift = i == 0 ? P.list[0].pat_shift : (i == 1 ? P.list[1].pat_shift : (i == 2 ? P.list[2].pat_shift : P.list[3].pat_shift));
+  return L;
+}
+
+// One CTA per list: the 2^b sorted subset sums (b = min(bits, kBaseBits)) of
+// the list's first b elements, by b doubling levels in shared memory:
+// L_{i+1} = merge(L_i, rotate(L_i + v_i)), every element placed by its rank
+// (its index plus a binary search in the other sorted half; ties put L_i
+// first), ping-ponging between two buffers.
+struct BaseSmem {
+  uint64_t k[2][1 << kBaseBits];
+  uint32_t p[2][1 << kBaseBits];
+};
+
+// # of entries of the ascending rotated sequence s[(r + j) mod n] + v, j < n,
+// that are < x (strict) or <= x (!strict)
+__device__ __forceinline__ uint32_t rank_rot(const uint64_t* s, uint32_t n, uint32_t r, uint64_t v,
+                                             uint64_t x, bool strict) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint64_t y = s[(r + mid) & (n - 1)] + v;
+    if (strict ? (y < x) : (y <= x)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __restrict__ keys,
-                                                          JoinPlan P, ListBufs out) {
-  __shared__ uint64_t sk[1 << kBaseBits];
-  __shared__ uint32_t sp[1 << kBaseBits];
-  const ListSpec L = P.list[blockIdx.x];
+                                                          JoinPlan P, ListBufs out, uint32_t* rot) {
+  extern __shared__ __align__(16) unsigned char base_raw[];
+  BaseSmem& S = *reinterpret_cast<BaseSmem*>(base_raw);
+  const ListSpec L = pick_list(P, blockIdx.x);
   const int b = L.bits < kBaseBits ? L.bits : kBaseBits;
   const int len = 1 << b;
-  uint64_t ek[kBaseBits];
-  for (int i = 0; i < b; i++) ek[i] = elem_key(keys, L, i);
-  for (int p = threadIdx.x; p < len; p += blockDim.x) {
-    uint64_t s = 0;
-    for (int i = 0; i < b; i++)
-      if ((p >> i) & 1) s += ek[i];
-    sk[p] = s;
-    sp[p] = (uint32_t)p;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    S.k[0][0] = 0;
+    S.p[0][0] = 0;
   }
   __syncthreads();
-  for (int k = 2; k <= len; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < len; i += blockDim.x) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          bool up = ((i & k) == 0);
-          uint64_t a = sk[i], c = sk[ixj];
-          if ((a > c) == up) {
-            sk[i] = c;
-            sk[ixj] = a;
-            uint32_t t = sp[i];
-            sp[i] = sp[ixj];
-            sp[ixj] = t;
-          }
-        }
+  int cur = 0;
+  for (int i = 0; i < b; i++) {
+    const uint32_t n = 1u << i;
+    const uint64_t v = elem_key(keys, L, i);
+    const uint64_t* A = S.k[cur];
+    // rotation start: # of A < -v (0 when v == 0 or when every A is < -v)
+    uint32_t r = 0;
+    if (v != 0) {
+      uint32_t lo = 0, hi = n;
+      const uint64_t t = 0ull - v;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (A[mid] < t) lo = mid + 1;
+        else hi = mid;
       }
-      __syncthreads();
+      r = lo == n ? 0 : lo;
     }
+    uint64_t* Ok = S.k[cur ^ 1];
+    uint32_t* Op = S.p[cur ^ 1];
+    for (uint32_t e = tid; e < 2 * n; e += blockDim.x) {
+      if (e < n) {  // A[e]: after e A's and the B's strictly below it
+        const uint64_t x = A[e];
+        const uint32_t d = e + rank_rot(A, n, r, v, x, true);
+        Ok[d] = x;
+        Op[d] = S.p[cur][e];
+      } else {  // B'[j] = A[(r + j) mod n] + v: after j B's and the A's <= it
+        const uint32_t j = e - n, src = (r + j) & (n - 1);
+        const uint64_t x = A[src] + v;
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (A[mid] <= x) lo = mid + 1;
+          else hi = mid;
+        }
+        Ok[j + lo] = x;
+        Op[j + lo] = S.p[cur][src] | (1u << i);
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
   }
-  uint64_t* ok = out.k[blockIdx.x];
-  uint32_t* op = out.p[blockIdx.x];
-  for (int p = threadIdx.x; p < len; p += blockDim.x) {
-    ok[p] = sk[p];
-    op[p] = sp[p];
+  uint64_t* ok = pick4(out.k, blockIdx.x);
+  uint32_t* op = pick4(out.p, blockIdx.x);
+  for (int p = tid; p < len; p += blockDim.x) {
+    ok[p] = S.k[cur][p];
+    op[p] = S.p[cur][p];
+  }
+  // rotation counters of the merge levels: zero them, and seed the first
+  // level's (# sums < -v_b, v_b = key of element b)
+  uint32_t* rc = rot + blockIdx.x * kRotSlots;
+  for (int k = tid; k < kRotSlots; k += blockDim.x) rc[k] = 0;
+  __syncthreads();
+  if (L.bits > b) {
+    const uint64_t thr = 0ull - elem_key(keys, L, b);
+    uint32_t c = 0;
+    for (int p = tid; p < len; p += blockDim.x) c += S.k[cur][p] < thr ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((tid & 31) == 0 && c) atomicAdd(rc + b, c);
   }
 }
 
@@ -113,51 +180,152 @@ __device__ __forceinline__ uint32_t count_below(const uint64_t* __restrict__ a, 
 
 // One doubling level for every list that has it: L (2^k sorted sums of the
 // list's first k elements) -> merge(L, rotate(L + v_k)), v_k the key of
-// element k.  Merge path, ITEMS outputs per thread.
+// element k; the rotated copy B'[j] = L[(rot + j) mod 2^k] + v_k is ascending.
+// Each CTA produces one tile of kMergeTile outputs between two merge-path
+// splits found by lists_split_kernel; the tile's inputs are
+// staged in shared memory with coalesced loads, every thread merges
+// kMergeItems outputs from shared memory, and the tile is stored coalesced.
+// rot comes from the counter the previous level accumulated (# sums < -v_k),
+// and this level accumulates the next one, so no thread ever binary-searches
+// a list in global memory for it.
 constexpr int kMergeItems = 8;
-__global__ void __launch_bounds__(256) lists_merge_kernel(const uint64_t* __restrict__ keys,
+constexpr int kMergeThreads = 256;
+constexpr int kMergeTile = kMergeItems * kMergeThreads;
+
+// Bank-conflict-free tile layout (XOR swizzle inside each 128-byte row): the
+// staging loads, the per-thread runs of kMergeItems and the coalesced
+// read-out all hit distinct banks.
+__device__ __forceinline__ uint32_t kswz(uint32_t i) { return i ^ ((i >> 4) & 15u); }
+__device__ __forceinline__ uint32_t pswz(uint32_t i) { return i ^ ((i >> 5) & 7u); }
+
+__device__ __forceinline__ uint32_t rot_of(const uint32_t* rc, int k, uint32_t n) {
+  const uint32_t c = rc[k];
+  return c >= n ? 0u : c;
+}
+
+// Merge-path splits of one doubling level, one warp per tile boundary
+// (32-ary search: ~5 dependent steps for 2^23-entry lists); all boundaries of
+// all lists are searched concurrently so the merge CTAs start at their loads.
+// split[li * stride + t] = # A elements before output tile t.
+__global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __restrict__ keys,
                                                           JoinPlan P, int k, ListBufs in,
-                                                          ListBufs out) {
+                                                          const uint32_t* __restrict__ rot,
+                                                          uint32_t* __restrict__ split, int stride) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x * 8u + (threadIdx.x >> 5);
   const int li = blockIdx.y;
-  const ListSpec L = P.list[li];
+  const ListSpec L = pick_list(P, li);
   if (L.bits <= k) return;
   const uint32_t n = 1u << k;
-  const uint64_t* __restrict__ A = in.k[li];
-  const uint32_t* __restrict__ Ap = in.p[li];
-  uint64_t* __restrict__ O = out.k[li];
-  uint32_t* __restrict__ Op = out.p[li];
+  const uint32_t ntiles = (2u * n + kMergeTile - 1) / kMergeTile;
+  if (w > ntiles) return;
+  const uint64_t* __restrict__ A = pick4(in.k, li);
+  const uint64_t v = elem_key(keys, L, k);
+  const uint32_t r0 = rot_of(rot + li * kRotSlots, k, n);
+  const uint32_t mask = n - 1;
+  auto Bk = [&](uint32_t j) { return __ldg(A + ((r0 + j) & mask)) + v; };
+  const uint32_t d = min(w * (uint32_t)kMergeTile, 2u * n);
+  // smallest i with A[i] > B'[d - 1 - i] (A first on ties)
+  uint32_t lo = d > n ? d - n : 0, hi = d < n ? d : n;
+  while (hi > lo) {
+    const uint32_t span = hi - lo;
+    if (span <= 32) {
+      const uint32_t q = lo + lane;
+      const bool pr = (uint32_t)lane < span && __ldg(A + q) <= Bk(d - 1 - q);
+      lo += __popc(__ballot_sync(0xffffffffu, pr));
+      break;
+    }
+    const uint32_t q = lo + (uint32_t)(((uint64_t)span * lane) >> 5);
+    const bool pr = __ldg(A + q) <= Bk(d - 1 - q);
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, pr));
+    const uint32_t qc1 = __shfl_sync(0xffffffffu, q, (c > 0 ? c : 1) - 1);
+    const uint32_t qc = __shfl_sync(0xffffffffu, q, c < 32 ? c : 31);
+    if (c > 0) lo = qc1 + 1;
+    if (c < 32) hi = qc;
+  }
+  if (lane == 0) split[li * stride + w] = lo;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64_t* __restrict__ keys,
+                                                                    JoinPlan P, int k,
+                                                                    ListBufs in, ListBufs out,
+                                                                    uint32_t* rot,
+                                                                    const uint32_t* __restrict__ split,
+                                                                    int stride) {
+  __shared__ uint64_t sK[kMergeTile];
+  __shared__ uint32_t sP[kMergeTile];
+  const int li = blockIdx.y;
+  const ListSpec L = pick_list(P, li);
+  if (L.bits <= k) return;
+  const uint32_t n = 1u << k;
+  const uint32_t d0 = blockIdx.x * (uint32_t)kMergeTile;
+  if (d0 >= 2u * n) return;
+  const uint64_t* __restrict__ A = pick4(in.k, li);
+  const uint32_t* __restrict__ Ap = pick4(in.p, li);
+  uint64_t* __restrict__ O = pick4(out.k, li);
+  uint32_t* __restrict__ Op = pick4(out.p, li);
+  uint32_t* rc = rot + li * kRotSlots;
   const uint64_t v = elem_key(keys, L, k);
   const uint32_t bit = 1u << k;
-  const uint32_t rot = rotation_start(A, n, v);
+  const uint32_t r0 = rot_of(rc, k, n);
   const uint32_t mask = n - 1;
-  const uint64_t d0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
-  if (d0 >= 2ull * n) return;
-  const uint32_t d = (uint32_t)d0;
-  // B'[j] = A[(rot + j) & mask] + v is ascending in j
-  auto Bk = [&](uint32_t j) { return __ldg(A + ((rot + j) & mask)) + v; };
-  uint32_t lo = d > n ? d - n : 0, hi = d < n ? d : n;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t a0 = __ldg(split + li * stride + blockIdx.x);
+  const uint32_t a1 = __ldg(split + li * stride + blockIdx.x + 1);
+  const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
+  const uint32_t na = a1 - a0, nb = tile - na;
+  const uint32_t b0 = d0 - a0;
+  for (uint32_t t = tid; t < na; t += kMergeThreads) {
+    sK[kswz(t)] = __ldg(A + a0 + t);
+    sP[pswz(t)] = __ldg(Ap + a0 + t);
+  }
+  for (uint32_t t = tid; t < nb; t += kMergeThreads) {
+    const uint32_t jj = (r0 + b0 + t) & mask;
+    sK[kswz(na + t)] = __ldg(A + jj) + v;
+    sP[pswz(na + t)] = __ldg(Ap + jj) | bit;
+  }
+  __syncthreads();
+  // per-thread merge of kMergeItems outputs from the staged tile
+  const uint32_t dt = min((uint32_t)(tid * kMergeItems), tile);
+  uint32_t lo = dt > nb ? dt - nb : 0, hi = dt < na ? dt : na;
   while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(A + mid) <= Bk(d - 1 - mid)) lo = mid + 1;
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sK[kswz(mid)] <= sK[kswz(na + dt - 1 - mid)]) lo = mid + 1;
     else hi = mid;
   }
-  uint32_t i = lo, j = d - lo;
+  uint32_t i = lo, j = dt - lo;
+  uint64_t ok[kMergeItems];
+  uint32_t op[kMergeItems];
 #pragma unroll
   for (int t = 0; t < kMergeItems; t++) {
-    bool takeA;
-    if (i >= n) takeA = false;
-    else if (j >= n) takeA = true;
-    else takeA = __ldg(A + i) <= Bk(j);
-    if (takeA) {
-      O[d + t] = __ldg(A + i);
-      Op[d + t] = __ldg(Ap + i);
-      i++;
-    } else {
-      uint32_t jj = (rot + j) & mask;
-      O[d + t] = __ldg(A + jj) + v;
-      Op[d + t] = __ldg(Ap + jj) | bit;
-      j++;
+    const bool takeA = j >= nb || (i < na && sK[kswz(i)] <= sK[kswz(na + j)]);
+    const uint32_t src = takeA ? i : na + j;
+    ok[t] = sK[kswz(src)];
+    op[t] = sP[pswz(src)];
+    if (takeA) i++;
+    else j++;
+  }
+  __syncthreads();
+  const uint32_t cnt = dt < tile ? min((uint32_t)kMergeItems, tile - dt) : 0u;
+#pragma unroll
+  for (int t = 0; t < kMergeItems; t++)
+    if ((uint32_t)t < cnt) {
+      sK[kswz(dt + t)] = ok[t];
+      sP[pswz(dt + t)] = op[t];
     }
+  __syncthreads();
+  for (uint32_t t = tid; t < tile; t += kMergeThreads) {
+    O[d0 + t] = sK[kswz(t)];
+    Op[d0 + t] = sP[pswz(t)];
+  }
+  // next level's rotation start: # outputs < -v_{k+1}
+  if (L.bits > k + 1) {
+    const uint64_t thr = 0ull - elem_key(keys, L, k + 1);
+    uint32_t c = 0;
+#pragma unroll
+    for (int t = 0; t < kMergeItems; t++) c += ((uint32_t)t < cnt && ok[t] < thr) ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && c) atomicAdd(rc + k + 1, c);
   }
 }
 
@@ -222,17 +390,34 @@ namespace rfr {
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
 
+// d_split: 4 * split_stride(P) words of scratch.
+size_t lists_split_words(const JoinPlan& P) {
+  int maxbits = 0;
+  for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
+  return 4 * ((((2ull << maxbits) + kMergeTile - 1) / kMergeTile) + 1);
+}
+
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
-                         cudaStream_t s) {
-  lists_base_kernel<<<4, 1024, 0, s>>>(d_keys, P, buf0);
+                         uint32_t* d_rot, uint32_t* d_split, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(lists_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(BaseSmem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  lists_base_kernel<<<4, 1024, sizeof(BaseSmem), s>>>(d_keys, P, buf0, d_rot);
   int maxbits = 0;
   for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
   for (int k = kBaseBits; k < maxbits; k++) {
     const int parity = (k - kBaseBits) & 1;
     const uint64_t outputs = 2ull << k;
-    const unsigned int blocks = (unsigned int)((outputs + 256ull * kMergeItems - 1) / (256ull * kMergeItems));
-    lists_merge_kernel<<<dim3(blocks, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
-                                                         parity ? buf0 : buf1);
+    const unsigned int blocks = (unsigned int)((outputs + kMergeTile - 1) / kMergeTile);
+    const int stride = (int)(((2ull << maxbits) + kMergeTile - 1) / kMergeTile) + 1;
+    lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
+                                                                 d_rot, d_split, stride);
+    lists_merge_kernel<<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+        d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, d_split, stride);
   }
   return cudaGetLastError();
 }
