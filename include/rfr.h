@@ -128,7 +128,7 @@ typedef struct rfr_profile {
 /* Verdicts written per candidate (rfr_verify). */
 enum {
   RFR_V_REJECT = 0,  /* not a factor (trace / rounding / division mod primes) */
-  RFR_V_PASS = 1,    /* integral, divides p modulo three 61-bit primes        */
+  RFR_V_PASS = 1,    /* integral, divides p modulo the three verify primes   */
   RFR_V_HOST = 2     /* coefficients beyond 2^62 or undecidable: host decides */
 };
 
@@ -137,7 +137,7 @@ enum {
  * trace_test -> round_and_divide (R/verify.py:60-155) for every candidate of
  * one search.  For candidate k the smaller-degree side of {pat, complement}
  * is rebuilt in double-double, screened by power-sum integrality, rounded,
- * and trial-divided into p modulo three 61-bit primes.
+ * and trial-divided into p modulo three primes (2^61-1, 2^62-57, 2^63-25).
  *   pats[m]          candidate patterns (bit i = rho index i)
  *   p_mod[3*(d+1)]   coefficients of the monic input p (low->high) mod the
  *                    primes returned by rfr_verify_primes

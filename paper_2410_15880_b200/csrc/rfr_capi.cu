@@ -78,6 +78,8 @@ struct Ctx {
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
+  void* h_stage = nullptr;       // pinned staging of rfr_verify (in, then out)
+  size_t h_stage_bytes = 0;
   // cache of the last built lists (key values + plan geometry)
   std::vector<uint64_t> built_keys;
   int built_bits[4] = {-1, -1, -1, -1};
@@ -111,7 +113,7 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   memset(P, 0, sizeof *P);
   const int m = n - 1;
   const int alpha = (m + 1) / 2, beta = m - alpha;
-  int r = alpha - 12;  // ~4096 A records per bucket
+  int r = alpha - kJoinRecLog;  // ~2^kJoinRecLog A records per bucket
   if (r < 2) r = 2;
   const uint64_t half = (width >> 1) + (width & 1);
   const int hb = bit_length(half);
@@ -246,7 +248,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     P.bucket_end = nb * (uint64_t)(shard + 1) / (uint64_t)nshards;
     uint64_t span = P.bucket_end - P.bucket_begin;
     if (span == 0) continue;
-    const uint64_t ctas = (uint64_t)g.nsm;  // one join CTA per SM
+    const uint64_t ctas = (uint64_t)g.nsm * kJoinCtasPerSm;  // resident join CTAs
     int grid = (int)(span < ctas ? span : ctas);
     RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
     g_launches += 1;
@@ -340,6 +342,7 @@ int rfr_shutdown(void) {
     for (auto& v : a) v.release();
   for (auto& e : g.ev) cudaEventDestroy(e);
   cudaFreeHost(g.h_ctr);
+  if (g.h_stage) cudaFreeHost(g.h_stage);
   cudaStreamDestroy(g.stream);
   g = Ctx();
   return RFR_OK;
@@ -503,10 +506,28 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
   if (m == 0) return RFR_OK;
   cudaSetDevice(g.device);
   cudaStream_t s = g.stream;
-  // pack the profile: 6 double arrays + perm
+  // one pinned staging block each way: [profile doubles | perm | pats | p_mod]
+  // in, [verdict | side | coeffs] out (one H2D and one D2H per call)
   const int r = prof->r, c = prof->c, n = prof->n;
-  std::vector<double> hostd(2 * r + 4 * c + 1, 0.0);
-  double* hp = hostd.data();
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t nd = (size_t)(2 * r + 4 * c + 1);
+  const size_t o_perm = al(nd * sizeof(double));
+  const size_t o_pats = o_perm + al((size_t)n * sizeof(int32_t));
+  const size_t o_pmod = o_pats + al((size_t)m * sizeof(uint64_t));
+  const size_t in_bytes = o_pmod + al((size_t)3 * (d + 1) * sizeof(uint64_t));
+  const size_t q_side = al((size_t)m);
+  const size_t q_coef = q_side + al((size_t)m);
+  const size_t out_bytes = q_coef + (size_t)m * stride * sizeof(int64_t);
+  const size_t stage = in_bytes > out_bytes ? in_bytes : out_bytes;
+  if (g.h_stage_bytes < stage) {
+    if (g.h_stage) cudaFreeHost(g.h_stage);
+    g.h_stage = nullptr;
+    g.h_stage_bytes = 0;
+    RFR_CUDA_OK(cudaMallocHost(&g.h_stage, stage));
+    g.h_stage_bytes = stage;
+  }
+  char* hs = (char*)g.h_stage;
+  double* hp = (double*)hs;
   for (int i = 0; i < r; i++) {
     hp[i] = prof->real_hi[i];
     hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
@@ -517,19 +538,15 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
     hp[2 * r + 2 * c + j] = prof->prod_hi[j];
     hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
   }
-  const size_t dbytes = hostd.size() * sizeof(double);
-  RFR_CUDA_OK(g.vprof.ensure(dbytes + 64 * sizeof(int32_t)));
-  RFR_CUDA_OK(g.vpats.ensure((size_t)m * sizeof(uint64_t)));
-  RFR_CUDA_OK(g.vpmod.ensure((size_t)3 * (d + 1) * sizeof(uint64_t)));
-  RFR_CUDA_OK(g.vverd.ensure((size_t)m));
-  RFR_CUDA_OK(g.vside.ensure((size_t)m));
-  RFR_CUDA_OK(g.vcoef.ensure((size_t)m * stride * sizeof(int64_t)));
+  hp[nd - 1] = 0.0;
+  memcpy(hs + o_perm, prof->perm, (size_t)n * sizeof(int32_t));
+  memcpy(hs + o_pats, pats, (size_t)m * sizeof(uint64_t));
+  memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
+  RFR_CUDA_OK(g.vprof.ensure(in_bytes));
+  RFR_CUDA_OK(g.vcoef.ensure(out_bytes));
   char* base = (char*)g.vprof.p;
-  RFR_CUDA_OK(cudaMemcpyAsync(base, hostd.data(), dbytes, cudaMemcpyHostToDevice, s));
-  RFR_CUDA_OK(cudaMemcpyAsync(base + dbytes, prof->perm, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  RFR_CUDA_OK(cudaMemcpyAsync(g.vpats.p, pats, (size_t)m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-  RFR_CUDA_OK(cudaMemcpyAsync(g.vpmod.p, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t),
-                              cudaMemcpyHostToDevice, s));
+  char* obase = (char*)g.vcoef.p;
+  RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
   VerifyArgs A;
   A.n = n;
   A.r = r;
@@ -542,24 +559,25 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
   A.sum_lo = dp + 2 * r + c;
   A.prod_hi = dp + 2 * r + 2 * c;
   A.prod_lo = dp + 2 * r + 3 * c;
-  A.perm = (const int32_t*)(base + dbytes);
+  A.perm = (const int32_t*)(base + o_perm);
   A.root_err = prof->root_err;
-  A.pats = (const uint64_t*)g.vpats.p;
+  A.pats = (const uint64_t*)(base + o_pats);
   A.m = m;
-  A.p_mod = (const uint64_t*)g.vpmod.p;
+  A.p_mod = (const uint64_t*)(base + o_pmod);
   for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
-  A.verdict = (uint8_t*)g.vverd.p;
-  A.side = (uint8_t*)g.vside.p;
-  A.coeffs = (long long*)g.vcoef.p;
+  A.verdict = (uint8_t*)obase;
+  A.side = (uint8_t*)(obase + q_side);
+  A.coeffs = (long long*)(obase + q_coef);
   A.stride = stride;
   RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
   RFR_CUDA_OK(launch_verify(A, s));
   RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
-  RFR_CUDA_OK(cudaMemcpyAsync(verdict, g.vverd.p, (size_t)m, cudaMemcpyDeviceToHost, s));
-  RFR_CUDA_OK(cudaMemcpyAsync(side, g.vside.p, (size_t)m, cudaMemcpyDeviceToHost, s));
-  RFR_CUDA_OK(cudaMemcpyAsync(coeffs, g.vcoef.p, (size_t)m * stride * sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, s));
+  // the staging block is reused for the results once the H2D has been consumed
+  RFR_CUDA_OK(cudaMemcpyAsync(hs, obase, out_bytes, cudaMemcpyDeviceToHost, s));
   RFR_CUDA_OK(cudaStreamSynchronize(s));
+  memcpy(verdict, hs, (size_t)m);
+  memcpy(side, hs + q_side, (size_t)m);
+  memcpy(coeffs, hs + q_coef, (size_t)m * stride * sizeof(int64_t));
   if (st) {
     memset(st, 0, sizeof *st);
     st->ms_post = ev_ms(g.ev[2], g.ev[3]);

@@ -18,6 +18,8 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
 cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaStream_t s);
 
 struct VerifyArgs;
-constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 1152921504606846883ull,
-                                       576460752303423433ull};
+// Primes of the modular division test, P = 2^k - c with small c (fast
+// reduction in the verify kernel): 2^61 - 1, 2^62 - 57, 2^63 - 25.
+constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 4611686018427387847ull,
+                                       9223372036854775783ull};
 }  // namespace rfr

@@ -37,12 +37,12 @@
 #define RFR_JOIN_TRACE 0
 #endif
 
-constexpr int kJoinThreads = 512;
+constexpr int kJoinThreads = 512 / kJoinCtasPerSm;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kJoinCtasPerSm = 1;
-constexpr int kL1Log = 15, kL2Log = 13, kL3Log = 11;  // index levels (slots)
-constexpr int kPart = 384;                            // A records per warp partition
-constexpr int kCapRec = kPart * kJoinWarps;           // 6144 A records per chunk
+// index levels (slots): 8, 2 and 1/2 slots per expected record
+constexpr int kL1Log = kJoinRecLog + 3, kL2Log = kJoinRecLog + 1, kL3Log = kJoinRecLog - 1;
+constexpr int kPart = 384;                   // A records per warp partition
+constexpr int kCapRec = kPart * kJoinWarps;  // A records per chunk (1.5x the expected)
 constexpr int kLose = 128;                            // per-warp level-1 loser list
 constexpr int kList4 = 256;                           // level-3 losers (CTA list)
 constexpr int kMaxOuter = 1 << kMaxOuterBits;
@@ -76,6 +76,9 @@ struct JoinSmem {
   int ovf;
   uint32_t cur_i, cur_t;  // slow path cursor
 };
+static_assert(sizeof(JoinSmem) + 1024 <= (228 * 1024) / kJoinCtasPerSm,
+              "join shared memory exceeds the per-SM budget for kJoinCtasPerSm CTAs");
+
 
 // The join's shared memory, addressed from the extern symbol inside every
 // (noinline) function so the compiler emits direct shared-window accesses

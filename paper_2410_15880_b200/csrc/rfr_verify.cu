@@ -10,8 +10,8 @@
 //      arithmetic (a magnitude polynomial evaluated with perturbed roots), and
 //      reject any coefficient farther from an integer than its bound (the
 //      reference's eps test, verify.py:145-148, with a derived tolerance);
-//   4. trial-divide the input p by the rounded monic q modulo three 61-bit
-//      primes (the reference's divide_exact, polynomial.py:155-183, as a
+//   4. trial-divide the input p by the rounded monic q modulo three primes
+//      2^61 - 1, 2^62 - 57, 2^63 - 25 (two-fold reduction, no division) (the reference's divide_exact, polynomial.py:155-183, as a
 //      filter; the host confirms survivors exactly with the certificate).
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -84,9 +84,19 @@ struct WarpBuf {
   long long q[kMaxE + 1];
 };
 
-__device__ __forceinline__ uint64_t mulmod61(uint64_t a, uint64_t b, uint64_t p) {
-  const unsigned __int128 x = (unsigned __int128)a * b;
-  return (uint64_t)(x % p);
+// a * b mod P for P = 2^k - c (c small, a, b < P): the 2k-bit product
+// x = xh 2^k + xl is folded twice with 2^k = c (mod P), leaving z < 2P.
+__device__ __forceinline__ uint64_t mulmod_k(uint64_t a, uint64_t b, uint64_t P, int k, uint64_t c) {
+  const uint64_t mask = (1ull << k) - 1ull;
+  const uint64_t lo = a * b, hi = __umul64hi(a, b);
+  const uint64_t xh = (hi << (64 - k)) | (lo >> k), xl = lo & mask;  // xh < 2^k
+  const uint64_t tl = xh * c, th = __umul64hi(xh, c);
+  const uint64_t yl = xl + tl, yh = th + (yl < xl ? 1ull : 0ull);     // y = xl + xh c
+  const uint64_t zh = (yh << (64 - k)) | (yl >> k);                   // y >> k <= c
+  uint64_t z = (yl & mask) + zh * c;                                   // < P + c + c^2
+  if (z >= P) z -= P;
+  if (z >= P) z -= P;
+  return z;
 }
 
 __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A) {
@@ -202,19 +212,26 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
 
   // ---- trial division of p by q modulo three 61-bit primes
   bool divides = true;
+  uint64_t* qm = reinterpret_cast<uint64_t*>(&B.mag[0][0]);  // q mod P (mag is dead here)
   for (int pi = 0; pi < 3 && divides; pi++) {
     const uint64_t P = A.primes[pi];
+    const int pk = 64 - __clzll((long long)P);  // P = 2^pk - pc
+    const uint64_t pc = (1ull << pk) - P;
     const uint64_t* pm = A.p_mod + (size_t)pi * (A.d + 1);
     for (int j = lane; j <= A.d; j += 32) B.rem[j] = pm[j];
+    for (int j = lane; j < e; j += 32) {  // |q_j| < 2^62, so one reduction each
+      const long long qj = B.q[j];
+      const uint64_t aq = qj >= 0 ? (uint64_t)qj : (uint64_t)(-qj);
+      const uint64_t r = aq % P;
+      qm[j] = (qj >= 0 || r == 0) ? r : P - r;
+    }
     __syncwarp();
     for (int kk = A.d - e; kk >= 0; kk--) {
       const uint64_t lead = B.rem[kk + e];  // q monic
       __syncwarp();
       if (lead) {
         for (int j = lane; j < e; j += 32) {
-          const long long qj = B.q[j];
-          const uint64_t qm = qj >= 0 ? (uint64_t)qj % P : (P - ((uint64_t)(-qj) % P)) % P;
-          const uint64_t sub = mulmod61(lead, qm, P);
+          const uint64_t sub = mulmod_k(lead, qm[j], P, pk, pc);
           const uint64_t r0 = B.rem[kk + j];
           B.rem[kk + j] = r0 >= sub ? r0 - sub : r0 + P - sub;
         }

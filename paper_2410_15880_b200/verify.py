@@ -14,7 +14,7 @@ Pipeline for one monic square-free part p:
      sum is within +-T of 0 -- the true factors and a handful of false hits;
   3. GPU (``verify_seconds``): one warp per candidate expands the smaller
      side in double-double, checks integrality against a derived error bound
-     and trial-divides p modulo three 61-bit primes (R/verify.py:60-155);
+     and trial-divides p modulo three primes below 2^63 (R/verify.py:60-155);
   4. host: the minimal passing patterns (atoms) are the irreducible factors;
      the certificate (exact re-multiplication, R/verify.py:224-231) proves
      the product.  The reference instead re-roots and re-searches every
@@ -258,13 +258,18 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
                 break
     factors = []
     rest = p
-    for a in atoms:
+    for k, a in enumerate(atoms):
+        if k == len(atoms) - 1 and covered == full and rest.degree >= 1:
+            break  # the last atom's factor is the cofactor of the others
         q = found.get(a)
         if q is None:
             q = divide_exact(p, found[~a & full])
-        if q is None or divide_exact(rest, q) is None:
+        if q is None:
             continue
-        rest = divide_exact(rest, q)
+        quo = divide_exact(rest, q)
+        if quo is None:
+            continue
+        rest = quo
         factors.append(q)
     if rest.degree >= 1:
         factors.append(rest)
