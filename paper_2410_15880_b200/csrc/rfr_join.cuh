@@ -88,6 +88,14 @@ __device__ __forceinline__ JoinSmem& join_smem() {
   return *reinterpret_cast<JoinSmem*>(smem_raw);
 }
 
+// Streaming read of a list key: read-only path without L1 allocation, so the
+// window loads do not evict the kernel's stack and small working set.
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
+  uint64_t v;
+  asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
   return (uint32_t)(rel >> shift) & ((1u << lg) - 1u);
 }
@@ -115,6 +123,7 @@ struct PassSt {
   uint32_t n_stat;    // records streamed (inserts for A, queries for B)
   uint32_t n_qprobe;  // A records compared against B records
   bool overflow;      // the A partition overflowed
+  bool cont;          // some outer of the warp was flagged for continue_pass
 };
 
 // Per-bucket constants, built once per pass into registers (reading them
@@ -260,7 +269,7 @@ __device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
   JoinSmem& S = join_smem();
   // register copies of the by-reference counters (written back once)
   uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
-  bool overflow = st.overflow;
+  bool overflow = st.overflow, cont = false;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -292,7 +301,7 @@ __device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
       const bool valid = i < hi && (uint32_t)l < Mi;
       const uint32_t ic = i < hi ? i : lo;
       const uint32_t j = (rots[ic] + poss[ic] + l) & (Mi - 1);
-      kn[u] = __ldg(kin + (valid ? j : 0u));
+      kn[u] = ld_stream(kin + (valid ? j : 0u));
     }
   };
   if (lo < hi) issue(lo);
@@ -363,6 +372,7 @@ __device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
       if (l == 0 && i < hi) {
         const bool sat = ((em >> gb) & gmask) == gmask && (uint32_t)gs < Mi;
         mainv[i] = (uint32_t)__popc((mm >> gb) & gmask) | (sat ? kFlagCont : 0u);
+        cont |= sat;
       }
     }
     if (!SIDE_A && nq) {
@@ -370,7 +380,8 @@ __device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
       nq = 0;
     }
   }
-  return PassSt{wfill, n_stat, n_qprobe, overflow};
+  cont = __any_sync(0xffffffffu, cont);
+  return PassSt{wfill, n_stat, n_qprobe, overflow, cont};
 }
 
 // Continue the saturated runs of one side, one outer at a time, 32 lanes.
@@ -380,7 +391,7 @@ __device__ __noinline__ PassSt continue_pass(const JoinArgs& a, uint64_t cW,
   JoinSmem& S = join_smem();
   // register copies of the by-reference counters (written back once)
   uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
-  bool overflow = st.overflow;
+  bool overflow = st.overflow, cont = false;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -410,7 +421,7 @@ __device__ __noinline__ PassSt continue_pass(const JoinArgs& a, uint64_t cW,
         const bool valid = q < Mi;
         const uint32_t o = pos + q;
         const uint32_t j = (rot + o) & (Mi - 1);
-        const uint64_t s = x + (valid ? __ldg(kin + j) : 0ull);
+        const uint64_t s = x + (valid ? ld_stream(kin + j) : 0ull);
         const uint64_t rel = s - cW;
         const bool m = valid && o < Mi && rel < W;
         const bool e = m || (valid && (rel - W) < H);
@@ -448,7 +459,7 @@ __device__ __noinline__ PassSt continue_pass(const JoinArgs& a, uint64_t cW,
       if (lane == 0) mainv[i] = mainc;
     }
   }
-  return PassSt{wfill, n_stat, n_qprobe, overflow};
+  return PassSt{wfill, n_stat, n_qprobe, overflow, cont};
 }
 
 // Branch-light level-1 probe of one B record (run_pass): the slot(s) and
@@ -492,7 +503,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
                                       int nch, PassSt st) {
   JoinSmem& S = join_smem();
   uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
-  bool overflow = st.overflow;
+  bool overflow = st.overflow, cont = false;
   const JoinPlan& P = a.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -516,7 +527,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
 #pragma unroll
     for (int k = 0; k < kMaxCh; k++) {
       const uint32_t q = (uint32_t)(k * 32 + lane);
-      kv[k] = (k < nch && q < Mi) ? __ldg(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
+      kv[k] = (k < nch && q < Mi) ? ld_stream(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
     }
     if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
     uint32_t mc = 0, nq = 0, em = 0;
@@ -562,10 +573,12 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
       }
     }
     if (!SIDE_A && nq) n_qprobe += process_staged(a, cW, nq);
-    if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | ((em == FULL && can_cont) ? kFlagCont : 0u);
+    const bool sat = em == FULL && can_cont;  // warp-uniform
+    if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | (sat ? kFlagCont : 0u);
+    cont |= sat;
   }
   if (RFR_JOIN_TRACE && tr && trn < 63) tr[trn++] = clock64();
-  return PassSt{wfill, n_stat, n_qprobe, overflow};
+  return PassSt{wfill, n_stat, n_qprobe, overflow, cont};
 }
 
 // Build levels 2 and 3 from the level-1 losers (plain stores + read-back).
@@ -759,23 +772,13 @@ __device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_
       continue;
     }
     const bool done = S.cur_i >= MoA;
-    uint32_t dummy_fill = 0;
-    bool dummy_ovf = false;
-    if (gsB > 32)
-      {
-      const PassSt o_ = run_pass<false>(a, cW, bLo, bHi, gsB >> 5, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
-    else
-      {
-      const PassSt o_ = window_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
+    PassSt sb{0u, n_q, n_qprobe, false, false};
+    sb = gsB > 32 ? run_pass<false>(a, cW, bLo, bHi, gsB >> 5, sb)
+                  : window_pass<false>(a, cW, bLo, bHi, gsB, sb);
     __syncwarp();
-    {
-      const PassSt o_ = continue_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
+    sb = continue_pass<false>(a, cW, bLo, bHi, gsB, sb);
+    n_q = sb.n_stat;
+    n_qprobe = sb.n_qprobe;
     __syncthreads();
     if (done) break;
   }
@@ -791,15 +794,12 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   JoinSmem& S = *reinterpret_cast<JoinSmem*>(smem_raw);
   const JoinPlan& P = a.P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const unsigned FULL = 0xffffffffu;
 
   const uint32_t MoA = 1u << P.list[0].bits, MiA = 1u << P.list[1].bits;
   const uint32_t MoB = 1u << P.list[2].bits, MiB = 1u << P.list[3].bits;
   const uint64_t* __restrict__ kA = a.key[1];
   const uint64_t* __restrict__ kB = a.key[3];
   const int sh = 64 - P.r;  // bucket = key >> sh
-  const uint64_t W = 1ull << sh;
-  const uint64_t H = P.half;
 
   const uint64_t nbk = P.bucket_end - P.bucket_begin;
   const uint64_t c_begin = P.bucket_begin + nbk * blockIdx.x / gridDim.x;
@@ -842,27 +842,19 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     __syncthreads();
     RFR_MARK();
 
-    // ---- fast path: A windows + continuations into the warp partitions
-    bool wovf = false;
-    uint32_t wfill = 0;
-    if (gsA > 32)
-      {
-      const PassSt o_ = run_pass<true>(a, cW, aLo, aHi, gsA >> 5, PassSt{wfill, n_ins, n_qprobe, wovf});
-      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
+    // ---- fast path: A runs (+ continuations) into the warp partitions
+    PassSt sa{0u, n_ins, n_qprobe, false, false};
+    sa = gsA > 32 ? run_pass<true>(a, cW, aLo, aHi, gsA >> 5, sa)
+                  : window_pass<true>(a, cW, aLo, aHi, gsA, sa);
+    if (sa.cont) {
+      __syncwarp();
+      sa = continue_pass<true>(a, cW, aLo, aHi, gsA, sa);
     }
-    else
-      {
-      const PassSt o_ = window_pass<true>(a, cW, aLo, aHi, gsA, PassSt{wfill, n_ins, n_qprobe, wovf});
-      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
-    }
-    __syncwarp();
-    {
-      const PassSt o_ = continue_pass<true>(a, cW, aLo, aHi, gsA, PassSt{wfill, n_ins, n_qprobe, wovf});
-      wfill = o_.wfill; n_ins = o_.n_stat; n_qprobe = o_.n_qprobe; wovf = o_.overflow;
-    }
+    n_ins = sa.n_stat;
+    n_qprobe = sa.n_qprobe;
     if (lane == 0) {
-      S.wcnt[wid] = wfill;
-      if (wovf) S.ovf = 1;
+      S.wcnt[wid] = sa.wfill;
+      if (sa.overflow) S.ovf = 1;
     }
     RFR_MARK();
     __syncthreads();
@@ -873,23 +865,17 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     }
     RFR_MARK();
     if (!overflowed) {
-      uint32_t dummy_fill = 0;
-      bool dummy_ovf = false;
-      if (gsB > 32)
-        {
-      const PassSt o_ = run_pass<false>(a, cW, bLo, bHi, gsB >> 5, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
-      else
-        {
-      const PassSt o_ = window_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
-      __syncwarp();
-      {
-      const PassSt o_ = continue_pass<false>(a, cW, bLo, bHi, gsB, PassSt{dummy_fill, n_q, n_qprobe, dummy_ovf});
-      dummy_fill = o_.wfill; n_q = o_.n_stat; n_qprobe = o_.n_qprobe; dummy_ovf = o_.overflow;
-    }
+      PassSt sb{0u, n_q, n_qprobe, false, false};
+      sb = gsB > 32 ? run_pass<false>(a, cW, bLo, bHi, gsB >> 5, sb)
+                    : window_pass<false>(a, cW, bLo, bHi, gsB, sb);
+      RFR_MARK();
+      if (sb.cont) {
+        __syncwarp();
+        sb = continue_pass<false>(a, cW, bLo, bHi, gsB, sb);
+      }
+      RFR_MARK();
+      n_q = sb.n_stat;
+      n_qprobe = sb.n_qprobe;
       __syncwarp();
       for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
       for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t bit = 1u << k;
   const uint32_t r0 = rot_of(rc, k, n);
   const uint32_t mask = n - 1;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t a0 = __ldg(split + li * stride + blockIdx.x);
   const uint32_t a1 = __ldg(split + li * stride + blockIdx.x + 1);
   const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
@@ -481,11 +481,12 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                 (t[k + 1] >> 63) ? "p" : "");
       fprintf(stderr, "\n");
     }
-    for (int b = 0; b < 6; b++) {  // marks: bucket start, A gen, A index, B pass, end barrier
-      const unsigned long long* q = h + 1 + b * 5;
-      if (!q[4]) break;
-      fprintf(stderr, "[rfr trace] bucket %d: A %llu index %llu B %llu barrier %llu\n", b,
-              q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4] - q[3]);
+    for (int b = 0; b < 6; b++) {  // marks: start, A, index, B run, B cont, B end, barrier
+      const unsigned long long* q = h + 1 + b * 7;
+      if (!q[6]) break;
+      fprintf(stderr,
+              "[rfr trace] bucket %d: A %llu index %llu B-run %llu B-cont %llu B-tail %llu barrier %llu\n",
+              b, q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4] - q[3], q[5] - q[4], q[6] - q[5]);
     }
   }
   return cudaGetLastError();
