@@ -309,7 +309,7 @@ def run_ours(args):
             "workload": "C3 d=100 random reducible (two degree-50 factors, coeffs in [-100,100]), seeds 0-4 in rotation",
             "n": sorted(set(ns)),
             "key_window": "exact 64-bit first+second power-sum keys, +-T from root error bounds",
-            "l2": "256 MB buffer written between timed steps (flush); search working set is L2-resident by design",
+            "l2": "256 MB buffer written between timed steps (flush); the inner quarter lists (2^23-2^24 entries, 12 B each, per half) exceed L2 and are streamed from HBM",
             "parallelism": f"key-range shards x{world}" if world > 1 else "1 GPU",
         },
         "search_ms": round(float(np.mean(np.array(joins) + np.array(lists))), 4),
