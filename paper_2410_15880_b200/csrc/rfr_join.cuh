@@ -72,6 +72,10 @@ struct JoinSmem {
   uint32_t bpos[kMaxOuter];
   uint32_t bmain[kMaxOuter];
   uint32_t wcnt[kJoinWarps];
+  // loop state kept on chip across the pass calls (which may clobber every
+  // register; state held in registers would be saved to the local stack)
+  uint32_t wlo[2][kJoinWarps], whi[2][kJoinWarps];  // per-warp outer ranges (A, B)
+  uint32_t cnt[3][kJoinThreads];                     // per-thread inserts, queries, probes
   unsigned int n4;
   int ovf;
   uint32_t cur_i, cur_t;  // slow path cursor
@@ -94,6 +98,14 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
   uint64_t v;
   asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
+}
+
+// threadIdx.x re-read at each use (volatile: never hoisted and kept across a
+// call, where it would be saved to and reloaded from the local stack).
+__device__ __forceinline__ int tid_now() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
 }
 
 __device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
@@ -592,28 +604,36 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   const int sh = 64 - P.r;
   const uint32_t nw = S.wcnt[wid];
   uint16_t* lose = S.lose[wid];
-  // level 1 read-back: losers go to level 2
+  // level 1 read-back: losers go to level 2.  Four 32-record groups per
+  // iteration: all record and slot loads are issued before the first ballot
+  // (a flag written by an earlier group leaves the slot's index bits intact).
   uint32_t nl = 0;
-  for (uint32_t e0 = 0; e0 < nw; e0 += 32) {
-    const uint32_t e = e0 + lane;
-    const uint32_t r = wid * kPart + e;
-    bool lost = false;
-    uint64_t rel = 0;
-    uint32_t h1 = 0, occ = 0;
-    if (e < nw) {
-      rel = S.recK[r] - cW;
-      h1 = home_of(rel, sh - kL1Log, kL1Log);
-      occ = S.t1[h1];
-      lost = (occ & 0x7fffu) != r;
+  constexpr int G = 4;
+  for (uint32_t e0 = 0; e0 < nw; e0 += 32 * G) {
+    uint64_t rel[G];
+    uint32_t h1[G], occ[G];
+#pragma unroll
+    for (int u = 0; u < G; u++) {
+      const uint32_t e = e0 + u * 32 + lane;
+      rel[u] = (e < nw ? S.recK[wid * kPart + e] : cW) - cW;
+      h1[u] = home_of(rel[u], sh - kL1Log, kL1Log);
     }
-    const uint32_t lm = __ballot_sync(FULL, lost);
-    if (lost) {
-      const uint32_t k = nl + __popc(lm & lt_mask);
-      if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
-      S.t2[home_of(rel, sh - kL2Log, kL2Log)] = (uint16_t)r;
-      S.t1[h1] = (uint16_t)(occ | 0x8000u);  // collision flag: B also probes levels 2-3
+#pragma unroll
+    for (int u = 0; u < G; u++) occ[u] = S.t1[h1[u]];
+#pragma unroll
+    for (int u = 0; u < G; u++) {
+      const uint32_t e = e0 + u * 32 + lane;
+      const uint32_t r = wid * kPart + e;
+      const bool lost = e < nw && (occ[u] & 0x7fffu) != r;
+      const uint32_t lm = __ballot_sync(FULL, lost);
+      if (lost) {
+        const uint32_t k = nl + __popc(lm & lt_mask);
+        if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
+        S.t2[home_of(rel[u], sh - kL2Log, kL2Log)] = (uint16_t)r;
+        S.t1[h1[u]] = (uint16_t)(occ[u] | 0x8000u);  // collision flag: B also probes levels 2-3
+      }
+      nl += __popc(lm);
     }
-    nl += __popc(lm);
   }
   if (nl > (uint32_t)kLose && lane == 0) S.ovf = 1;
   const int any2 = __syncthreads_or(nl > 0);
@@ -826,16 +846,25 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     S.bpos[i] = count_below(kB, MiB, x, c_begin << sh);
   }
 
-  uint32_t n_ins = 0, n_q = 0, n_qprobe = 0, n_chunks = 0;
-  const uint32_t perWA = (MoA + kJoinWarps - 1) / kJoinWarps;
-  const uint32_t aLo = min(MoA, wid * perWA), aHi = min(MoA, aLo + perWA);
-  const uint32_t perWB = (MoB + kJoinWarps - 1) / kJoinWarps;
-  const uint32_t bLo = min(MoB, wid * perWB), bHi = min(MoB, bLo + perWB);
+  {
+    const uint32_t perWA = (MoA + kJoinWarps - 1) / kJoinWarps;
+    const uint32_t perWB = (MoB + kJoinWarps - 1) / kJoinWarps;
+    if (lane == 0) {
+      S.wlo[0][wid] = min(MoA, wid * perWA);
+      S.whi[0][wid] = min(MoA, wid * perWA + perWA);
+      S.wlo[1][wid] = min(MoB, wid * perWB);
+      S.whi[1][wid] = min(MoB, wid * perWB + perWB);
+    }
+    S.cnt[0][tid] = 0;
+    S.cnt[1][tid] = 0;
+    S.cnt[2][tid] = 0;
+  }
+  uint32_t n_chunks = 0;
 
   for (uint64_t c = c_begin; c < c_end; c++) {
-    const uint64_t cW = c << sh;
+    const uint64_t cW = c << (64 - P.r);
     clear_index(S);
-    if (tid == 0) {
+    if (tid_now() == 0) {
       S.n4 = 0;
       S.ovf = 0;
     }
@@ -843,18 +872,21 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     RFR_MARK();
 
     // ---- fast path: A runs (+ continuations) into the warp partitions
-    PassSt sa{0u, n_ins, n_qprobe, false, false};
-    sa = gsA > 32 ? run_pass<true>(a, cW, aLo, aHi, gsA >> 5, sa)
-                  : window_pass<true>(a, cW, aLo, aHi, gsA, sa);
-    if (sa.cont) {
-      __syncwarp();
-      sa = continue_pass<true>(a, cW, aLo, aHi, gsA, sa);
-    }
-    n_ins = sa.n_stat;
-    n_qprobe = sa.n_qprobe;
-    if (lane == 0) {
-      S.wcnt[wid] = sa.wfill;
-      if (sa.overflow) S.ovf = 1;
+    {
+      const int t = tid_now(), w = t >> 5;
+      PassSt sa{0u, S.cnt[0][t], S.cnt[2][t], false, false};
+      sa = gsA > 32 ? run_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA >> 5, sa)
+                    : window_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA, sa);
+      if (sa.cont) {
+        __syncwarp();
+        sa = continue_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA, sa);
+      }
+      S.cnt[0][t] = sa.n_stat;
+      S.cnt[2][t] = sa.n_qprobe;
+      if ((t & 31) == 0) {
+        S.wcnt[w] = sa.wfill;
+        if (sa.overflow) S.ovf = 1;
+      }
     }
     RFR_MARK();
     __syncthreads();
@@ -865,20 +897,26 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     }
     RFR_MARK();
     if (!overflowed) {
-      PassSt sb{0u, n_q, n_qprobe, false, false};
-      sb = gsB > 32 ? run_pass<false>(a, cW, bLo, bHi, gsB >> 5, sb)
-                    : window_pass<false>(a, cW, bLo, bHi, gsB, sb);
-      RFR_MARK();
-      if (sb.cont) {
-        __syncwarp();
-        sb = continue_pass<false>(a, cW, bLo, bHi, gsB, sb);
+      {
+        const int t = tid_now(), w = t >> 5;
+        PassSt sb{0u, S.cnt[1][t], S.cnt[2][t], false, false};
+        sb = gsB > 32 ? run_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB >> 5, sb)
+                      : window_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB, sb);
+        RFR_MARK();
+        if (sb.cont) {
+          __syncwarp();
+          sb = continue_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB, sb);
+        }
+        RFR_MARK();
+        S.cnt[1][t] = sb.n_stat;
+        S.cnt[2][t] = sb.n_qprobe;
       }
-      RFR_MARK();
-      n_q = sb.n_stat;
-      n_qprobe = sb.n_qprobe;
       __syncwarp();
-      for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
-      for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
+      {
+        const int t = tid_now(), w = t >> 5, l = t & 31;
+        for (uint32_t i = S.wlo[1][w] + l; i < S.whi[1][w]; i += 32) S.bpos[i] += S.bmain[i];
+        for (uint32_t i = S.wlo[0][w] + l; i < S.whi[0][w]; i += 32) S.apos[i] += S.amain[i];
+      }
       RFR_MARK();
       __syncthreads();
       RFR_MARK();
@@ -886,11 +924,20 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     }
 
     // ---- slow path (skewed bucket)
-    slow_bucket(a, cW, aLo, aHi, bLo, bHi, gsB, n_ins, n_q, n_qprobe, n_chunks);
-    for (uint32_t i = bLo + lane; i < bHi; i += 32) S.bpos[i] += S.bmain[i];
-    for (uint32_t i = aLo + lane; i < aHi; i += 32) S.apos[i] += S.amain[i];
+    {
+      const int t = tid_now(), w = t >> 5, l = t & 31;
+      uint32_t n_ins = S.cnt[0][t], n_q = S.cnt[1][t], n_qprobe = S.cnt[2][t];
+      slow_bucket(a, cW, S.wlo[0][w], S.whi[0][w], S.wlo[1][w], S.whi[1][w], gsB, n_ins, n_q,
+                  n_qprobe, n_chunks);
+      S.cnt[0][t] = n_ins;
+      S.cnt[1][t] = n_q;
+      S.cnt[2][t] = n_qprobe;
+      for (uint32_t i = S.wlo[1][w] + l; i < S.whi[1][w]; i += 32) S.bpos[i] += S.bmain[i];
+      for (uint32_t i = S.wlo[0][w] + l; i < S.whi[0][w]; i += 32) S.apos[i] += S.amain[i];
+    }
     __syncthreads();
   }
+  const uint32_t n_ins = S.cnt[0][tid], n_q = S.cnt[1][tid], n_qprobe = S.cnt[2][tid];
   atomicAdd(&a.ctr->inserts, (unsigned long long)n_ins);
   atomicAdd(&a.ctr->queries, (unsigned long long)n_q);
   atomicAdd(&a.ctr->query_probes, (unsigned long long)n_qprobe);
