@@ -489,18 +489,26 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
   const uint32_t m1 = (1u << kL1Log) - 1u;
   const bool narrow = e && hn <= 1;  // wide windows go to probe_b_wide whole
   const uint32_t e0 = narrow ? (uint32_t)S.t1[h0 & m1] : (uint32_t)kNone;
-  const uint32_t e1 = (narrow && hn == 1) ? (uint32_t)S.t1[(h0 + 1) & m1] : (uint32_t)kNone;
   const uint32_t r0 = min(e0 & 0x7fffu, (uint32_t)kCapRec - 1u);
-  const uint32_t r1 = min(e1 & 0x7fffu, (uint32_t)kCapRec - 1u);
-  const uint64_t k0 = S.recK[r0], k1 = S.recK[r1];
-  const bool o0 = e0 != kNone, o1 = e1 != kNone;
+  const uint64_t k0 = S.recK[r0];
+  const bool o0 = e0 != kNone;
   const bool hit0 = o0 && !(bghost && (k0 - K.cW >= K.W)) && (k0 - s + K.hw <= K.width);
-  const bool hit1 = o1 && !(bghost && (k1 - K.cW >= K.W)) && (k1 - s + K.hw <= K.width);
-  n_qprobe += (o0 ? 1u : 0u) + (o1 ? 1u : 0u);
+  n_qprobe += o0 ? 1u : 0u;
   if (hit0) emit_match(a, r0, ib, jb);
-  if (hit1) emit_match(a, r1, ib, jb);
-  const int deep = ((o0 && (e0 >> 15)) || (o1 && (e1 >> 15))) ? 1 : 0;
-  return (e && hn > 1) ? 2 : deep;
+  bool deep = o0 && (e0 >> 15);
+  // second home: only when the window crosses a level-1 home boundary (rare
+  // for factor-mode windows), so it is taken warp-uniformly
+  if (__any_sync(0xffffffffu, narrow && hn == 1)) {
+    const uint32_t e1 = (narrow && hn == 1) ? (uint32_t)S.t1[(h0 + 1) & m1] : (uint32_t)kNone;
+    const uint32_t r1 = min(e1 & 0x7fffu, (uint32_t)kCapRec - 1u);
+    const uint64_t k1 = S.recK[r1];
+    const bool o1 = e1 != kNone;
+    const bool hit1 = o1 && !(bghost && (k1 - K.cW >= K.W)) && (k1 - s + K.hw <= K.width);
+    n_qprobe += o1 ? 1u : 0u;
+    if (hit1) emit_match(a, r1, ib, jb);
+    deep = deep || (o1 && (e1 >> 15));
+  }
+  return (e && hn > 1) ? 2 : (deep ? 1 : 0);
 }
 
 // Warp-wide walk for long runs (expected run >= 32 records per outer per
@@ -557,7 +565,9 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
         em = __ballot_sync(FULL, e);
         mc += __popc(__ballot_sync(FULL, m));
         n_stat += e ? 1u : 0u;
-        if (SIDE_A) {
+        if (em == 0) {
+          // chunk entirely past the run (warp-uniform): nothing to store or probe
+        } else if (SIDE_A) {
           const uint32_t ne = __popc(em);
           if (wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
           if (!overflow && e) {
