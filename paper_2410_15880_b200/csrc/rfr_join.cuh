@@ -598,6 +598,13 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     const bool sat = em == FULL && can_cont;  // warp-uniform
     if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | (sat ? kFlagCont : 0u);
     cont |= sat;
+    // the next bucket's run of this outer starts at pos + mc: pull its lines
+    // into L2 now (one 128-byte line per lane), so the next bucket's loads do
+    // not all wait on HBM together right after the barrier
+    if ((uint32_t)lane < (uint32_t)(nch * 2)) {
+      const uint32_t q = pos + mc + (uint32_t)lane * 16u;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(kin + ((rot + q) & (Mi - 1))));
+    }
   }
   if (RFR_JOIN_TRACE && tr && trn < 63) tr[trn++] = clock64();
   return PassSt{wfill, n_stat, n_qprobe, overflow, cont};
