@@ -89,7 +89,9 @@ static_assert(sizeof(JoinSmem) + 1024 <= (228 * 1024) / kJoinCtasPerSm,
 // instead of re-deriving them from a generic reference.
 __device__ __forceinline__ JoinSmem& join_smem() {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  return *reinterpret_cast<JoinSmem*>(smem_raw);
+  uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(sa));  // re-derived at each use, never kept across a call
+  return *reinterpret_cast<JoinSmem*>(__cvta_shared_to_generic(sa));
 }
 
 // Streaming read of a list key: read-only path without L1 allocation, so the
@@ -691,14 +693,18 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   __syncthreads();
 }
 
-__device__ __forceinline__ void clear_index(JoinSmem& S) {
+__device__ __forceinline__ void clear_index() {
+  JoinSmem& S = join_smem();
+  const int t = tid_now();
   const uint4 f4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
   uint4* p1 = reinterpret_cast<uint4*>(S.t1);
-  for (int i = threadIdx.x; i < (1 << kL1Log) / 8; i += kJoinThreads) p1[i] = f4;
+#pragma unroll
+  for (int i = 0; i < (1 << kL1Log) / 8 / kJoinThreads; i++) p1[t + i * kJoinThreads] = f4;
   uint4* p2 = reinterpret_cast<uint4*>(S.t2);
-  for (int i = threadIdx.x; i < (1 << kL2Log) / 8; i += kJoinThreads) p2[i] = f4;
+#pragma unroll
+  for (int i = 0; i < (1 << kL2Log) / 8 / kJoinThreads; i++) p2[t + i * kJoinThreads] = f4;
   uint4* p3 = reinterpret_cast<uint4*>(S.t3);
-  for (int i = threadIdx.x; i < (1 << kL3Log) / 8; i += kJoinThreads) p3[i] = f4;
+  for (int i = t; i < (1 << kL3Log) / 8; i += kJoinThreads) p3[i] = f4;
 }
 
 // Slow path for a skewed bucket whose A side overflowed the warp partitions:
@@ -730,7 +736,7 @@ __device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_
   uint32_t chunk_cap = (uint32_t)kCapRec;  // halves when a chunk overflows the index
   while (true) {
     n_chunks++;
-    clear_index(S);
+    clear_index();
     const uint32_t save_i = S.cur_i, save_t = S.cur_t;
     __syncthreads();
     if (tid == 0) {
@@ -880,10 +886,10 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
 
   for (uint64_t c = c_begin; c < c_end; c++) {
     const uint64_t cW = c << (64 - P.r);
-    clear_index(S);
+    clear_index();
     if (tid_now() == 0) {
-      S.n4 = 0;
-      S.ovf = 0;
+      join_smem().n4 = 0;
+      join_smem().ovf = 0;
     }
     __syncthreads();
     RFR_MARK();
@@ -891,48 +897,48 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     // ---- fast path: A runs (+ continuations) into the warp partitions
     {
       const int t = tid_now(), w = t >> 5;
-      PassSt sa{0u, S.cnt[0][t], S.cnt[2][t], false, false};
-      sa = gsA > 32 ? run_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA >> 5, sa)
-                    : window_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA, sa);
+      PassSt sa{0u, join_smem().cnt[0][t], join_smem().cnt[2][t], false, false};
+      sa = gsA > 32 ? run_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa)
+                    : window_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
       if (sa.cont) {
         __syncwarp();
-        sa = continue_pass<true>(a, cW, S.wlo[0][w], S.whi[0][w], gsA, sa);
+        sa = continue_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
       }
-      S.cnt[0][t] = sa.n_stat;
-      S.cnt[2][t] = sa.n_qprobe;
+      join_smem().cnt[0][t] = sa.n_stat;
+      join_smem().cnt[2][t] = sa.n_qprobe;
       if ((t & 31) == 0) {
-        S.wcnt[w] = sa.wfill;
-        if (sa.overflow) S.ovf = 1;
+        join_smem().wcnt[w] = sa.wfill;
+        if (sa.overflow) join_smem().ovf = 1;
       }
     }
     RFR_MARK();
     __syncthreads();
-    bool overflowed = S.ovf != 0;
+    bool overflowed = join_smem().ovf != 0;
     if (!overflowed) {
       build_index_levels(P, cW);
-      overflowed = S.ovf != 0;
+      overflowed = join_smem().ovf != 0;
     }
     RFR_MARK();
     if (!overflowed) {
       {
         const int t = tid_now(), w = t >> 5;
-        PassSt sb{0u, S.cnt[1][t], S.cnt[2][t], false, false};
-        sb = gsB > 32 ? run_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB >> 5, sb)
-                      : window_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB, sb);
+        PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
+        sb = gsB > 32 ? run_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb)
+                      : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
           __syncwarp();
-          sb = continue_pass<false>(a, cW, S.wlo[1][w], S.whi[1][w], gsB, sb);
+          sb = continue_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         }
         RFR_MARK();
-        S.cnt[1][t] = sb.n_stat;
-        S.cnt[2][t] = sb.n_qprobe;
+        join_smem().cnt[1][t] = sb.n_stat;
+        join_smem().cnt[2][t] = sb.n_qprobe;
       }
       __syncwarp();
       {
         const int t = tid_now(), w = t >> 5, l = t & 31;
-        for (uint32_t i = S.wlo[1][w] + l; i < S.whi[1][w]; i += 32) S.bpos[i] += S.bmain[i];
-        for (uint32_t i = S.wlo[0][w] + l; i < S.whi[0][w]; i += 32) S.apos[i] += S.amain[i];
+        for (uint32_t i = join_smem().wlo[1][w] + l; i < join_smem().whi[1][w]; i += 32) join_smem().bpos[i] += join_smem().bmain[i];
+        for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
       }
       RFR_MARK();
       __syncthreads();
@@ -943,14 +949,14 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     // ---- slow path (skewed bucket)
     {
       const int t = tid_now(), w = t >> 5, l = t & 31;
-      uint32_t n_ins = S.cnt[0][t], n_q = S.cnt[1][t], n_qprobe = S.cnt[2][t];
-      slow_bucket(a, cW, S.wlo[0][w], S.whi[0][w], S.wlo[1][w], S.whi[1][w], gsB, n_ins, n_q,
+      uint32_t n_ins = join_smem().cnt[0][t], n_q = join_smem().cnt[1][t], n_qprobe = join_smem().cnt[2][t];
+      slow_bucket(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], join_smem().wlo[1][w], join_smem().whi[1][w], gsB, n_ins, n_q,
                   n_qprobe, n_chunks);
-      S.cnt[0][t] = n_ins;
-      S.cnt[1][t] = n_q;
-      S.cnt[2][t] = n_qprobe;
-      for (uint32_t i = S.wlo[1][w] + l; i < S.whi[1][w]; i += 32) S.bpos[i] += S.bmain[i];
-      for (uint32_t i = S.wlo[0][w] + l; i < S.whi[0][w]; i += 32) S.apos[i] += S.amain[i];
+      join_smem().cnt[0][t] = n_ins;
+      join_smem().cnt[1][t] = n_q;
+      join_smem().cnt[2][t] = n_qprobe;
+      for (uint32_t i = join_smem().wlo[1][w] + l; i < join_smem().whi[1][w]; i += 32) join_smem().bpos[i] += join_smem().bmain[i];
+      for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
     }
     __syncthreads();
   }
