@@ -30,6 +30,7 @@
 // each chunk re-streaming B; the fast attempt emits nothing before the
 // overflow is known, so no pair is duplicated.
 #pragma once
+#include <type_traits>
 
 // Clock64 phase trace of CTA 0 (RFR_TRACE=1 at run time, needs a build with
 // `make TRACE=1`); compiled out of the production kernel.
@@ -627,8 +628,8 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   // iteration: all record and slot loads are issued before the first ballot
   // (a flag written by an earlier group leaves the slot's index bits intact).
   uint32_t nl = 0;
-  constexpr int G = 4;
-  for (uint32_t e0 = 0; e0 < nw; e0 += 32 * G) {
+  auto group = [&](uint32_t e0, auto Gc) {
+    constexpr int G = decltype(Gc)::value;
     uint64_t rel[G];
     uint32_t h1[G], occ[G];
 #pragma unroll
@@ -653,7 +654,12 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
       }
       nl += __popc(lm);
     }
-  }
+  };
+  // whole groups of 128 records, then the tail 32 at a time (partitions are
+  // ~256 +- 16 records: no warp pays a whole extra group for a few records)
+  uint32_t e0 = 0;
+  for (; e0 + 128 <= nw; e0 += 128) group(e0, std::integral_constant<int, 4>());
+  for (; e0 < nw; e0 += 32) group(e0, std::integral_constant<int, 1>());
   if (nl > (uint32_t)kLose && lane == 0) S.ovf = 1;
   const int any2 = __syncthreads_or(nl > 0);
   if (!any2) return;
