@@ -120,16 +120,23 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   if (r > 61 - hb) r = 61 - hb;  // keep the window radius <= W / 8
   if (r < 2) return rfr_fail(RFR_E_ARG, "window too wide for one plan (internal)");
   auto clampi = [](int v, int lo_, int hi_) { return v < lo_ ? lo_ : (v > hi_ ? hi_ : v); };
-  // outer lists sized so each outer contributes ~2^lam records per bucket
-  // (long runs: the join's warp-wide run pass), inner lists
-  // capped at 2^kMaxInnerBits entries (streamed, so they need not fit L2)
+  // outer lists: one outer per join warp per side (each warp walks one long
+  // run per bucket), unless the runs would exceed 2^lam records
+  // per bucket (default 256: the run pass keeps <= 12 chunks of a run in
+  // flight); inner lists capped at 2^kMaxInnerBits entries (streamed)
   static int lam = -1;
   if (lam < 0) {
     const char* e = getenv("RFR_LAMBDA_LOG");
     lam = e ? atoi(e) : 8;
   }
-  const int ao = clampi(alpha - r - lam, alpha > kMaxInnerBits ? alpha - kMaxInnerBits : 0, kMaxOuterBits);
-  const int bo = clampi(beta - r - lam, beta > kMaxInnerBits ? beta - kMaxInnerBits : 0, kMaxOuterBits);
+  int warps_log = 0;
+  while ((1 << (warps_log + 1)) <= 512 / kJoinCtasPerSm / 32) warps_log++;
+  auto outer_bits = [&](int side) {
+    const int want = side - r - lam > warps_log ? side - r - lam : warps_log;
+    return clampi(want, side > kMaxInnerBits ? side - kMaxInnerBits : 0,
+                  side < kMaxOuterBits ? side : kMaxOuterBits);
+  };
+  const int ao = outer_bits(alpha), bo = outer_bits(beta);
   const int ai = alpha - ao, bi = beta - bo;
   if (ai > kMaxInnerBits || bi > kMaxInnerBits)
     return rfr_fail(RFR_E_WIDTH, "inner list too large (n=%d)", n);
