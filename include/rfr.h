@@ -98,6 +98,20 @@ int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, in
                     int nshards, uint64_t* out, int64_t cap, int64_t* nout, rfr_stats* st);
 
 /*
+ * Factor-mode search with a secondary key: the patterns of rfr_search_keys
+ * that also satisfy (sum_{i in t} keys2[i] - lo2) mod 2^64 <= width2, the
+ * second window applied on the device to the raw hits.  keys2 are the
+ * fixed-point fractional parts of the third power sums of the entities (an
+ * integer for every true factor), so this adds the trace test of
+ * R/verify.py:123-138 at m = 3 in front of verification; it cuts
+ * Swinnerton-Dyer-like inputs, where Tr1 and Tr2 are integral for millions
+ * of non-factors, to a handful of candidates.  Same output protocol.
+ */
+int rfr_search_keys2(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                     uint64_t lo2, uint64_t width2, int shard, int nshards, uint64_t* out,
+                     int64_t cap, int64_t* nout, rfr_stats* st);
+
+/*
  * Device-resident variant for inputs already in HBM: d_keys (n uint64) and
  * d_out (cap uint64) are device pointers, *d_count a device uint64 that
  * receives the true count.  Enqueued on `stream` (cudaStream_t, NULL = the

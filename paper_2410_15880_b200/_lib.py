@@ -30,6 +30,7 @@ EXPORTS = (
     "rfr_num_sms",
     "rfr_recombine_e",
     "rfr_search_keys",
+    "rfr_search_keys2",
     "rfr_search_keys_dev",
     "rfr_verify",
     "rfr_verify_primes",
@@ -118,6 +119,11 @@ def load():
         L.rfr_search_keys.argtypes = [
             U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
             U64_P, ctypes.c_int64, I64_P, ctypes.POINTER(RfrStats),
+        ]
+        L.rfr_search_keys2.argtypes = [
+            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
+            ctypes.c_uint64, ctypes.c_int, ctypes.c_int, U64_P, ctypes.c_int64, I64_P,
+            ctypes.POINTER(RfrStats),
         ]
         L.rfr_search_keys_dev.argtypes = [
             ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,

@@ -74,7 +74,7 @@ struct Ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  DevVec keys, rho, raw, post, ctr, rotc, splits;
+  DevVec keys, keys2, rho, raw, post, ctr, rotc, splits;
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
@@ -334,6 +334,7 @@ int rfr_shutdown(void) {
   g.rho.release();
   g.raw.release();
   g.post.release();
+  g.keys2.release();
   g.rotc.release();
   g.splits.release();
   g.vprof.release();
@@ -357,7 +358,8 @@ int rfr_shutdown(void) {
 
 static int run_search_host(const uint64_t* h_keys, const double* h_rho, int n, uint64_t lo,
                            uint64_t width, double eps, int shard, int nshards, uint64_t* out,
-                           int64_t cap, int64_t* nout, rfr_stats* st) {
+                           int64_t cap, int64_t* nout, rfr_stats* st,
+                           const uint64_t* h_keys2 = nullptr, uint64_t lo2 = 0, uint64_t width2 = 0) {
   int rc = ensure_ready();
   if (rc) return rc;
   if ((rc = check_n(n))) return rc;
@@ -376,6 +378,10 @@ static int run_search_host(const uint64_t* h_keys, const double* h_rho, int n, u
     RFR_CUDA_OK(launch_rho_keys((const double*)g.rho.p, n, (uint64_t*)g.keys.p, s));
   } else {
     RFR_CUDA_OK(cudaMemcpyAsync(g.keys.p, h_keys, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    if (h_keys2) {
+      RFR_CUDA_OK(g.keys2.ensure(64 * sizeof(uint64_t)));
+      RFR_CUDA_OK(cudaMemcpyAsync(g.keys2.p, h_keys2, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    }
   }
   int r_bits = 0, nwin = 0;
   unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
@@ -410,6 +416,33 @@ static int run_search_host(const uint64_t* h_keys, const double* h_rho, int n, u
     c = *g.h_ctr;
     count = c.post_count;
     d_res = (const uint64_t*)g.post.p;
+  } else if (h_keys2) {
+    // secondary key window on the device; the survivors are a subset of the
+    // raw hits, so copying min(raw, cap) entries with the counters needs no
+    // second synchronisation
+    RFR_CUDA_OK(g.post.ensure((count ? count : 1) * sizeof(uint64_t)));
+    g_launches += 1;
+    RFR_CUDA_OK(launch_keyfilter((const uint64_t*)g.keys2.p, n, (const uint64_t*)g.raw.p,
+                                 &d_ctr->out_count, raw_cap, lo2, width2, (uint64_t*)g.post.p,
+                                 g.post.bytes / sizeof(uint64_t), d_ctr, g.nsm, s));
+    RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    const unsigned long long pre = count < (unsigned long long)cap ? count : (unsigned long long)cap;
+    if (pre)
+      RFR_CUDA_OK(cudaMemcpyAsync(out, g.post.p, pre * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    c = *g.h_ctr;
+    count = c.post_count;
+    *nout = (int64_t)count;
+    if (st) {
+      fill_stats(st, c, n, r_bits, nwin);
+      st->raw_hits = (int64_t)c.out_count;
+      st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
+      st->ms_join = ev_ms(g.ev[1], g.ev[2]);
+      st->ms_post = ev_ms(g.ev[2], g.ev[3]);
+      st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+    }
+    return RFR_OK;
   } else {
     RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
   }
@@ -456,6 +489,15 @@ int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, in
   std::lock_guard<std::mutex> lk(g_mu);
   if (!keys && n > 0) return rfr_fail(RFR_E_ARG, "null keys");
   return run_search_host(keys, nullptr, n, lo, width, 0.0, shard, nshards, out, cap, nout, st);
+}
+
+int rfr_search_keys2(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                     uint64_t lo2, uint64_t width2, int shard, int nshards, uint64_t* out,
+                     int64_t cap, int64_t* nout, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((!keys || !keys2) && n > 0) return rfr_fail(RFR_E_ARG, "null keys");
+  return run_search_host(keys, nullptr, n, lo, width, 0.0, shard, nshards, out, cap, nout, st, keys2,
+                         lo2, width2);
 }
 
 int rfr_search_keys_dev(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard,

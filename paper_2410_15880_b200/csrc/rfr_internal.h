@@ -11,6 +11,10 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
                          uint32_t* d_rot, uint32_t* d_split, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s);
+cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_in,
+                             const unsigned long long* d_in_count, unsigned long long cap_in,
+                             uint64_t lo2, uint64_t width2, uint64_t* d_out,
+                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            const unsigned long long* d_in_count, unsigned long long cap_in,
                            double eps, uint64_t* d_out, unsigned long long cap_out,

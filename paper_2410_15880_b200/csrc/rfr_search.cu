@@ -14,6 +14,7 @@
 //   join_kernel              bucket-walk generation + smem counting sort +
 //                            windowed probe; emits matching patterns
 //   recheck_kernel           parity mode: reference float64 value/accept
+//   keyfilter_kernel         factor mode: secondary (third power sum) key window
 //                            (recombine.py:106-123, :148-162) on every hit
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -369,6 +370,35 @@ __global__ void recheck_kernel(const double* __restrict__ rho, const uint64_t* _
   }
 }
 
+// Factor mode, secondary key: keep the raw hits t whose second key sum lies
+// in the window, (sum_{i in t} keys2[i] - lo2) mod 2^64 <= width2 (the third
+// power sum of a true factor is an integer, so its key sum is near 0).
+__global__ void keyfilter_kernel(const uint64_t* __restrict__ keys2, int n,
+                                 const uint64_t* __restrict__ in,
+                                 const unsigned long long* __restrict__ in_count,
+                                 unsigned long long cap_in, uint64_t lo2, uint64_t width2,
+                                 uint64_t* __restrict__ out, unsigned long long cap_out,
+                                 DevCounters* ctr) {
+  __shared__ uint64_t sk[64];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = keys2[i];
+  __syncthreads();
+  unsigned long long m = *in_count;
+  if (m > cap_in) m = cap_in;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t t = in[i];
+    uint64_t sum = 0, u = t;
+    while (u) {
+      sum += sk[__ffsll((long long)u) - 1];
+      u &= u - 1;
+    }
+    if (sum - lo2 <= width2) {
+      const unsigned long long k = atomicAdd(&ctr->post_count, 1ull);
+      if (k < cap_out) out[k] = t;
+    }
+  }
+}
+
 // Parity-mode keys: round(rho * 2^64) mod 2^64 (exact: rho * 2^64 is an
 // exact double; values >= 2^63 are split before the unsigned conversion).
 __global__ void rho_keys_kernel(const double* __restrict__ rho, int n, uint64_t* __restrict__ keys) {
@@ -496,6 +526,15 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in, const unsi
                            unsigned long long cap_in, double eps, uint64_t* d_out,
                            unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s) {
   recheck_kernel<<<nsm * 4, 256, 0, s>>>(d_rho, d_in, d_in_count, cap_in, eps, d_out, cap_out, d_ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_in,
+                             const unsigned long long* d_in_count, unsigned long long cap_in,
+                             uint64_t lo2, uint64_t width2, uint64_t* d_out,
+                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s) {
+  keyfilter_kernel<<<nsm * 4, 256, 0, s>>>(d_keys2, n, d_in, d_in_count, cap_in, lo2, width2, d_out,
+                                          cap_out, d_ctr);
   return cudaGetLastError();
 }
 

@@ -59,17 +59,20 @@ def allgather_patterns(local: np.ndarray) -> np.ndarray:
 
 
 def sharded_search_keys(keys: np.ndarray, half_width: int, workers: int,
-                        stats: RecombineStats | None = None) -> np.ndarray:
+                        stats: RecombineStats | None = None, keys2: np.ndarray | None = None,
+                        half_width2: int = 0) -> np.ndarray:
     """Factor-mode search split into `workers` key-range shards: this rank's
     shard(s) on its GPU, then an all-gather of the candidate patterns."""
+    kw = dict(keys2=keys2, half_width2=half_width2)
     dist = _dist()
     if dist is not None:
         world, rank = dist.get_world_size(), dist.get_rank()
         mine = [g for g in range(workers) if g % world == rank]
-        local = [search_keys(keys, half_width, stats, shard=g, nshards=workers) for g in mine]
+        local = [search_keys(keys, half_width, stats, shard=g, nshards=workers, **kw) for g in mine]
         local = np.concatenate(local) if local else np.zeros(0, dtype=np.uint64)
         return allgather_patterns(local)
-    parts = [search_keys(keys, half_width, stats, shard=g, nshards=workers) for g in range(workers)]
+    parts = [search_keys(keys, half_width, stats, shard=g, nshards=workers, **kw)
+             for g in range(workers)]
     return np.sort(np.concatenate(parts))
 
 

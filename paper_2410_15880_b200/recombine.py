@@ -176,10 +176,20 @@ def recombine_e(rho: RhoVector, eps: float, stats: RecombineStats | None = None,
     return CandidateSet(frozenset(int(v) for v in out[: nout.value]), n)
 
 
+def _window(half_width: int) -> tuple[int, int]:
+    T = int(half_width)
+    if 2 * T >= (1 << 64) - 1:
+        return 0, (1 << 64) - 1
+    return (-T) % (1 << 64), 2 * T
+
+
 def search_keys(keys: np.ndarray, half_width: int, stats: RecombineStats | None = None,
-                shard: int = 0, nshards: int = 1) -> np.ndarray:
+                shard: int = 0, nshards: int = 1, keys2: np.ndarray | None = None,
+                half_width2: int = 0) -> np.ndarray:
     """Factor-mode search: sorted uint64 patterns t < 2^(n-1) whose key sum
-    lies within +-half_width of 0 (mod 2^64)."""
+    lies within +-half_width of 0 (mod 2^64) -- and, when ``keys2`` is given,
+    whose ``keys2`` sum lies within +-half_width2 of 0 as well (the secondary
+    window is applied on the device, ``rfr_search_keys2``)."""
     keys = np.ascontiguousarray(keys, dtype=np.uint64)
     n = len(keys)
     _guard_width(n)
@@ -187,22 +197,27 @@ def search_keys(keys: np.ndarray, half_width: int, stats: RecombineStats | None 
         return np.zeros(0, dtype=np.uint64)
     lib = _lib.load()
     _lib.device()
-    T = int(half_width)
-    if 2 * T >= (1 << 64) - 1:
-        lo, width = 0, (1 << 64) - 1
-    else:
-        lo, width = (-T) % (1 << 64), 2 * T
+    lo, width = _window(half_width)
+    if keys2 is not None:
+        keys2 = np.ascontiguousarray(keys2, dtype=np.uint64)
+        if len(keys2) != n:
+            raise ValueError("keys2 must have one key per rho entry")
+        lo2, width2 = _window(half_width2)
     cap = 1 << 12
     while True:
         out = np.empty(cap, dtype=np.uint64)
         nout = ctypes.c_int64(0)
         st = _lib.RfrStats()
-        _lib.check(
-            lib.rfr_search_keys(_lib.ptr(keys, _lib.U64_P), n, lo, width, shard, nshards,
-                                _lib.ptr(out, _lib.U64_P), cap, ctypes.byref(nout),
-                                ctypes.byref(st)),
-            "rfr_search_keys",
-        )
+        if keys2 is None:
+            rc = lib.rfr_search_keys(_lib.ptr(keys, _lib.U64_P), n, lo, width, shard, nshards,
+                                     _lib.ptr(out, _lib.U64_P), cap, ctypes.byref(nout),
+                                     ctypes.byref(st))
+        else:
+            rc = lib.rfr_search_keys2(_lib.ptr(keys, _lib.U64_P), n, lo, width,
+                                      _lib.ptr(keys2, _lib.U64_P), lo2, width2, shard, nshards,
+                                      _lib.ptr(out, _lib.U64_P), cap, ctypes.byref(nout),
+                                      ctypes.byref(st))
+        _lib.check(rc, "rfr_search_keys")
         if nout.value <= cap:
             break
         cap = int(nout.value)

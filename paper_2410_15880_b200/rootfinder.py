@@ -81,8 +81,10 @@ class RootProfile:
     prod_lo: np.ndarray | None = field(default=None, repr=False, compare=False)
     keys1: np.ndarray | None = field(default=None, repr=False, compare=False)
     keys2: np.ndarray | None = field(default=None, repr=False, compare=False)
+    keys3: np.ndarray | None = field(default=None, repr=False, compare=False)
     key_err1: int = field(default=0, repr=False, compare=False)
     key_err2: int = field(default=0, repr=False, compare=False)
+    key_err3: int = field(default=0, repr=False, compare=False)
     root_err: float = field(default=0.0, repr=False, compare=False)
 
     @property
@@ -272,12 +274,15 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
     double entities, the 64-bit keys in rho order and their error bounds."""
     re_hi, re_lo, im_hi, im_lo, err = hp_roots(p)
     reals, pairs = _pair_up(re_hi, re_lo, im_hi, im_lo, err)
-    ents = []  # (rho, value R (Fraction), tau (Fraction), errR, errTau, kind, data)
+    # (kind, R = first power sum, tau = second, errR, errTau, data, p3 = third, errP3)
+    ents = []
     # exact rationals of the double-double values
     for i in reals:
         u = _dd_frac(re_hi[i], re_lo[i])
         du = float(err[i])
-        ents.append(("r", u, u * u, du, 2 * abs(float(u)) * du + du * du, i))
+        au = abs(float(u))
+        ents.append(("r", u, u * u, du, 2 * au * du + du * du, i, u * u * u,
+                     3 * au * au * du + 3 * au * du * du + du ** 3))
     for a, b in pairs:
         # symmetrise: z = (z_a + conj z_b) / 2
         re = (_dd_frac(re_hi[a], re_lo[a]) + _dd_frac(re_hi[b], re_lo[b])) / 2
@@ -290,21 +295,25 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         dm = 2 * mod * dz + dz * dz
         tau = t * t - 2 * m
         dtau = 2 * abs(float(t)) * dt + dt * dt + 2 * dm
-        ents.append(("p", t, tau, dt, dtau, m))
+        # z^3 + conj(z)^3 = t^3 - 3 t m
+        at, am = abs(float(t)), abs(float(m))
+        p3 = t * t * t - 3 * t * m
+        dp3 = 3 * at * at * dt + 3 * at * dt * dt + dt ** 3 + 3 * (at * dm + am * dt + dt * dm)
+        ents.append(("p", t, tau, dt, dtau, m, p3, dp3))
     rows = []
-    for kind, R, tau, dR, dtau, extra in ents:
+    for kind, R, tau, dR, dtau, extra, p3, dp3 in ents:
         fr = R - math.floor(R)
         rho = float(fr)
         if rho >= 1.0:
             rho = math.nextafter(1.0, 0.0)
-        rows.append((rho, kind, R, tau, dR, dtau, extra))
+        rows.append((rho, kind, R, tau, dR, dtau, extra, p3, dp3))
     # sort by rho (ties: reals before pairs, then value) -- any fixed order works
     order = sorted(range(len(rows)), key=lambda k: (rows[k][0], rows[k][1], float(rows[k][2])))
     r = len(reals)
     real_hi, real_lo, sum_hi, sum_lo, prod_hi, prod_lo = [], [], [], [], [], []
     perm = []
-    keys1, keys2 = [], []
-    e1 = e2 = 0.0
+    keys1, keys2, keys3 = [], [], []
+    e1 = e2 = e3 = 0.0
     # entities are numbered reals first (in rho order), then pairs (in rho order)
     real_rows = [k for k in order if rows[k][1] == "r"]
     pair_rows = [k for k in order if rows[k][1] == "p"]
@@ -324,13 +333,15 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         prod_lo.append(ml)
     rho = []
     for k in order:
-        rho_k, kind, R, tau, dR, dtau, _ = rows[k]
+        rho_k, kind, R, tau, dR, dtau, _, p3, dp3 = rows[k]
         rho.append(rho_k)
         perm.append(ent_of[k])
         keys1.append(math.floor((R - math.floor(R)) * _TWO64 + Fraction(1, 2)) % _TWO64)
         keys2.append(math.floor((tau - math.floor(tau)) * _TWO64 + Fraction(1, 2)) % _TWO64)
+        keys3.append(math.floor((p3 - math.floor(p3)) * _TWO64 + Fraction(1, 2)) % _TWO64)
         e1 += dR * 2.0**64 + 1.0
         e2 += dtau * 2.0**64 + 1.0
+        e3 += dp3 * 2.0**64 + 1.0
     root_err = float(max(err)) if len(err) else 0.0
     # double-double representation slack of the stored entity values
     root_err = root_err + 2.0**-100 * max([1.0] + [abs(v) for v in real_hi + sum_hi])
@@ -345,8 +356,10 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         prod_lo=np.asarray(prod_lo, dtype=np.float64),
         keys1=np.asarray(keys1, dtype=np.uint64),
         keys2=np.asarray(keys2, dtype=np.uint64),
+        keys3=np.asarray(keys3, dtype=np.uint64),
         key_err1=int(math.ceil(e1)),
         key_err2=int(math.ceil(e2)),
+        key_err3=int(math.ceil(min(e3, 2.0**66))),
         root_err=root_err,
     )
 

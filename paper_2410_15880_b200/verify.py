@@ -11,7 +11,10 @@ Pipeline for one monic square-free part p:
   1. host (not timed, ``root_seconds``): hp_profile -- roots to ~2^-100,
      exact 64-bit keys of the first two power sums, window half-width T;
   2. GPU (``recombine_seconds``): search every pattern t < 2^(n-1) whose key
-     sum is within +-T of 0 -- the true factors and a handful of false hits;
+     sum is within +-T of 0, then keep those whose third-power-sum key sum
+     is within +-T3 of 0 (device filter) -- the true factors and a handful
+     of false hits (also for Swinnerton-Dyer inputs, where Tr1 and Tr2 are
+     integral for millions of non-factors);
   3. GPU (``verify_seconds``): one warp per candidate expands the smaller
      side in double-double, checks integrality against a derived error bound
      and trial-divides p modulo three primes below 2^63 (R/verify.py:60-155);
@@ -100,6 +103,14 @@ def _search_window(prof: RootProfile) -> tuple[np.ndarray, int]:
     keys = ((prof.keys1.astype(object) + prof.keys2.astype(object)) % (1 << 64)).astype(np.uint64)
     T = KEY_SAFETY * (prof.key_err1 + prof.key_err2) + prof.n + 64
     return keys, T
+
+
+def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
+    """Third-power-sum keys and half-width (the device's secondary filter),
+    or (None, 0) for a profile without them."""
+    if prof.keys3 is None:
+        return None, 0
+    return prof.keys3, KEY_SAFETY * prof.key_err3 + prof.n + 64
 
 
 def _p_mod(p: IntPolynomial) -> np.ndarray:
@@ -210,12 +221,13 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
 
     t0 = time.perf_counter()
     keys, T = _search_window(prof)
+    keys3, T3 = _secondary_window(prof)
     if workers > 1:
         from .parallel import sharded_search_keys
 
-        pats = sharded_search_keys(keys, T, workers, stats.recombine)
+        pats = sharded_search_keys(keys, T, workers, stats.recombine, keys2=keys3, half_width2=T3)
     else:
-        pats = search_keys(keys, T, stats.recombine)
+        pats = search_keys(keys, T, stats.recombine, keys2=keys3, half_width2=T3)
     pats = pats[pats != 0]
     stats.recombine_seconds += time.perf_counter() - t0
     stats.candidates += len(pats)

@@ -48,7 +48,13 @@ def test_version_and_primes():
     assert lib.rfr_verify_primes(primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))) == 0
     import sympy
 
-    assert all(sympy.isprime(int(q)) and int(q) < (1 << 61) for q in primes)
+    # primes below 2^63 of the form 2^k - c, c small (the verify kernel's
+    # two-fold reduction needs z < 2P after folding: c + c^2 << P)
+    for q in (int(v) for v in primes):
+        k = q.bit_length()
+        assert sympy.isprime(q) and q < (1 << 63)
+        assert (1 << k) - q < (1 << 10)
+    assert len(set(int(v) for v in primes)) == 3
 
 
 def _polish(coeffs, seeds):

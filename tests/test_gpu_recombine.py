@@ -86,6 +86,29 @@ def test_search_keys_matches_window_oracle(seed):
         assert np.array_equal(got, want), (n, T)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_search_keys2_matches_two_window_oracle(seed):
+    """rfr_search_keys2: the first-window set of the oracle, filtered by the
+    second key window (computed here exactly on Python ints)."""
+    rng = random.Random(100 + seed)
+    for _ in range(8):
+        n = rng.randint(1, 24)
+        keys = np.array([rng.getrandbits(64) for _ in range(n)], dtype=np.uint64)
+        keys2 = np.array([rng.getrandbits(64) for _ in range(n)], dtype=np.uint64)
+        T = rng.choice([0, 1000, 1 << 50, 1 << 58, 1 << 61])
+        T2 = rng.choice([0, 1 << 40, 1 << 60, 1 << 62, (1 << 63)])
+        got = search_keys(keys, T, keys2=keys2, half_width2=T2)
+        first = _oracle_keys(keys, T)
+        k2 = [int(v) for v in keys2]
+
+        def ok(t):
+            s = sum(k2[i] for i in range(n) if (int(t) >> i) & 1) % TWO64
+            return (s + T2) % TWO64 <= 2 * T2
+
+        want = np.array([t for t in first if ok(t)], dtype=np.uint64)
+        assert np.array_equal(got, want), (n, T, T2)
+
+
 def test_search_keys_skewed_duplicates_match_oracle():
     # heavy duplicates: few distinct keys drive buckets past their capacity
     rng = random.Random(9)
