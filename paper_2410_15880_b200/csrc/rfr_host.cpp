@@ -176,43 +176,74 @@ int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double
   return status;
 }
 
-static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) {
-  return (uint64_t)(((unsigned __int128)a * b) % q);
-}
-static inline uint64_t powmod(uint64_t a, uint64_t e, uint64_t q) {
-  uint64_t r = 1 % q;
-  while (e) {
-    if (e & 1) r = mulmod(r, a, q);
-    a = mulmod(a, a, q);
-    e >>= 1;
+// a * b mod q; for q = 2^k - c with small c (every prime the library uses)
+// the 2k-bit product is folded twice with 2^k = c (mod q) instead of the
+// 128-bit division.
+struct Modulus {
+  uint64_t q, c;
+  int k;  // 0: generic modulus (128-bit remainder)
+  explicit Modulus(uint64_t q_) : q(q_), c(0), k(0) {
+    const int kk = 64 - __builtin_clzll(q_);
+    if (kk <= 63) {
+      const uint64_t cc = (1ull << kk) - q_;
+      if (cc < 1024) {
+        k = kk;
+        c = cc;
+      }
+    }
   }
-  return r;
+};
+static inline uint64_t mulmod(uint64_t a, uint64_t b, const Modulus M) {
+  const unsigned __int128 x = (unsigned __int128)a * b;
+  if (!M.k) return (uint64_t)(x % M.q);
+  const uint64_t mask = (1ull << M.k) - 1ull;
+  const unsigned __int128 y = (unsigned __int128)(uint64_t)(x >> M.k) * M.c + (uint64_t)(x & mask);
+  uint64_t z = (uint64_t)(y & mask) + (uint64_t)(y >> M.k) * M.c;
+  while (z >= M.q) z -= M.q;
+  return z;
 }
+extern "C++" {
+// Reducers for the Euclid loop: the Mersenne prime 2^61 - 1 (the screen's
+// first choice) and any other modulus.
+struct RedM61 {
+  static constexpr uint64_t q = (1ull << 61) - 1;
+  uint64_t mul(uint64_t a, uint64_t b) const {
+    const unsigned __int128 x = (unsigned __int128)a * b;
+    uint64_t z = (uint64_t)(x & q) + (uint64_t)(x >> 61);
+    z = (z & q) + (z >> 61);
+    return z >= q ? z - q : z;
+  }
+};
+struct RedAny {
+  Modulus M;
+  uint64_t mul(uint64_t a, uint64_t b) const { return mulmod(a, b, M); }
+};
 
-int rfr_squarefree_mod(const uint64_t* cm, int d, uint64_t q) {
-  if (d < 1 || q < 3) return 0;
-  if (cm[d] % q == 0) return 0;
-  if (d == 1) return 1;
+template <class Red>
+static int squarefree_euclid(const uint64_t* cm, int d, uint64_t q, const Red R) {
   std::vector<uint64_t> a(cm, cm + d + 1), b(d);
   for (auto& v : a) v %= q;
-  for (int k = 1; k <= d; k++) b[k - 1] = mulmod(a[k], (uint64_t)k % q, q);
+  for (int k = 1; k <= d; k++) b[k - 1] = R.mul(a[k], (uint64_t)k % q);
   int da = d, db = d - 1;
   while (db >= 0 && b[db] == 0) db--;
   if (db < 0) return 0;  // p' == 0 mod q: undecided
-  // Euclid over F_q
+  // Euclid over F_q by pseudo-division (a <- lc(b) a - lc(a) x^s b): no
+  // inverses, whose dependent chains would dominate; only the degree of the
+  // gcd matters, and scaling by the unit lc(b) does not change it
   while (db >= 0) {
-    const uint64_t inv = powmod(b[db], q - 2, q);
+    uint64_t* A = a.data();
+    const uint64_t* B = b.data();
+    const uint64_t lb = B[db];
     while (da >= db) {
-      const uint64_t f = mulmod(a[da], inv, q);
-      if (f) {
-        for (int k = 0; k <= db; k++) {
-          const uint64_t sub = mulmod(f, b[k], q);
-          const int idx = da - db + k;
-          a[idx] = a[idx] >= sub ? a[idx] - sub : a[idx] + q - sub;
-        }
+      const uint64_t la = A[da];
+      const int s0 = da - db;
+      for (int k = 0; k < s0; k++) A[k] = R.mul(A[k], lb);
+      for (int k = 0; k < db; k++) {
+        const uint64_t x = R.mul(A[s0 + k], lb), y = R.mul(la, B[k]);
+        A[s0 + k] = x >= y ? x - y : x + q - y;
       }
       da--;
-      while (da >= 0 && a[da] == 0) da--;
+      while (da >= 0 && A[da] == 0) da--;
       if (da < 0) break;
     }
     std::swap(a, b);
@@ -221,6 +252,15 @@ int rfr_squarefree_mod(const uint64_t* cm, int d, uint64_t q) {
   }
   // gcd is a (degree da)
   return da == 0 ? 1 : 0;
+}
+}  // extern "C++"
+
+int rfr_squarefree_mod(const uint64_t* cm, int d, uint64_t q) {
+  if (d < 1 || q < 3) return 0;
+  if (cm[d] % q == 0) return 0;
+  if (d == 1) return 1;
+  if (q == RedM61::q) return squarefree_euclid(cm, d, q, RedM61());
+  return squarefree_euclid(cm, d, q, RedAny{Modulus(q)});
 }
 
 }  // extern "C"
