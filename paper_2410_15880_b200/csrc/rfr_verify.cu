@@ -99,9 +99,31 @@ __device__ __forceinline__ uint64_t mulmod_k(uint64_t a, uint64_t b, uint64_t P,
   return z;
 }
 
+// The profile, staged once per CTA in shared memory: the product loop below
+// walks it serially, and global loads there would put an L2 round trip on
+// every step of the chain.
+struct ProfSmem {  // by entity e < n <= 64: real root / pair sum, pair product
+  double v_hi[kMaxE], v_lo[kMaxE];
+  double m_hi[kMaxE], m_lo[kMaxE];
+  int8_t perm[kMaxE];
+};
+
 __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A) {
   __shared__ WarpBuf bufs[kVerifyWarps];
+  __shared__ ProfSmem PS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < A.n; i += blockDim.x) PS.perm[i] = (int8_t)A.perm[i];
+  for (int i = threadIdx.x; i < A.r; i += blockDim.x) {
+    PS.v_hi[i] = A.real_hi[i];
+    PS.v_lo[i] = A.real_lo[i];
+  }
+  for (int i = threadIdx.x; i < A.c; i += blockDim.x) {
+    PS.v_hi[A.r + i] = A.sum_hi[i];
+    PS.v_lo[A.r + i] = A.sum_lo[i];
+    PS.m_hi[A.r + i] = A.prod_hi[i];
+    PS.m_lo[A.r + i] = A.prod_lo[i];
+  }
+  __syncthreads();
   WarpBuf& B = bufs[w];
   const long long k = (long long)blockIdx.x * kVerifyWarps + w;
   if (k >= A.m) return;
@@ -109,7 +131,7 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   const uint64_t s = A.pats[k] & full;
   int deg_s = 0;
   for (int i = 0; i < A.n; i++)
-    if ((s >> i) & 1ull) deg_s += A.perm[i] < A.r ? 1 : 2;
+    if ((s >> i) & 1ull) deg_s += PS.perm[i] < A.r ? 1 : 2;
   const bool use_comp = deg_s > A.d - deg_s;
   const uint64_t t = use_comp ? (~s & full) : s;
   const int e = use_comp ? A.d - deg_s : deg_s;
@@ -128,12 +150,12 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   }
   __syncwarp();
   const double de = A.root_err;
-  for (int i = 0; i < A.n; i++) {
-    if (!((t >> i) & 1ull)) continue;
-    const int ent = A.perm[i];
+  for (uint64_t tb = t; tb; tb &= tb - 1) {
+    const int i = __ffsll((long long)tb) - 1;
+    const int ent = PS.perm[i];
     const int nxt = cur ^ 1;
     if (ent < A.r) {
-      const ddv u = {A.real_hi[ent], A.real_lo[ent]};
+      const ddv u = {PS.v_hi[ent], PS.v_lo[ent]};
       const double au = fabs(u.hi);
       for (int j = lane; j <= len; j += 32) {
         ddv v = {0.0, 0.0};
@@ -148,9 +170,8 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
       }
       len += 1;
     } else {
-      const int jj = ent - A.r;
-      const ddv tt = {A.sum_hi[jj], A.sum_lo[jj]};
-      const ddv mm = {A.prod_hi[jj], A.prod_lo[jj]};
+      const ddv tt = {PS.v_hi[ent], PS.v_lo[ent]};
+      const ddv mm = {PS.m_hi[ent], PS.m_lo[ent]};
       const double at = fabs(tt.hi), am = fabs(mm.hi);
       const double dt = 2.0 * de, dm = 2.0 * sqrt(am) * de + de * de;
       for (int j = lane; j <= len + 1; j += 32) {
