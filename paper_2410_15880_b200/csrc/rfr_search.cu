@@ -297,27 +297,42 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   uint32_t i = lo, j = dt - lo;
   uint64_t ok[kMergeItems];
   uint32_t op[kMergeItems];
+  // both run heads held in registers: one shared key load per output
+  const uint64_t kInf = ~0ull;
+  uint64_t ka = i < na ? sK[kswz(i)] : kInf, kb = j < nb ? sK[kswz(na + j)] : kInf;
 #pragma unroll
   for (int t = 0; t < kMergeItems; t++) {
-    const bool takeA = j >= nb || (i < na && sK[kswz(i)] <= sK[kswz(na + j)]);
-    const uint32_t src = takeA ? i : na + j;
-    ok[t] = sK[kswz(src)];
-    op[t] = sP[pswz(src)];
-    if (takeA) i++;
-    else j++;
-  }
-  __syncthreads();
-  const uint32_t cnt = dt < tile ? min((uint32_t)kMergeItems, tile - dt) : 0u;
-#pragma unroll
-  for (int t = 0; t < kMergeItems; t++)
-    if ((uint32_t)t < cnt) {
-      sK[kswz(dt + t)] = ok[t];
-      sP[pswz(dt + t)] = op[t];
+    const bool takeA = j >= nb || (i < na && ka <= kb);
+    if (takeA) {
+      ok[t] = ka;
+      op[t] = sP[pswz(i)];
+      i++;
+      ka = i < na ? sK[kswz(i)] : kInf;
+    } else {
+      ok[t] = kb;
+      op[t] = sP[pswz(na + j)];
+      j++;
+      kb = j < nb ? sK[kswz(na + j)] : kInf;
     }
-  __syncthreads();
-  for (uint32_t t = tid; t < tile; t += kMergeThreads) {
-    O[d0 + t] = sK[kswz(t)];
-    Op[d0 + t] = sP[pswz(t)];
+  }
+  // each thread's run of outputs is contiguous and 64-byte aligned: store it
+  // directly with 16-byte vector stores (no staging round trip)
+  const uint32_t cnt = dt < tile ? min((uint32_t)kMergeItems, tile - dt) : 0u;
+  if (cnt == (uint32_t)kMergeItems) {
+    ulonglong2* ko = reinterpret_cast<ulonglong2*>(O + d0 + dt);
+#pragma unroll
+    for (int t = 0; t < kMergeItems / 2; t++) ko[t] = make_ulonglong2(ok[2 * t], ok[2 * t + 1]);
+    uint4* po = reinterpret_cast<uint4*>(Op + d0 + dt);
+#pragma unroll
+    for (int t = 0; t < kMergeItems / 4; t++)
+      po[t] = make_uint4(op[4 * t], op[4 * t + 1], op[4 * t + 2], op[4 * t + 3]);
+  } else {
+#pragma unroll
+    for (int t = 0; t < kMergeItems; t++)
+      if ((uint32_t)t < cnt) {
+        O[d0 + dt + t] = ok[t];
+        Op[d0 + dt + t] = op[t];
+      }
   }
   // next level's rotation start: # outputs < -v_{k+1}
   if (L.bits > k + 1) {
