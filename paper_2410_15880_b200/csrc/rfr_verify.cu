@@ -52,7 +52,7 @@ __device__ __forceinline__ ddv dd_mul(ddv a, ddv b) {
 }
 __device__ __forceinline__ ddv dd_neg(ddv a) { return {-a.hi, -a.lo}; }
 
-constexpr int kVerifyWarps = 8;
+constexpr int kVerifyWarps = 4;
 constexpr int kMaxE = 64;          // smaller side degree <= 64 (n <= 64 roots of p, d <= 128)
 constexpr int kMaxD = 128;
 
@@ -80,7 +80,7 @@ struct WarpBuf {
   ddv c[2][kMaxE + 2];
   double mag[2][kMaxE + 2];
   double magp[2][kMaxE + 2];
-  uint64_t rem[kMaxD + 1];
+  uint64_t rem[3][kMaxD + 1];  // p mod each prime, reduced in lockstep
   long long q[kMaxE + 1];
 };
 
@@ -231,39 +231,53 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
     return;
   }
 
-  // ---- trial division of p by q modulo three 61-bit primes
-  bool divides = true;
-  uint64_t* qm = reinterpret_cast<uint64_t*>(&B.mag[0][0]);  // q mod P (mag is dead here)
-  for (int pi = 0; pi < 3 && divides; pi++) {
-    const uint64_t P = A.primes[pi];
-    const int pk = 64 - __clzll((long long)P);  // P = 2^pk - pc
-    const uint64_t pc = (1ull << pk) - P;
+  // ---- trial division of p by q modulo three primes, the three divisions
+  // interleaved step by step (independent mulmod chains per lane)
+  uint64_t* qm0 = reinterpret_cast<uint64_t*>(&B.mag[0][0]);   // q mod P_i: the magnitude
+  uint64_t* qm1 = reinterpret_cast<uint64_t*>(&B.mag[1][0]);   // arrays are dead here
+  uint64_t* qm2 = reinterpret_cast<uint64_t*>(&B.magp[0][0]);
+  uint64_t* qmv[3] = {qm0, qm1, qm2};
+  uint64_t P[3], pc[3];
+  int pk[3];
+#pragma unroll
+  for (int pi = 0; pi < 3; pi++) {
+    P[pi] = A.primes[pi];
+    pk[pi] = 64 - __clzll((long long)P[pi]);  // P = 2^pk - pc
+    pc[pi] = (1ull << pk[pi]) - P[pi];
     const uint64_t* pm = A.p_mod + (size_t)pi * (A.d + 1);
-    for (int j = lane; j <= A.d; j += 32) B.rem[j] = pm[j];
+    for (int j = lane; j <= A.d; j += 32) B.rem[pi][j] = pm[j];
     for (int j = lane; j < e; j += 32) {  // |q_j| < 2^62, so one reduction each
       const long long qj = B.q[j];
       const uint64_t aq = qj >= 0 ? (uint64_t)qj : (uint64_t)(-qj);
-      const uint64_t r = aq % P;
-      qm[j] = (qj >= 0 || r == 0) ? r : P - r;
+      const uint64_t r = aq % P[pi];
+      qmv[pi][j] = (qj >= 0 || r == 0) ? r : P[pi] - r;
     }
+  }
+  __syncwarp();
+  for (int kk = A.d - e; kk >= 0; kk--) {
+    uint64_t lead[3];
+#pragma unroll
+    for (int pi = 0; pi < 3; pi++) lead[pi] = B.rem[pi][kk + e];  // q monic
     __syncwarp();
-    for (int kk = A.d - e; kk >= 0; kk--) {
-      const uint64_t lead = B.rem[kk + e];  // q monic
-      __syncwarp();
-      if (lead) {
-        for (int j = lane; j < e; j += 32) {
-          const uint64_t sub = mulmod_k(lead, qm[j], P, pk, pc);
-          const uint64_t r0 = B.rem[kk + j];
-          B.rem[kk + j] = r0 >= sub ? r0 - sub : r0 + P - sub;
+    // e <= 64: each lane owns coefficients lane and lane + 32; all six
+    // (coefficient, prime) mulmod chains of a lane are issued together
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int j = lane + 32 * h;
+      if (j < e) {
+#pragma unroll
+        for (int pi = 0; pi < 3; pi++) {
+          const uint64_t sub = mulmod_k(lead[pi], qmv[pi][j], P[pi], pk[pi], pc[pi]);
+          const uint64_t r0 = B.rem[pi][kk + j];
+          B.rem[pi][kk + j] = r0 >= sub ? r0 - sub : r0 + P[pi] - sub;
         }
       }
-      __syncwarp();
     }
-    bool nz = false;
-    for (int j = lane; j < e; j += 32) nz |= B.rem[j] != 0;
-    divides = !__any_sync(0xffffffffu, nz);
     __syncwarp();
   }
+  bool nz = false;
+  for (int j = lane; j < e; j += 32) nz |= (B.rem[0][j] | B.rem[1][j] | B.rem[2][j]) != 0;
+  const bool divides = !__any_sync(0xffffffffu, nz);
   if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
   if (divides)
     for (int j = lane; j <= e && j < A.stride; j += 32) A.coeffs[k * A.stride + j] = B.q[j];
