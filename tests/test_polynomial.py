@@ -101,3 +101,87 @@ def test_generator_validation():
         gen_random_reducible_parts(5, 10, 0, irreducible=lambda q: True)
     with pytest.raises(ValueError):
         gen_random_reducible_parts(8, 0, 0, irreducible=lambda q: True)
+
+
+def _school_mul(a, b):
+    out = [0] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            out[i + j] += x * y
+    return out
+
+
+def _school_div(p, q):
+    """Long division over Z (R/polynomial.py:155-183 semantics), plain lists."""
+    dp, dq = len(p) - 1, len(q) - 1
+    if dp < dq:
+        return None
+    rem, quot, lead = list(p), [0] * (dp - dq + 1), q[-1]
+    for k in range(dp - dq, -1, -1):
+        t, r = divmod(rem[k + dq], lead)
+        if r:
+            return None
+        quot[k] = t
+        for i in range(dq + 1):
+            rem[k + i] -= t * q[i]
+    return None if any(rem[:dq]) else quot
+
+
+def test_kronecker_multiply_and_divide_match_schoolbook():
+    """multiply / divide_exact switch to Kronecker substitution for large
+    degrees; both must agree with the schoolbook definitions exactly,
+    including huge coefficients, negative leads and near-miss dividends."""
+    from paper_2410_15880_b200.polynomial import divide_exact, multiply
+
+    rng = random.Random(11)
+    hits = 0
+    for _ in range(400):
+        dq, dr = rng.randint(0, 40), rng.randint(0, 40)
+        bits = rng.choice([2, 17, 64, 140])
+        q = [rng.randint(-(1 << bits), 1 << bits) for _ in range(dq)] + [rng.choice([1, -1, 3, -7])]
+        r = [rng.randint(-(1 << bits), 1 << bits) for _ in range(dr)] + [rng.choice([1, -2, 5])]
+        prod = multiply(P(q), P(r))
+        assert list(prod.coeffs) == list(P(_school_mul(q, r)).coeffs)
+        pc = list(prod.coeffs)
+        if rng.random() < 0.5:
+            pc[rng.randrange(len(pc))] += rng.choice([1, -1, 1 << bits])
+        got = divide_exact(P(pc), P(q))
+        want = _school_div(pc, q)
+        if want is None:
+            assert got is None
+        else:
+            hits += 1
+            assert got is not None and list(got.coeffs) == list(P(want).coeffs)
+    assert hits > 100
+
+
+def test_squarefree_screen_never_accepts_a_square():
+    """The native modular screen (rfr_squarefree_mod, pseudo-division Euclid)
+    answers 'square-free' only for square-free inputs (checked with sympy)."""
+    import ctypes
+
+    import numpy as np
+    import sympy
+
+    from paper_2410_15880_b200 import _lib
+
+    lib = _lib.load()
+    x = sympy.symbols("x")
+    rng = random.Random(5)
+    q = 2305843009213693951
+    accepted = 0
+    for _ in range(120):
+        d = rng.randint(2, 30)
+        co = [rng.randint(-50, 50) for _ in range(d)] + [1]
+        if rng.random() < 0.4:
+            f = [rng.randint(-5, 5) for _ in range(rng.randint(1, 3))] + [1]
+            pp = sympy.Poly(list(reversed(co)), x) * sympy.Poly(list(reversed(f)), x) ** 2
+            co = [int(c) for c in reversed(pp.all_coeffs())]
+        cm = np.array([c % q for c in co], dtype=np.uint64)
+        got = lib.rfr_squarefree_mod(cm.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(co) - 1, q)
+        poly = sympy.Poly(list(reversed(co)), x)
+        square_free = sympy.gcd(poly, poly.diff(x)).degree() == 0
+        if got == 1:
+            accepted += 1
+            assert square_free
+    assert accepted > 30
