@@ -1,28 +1,36 @@
 // rfr_join.cuh -- the bucket join kernel (included by rfr_search.cu).
 //
-// Each CTA owns a contiguous range of key buckets and walks it in order.  Per
-// bucket c (keys [cW, (c+1)W), W = 2^(64-r)):
+// Two CTAs per SM (8 warps each); each CTA owns a contiguous range of key
+// buckets and walks it in order.  Per bucket c (keys [cW, (c+1)W), W = 2^(64-r),
+// ~2^11 A records):
 //   A side   every A outer x contributes the contiguous run of its rotated
 //            inner list whose sums x + k fall in bucket c, followed by the
-//            halo run [(c+1)W, (c+1)W + H).  A group of gs lanes loads one
-//            window of gs consecutive keys of one outer (coalesced); because
-//            the sums are sorted, "main or halo" is a per-lane test and the
-//            emitted lanes are a prefix of the group.  kU windows are loaded
-//            before any is processed (kU loads in flight per lane).  A ballot
-//            compacts the records into the warp's own partition of the
-//            shared record array.
-//   A index  a three-level direct-mapped index with 2^15, 2^13 and 2^11 slots
-//            over the bucket (the reference's splat table, recombine.py:
-//            297-325, moved on chip): every record stores its index in its
-//            level-1 home with a plain store, reads it back after a barrier,
-//            and only the records that lost a slot collision move to the next
-//            level; the few level-3 losers go to a short list.  No shared
+//            halo run [(c+1)W, (c+1)W + H).  The plan gives each warp one
+//            outer per bucket with a long run (lambda ~ 256 records):
+//            run_pass loads all nch chunks of 32 consecutive inner keys of
+//            the run at once (coalesced, L1 no-allocate; the next bucket's
+//            lines were prefetched into L2), classifies each lane as main /
+//            halo / past the run (the emitted lanes are a prefix: the sums
+//            are sorted), and a ballot compacts the records into the warp's
+//            own partition of the shared record array.  Short runs (small n)
+//            use window_pass: lane groups of 2 lambda lanes per outer window.
+//   A index  a three-level direct-mapped index (8, 2 and 1/2 slots per
+//            record) over the bucket (the reference's splat table,
+//            recombine.py:297-325, moved on chip): every record stores its
+//            index in its level-1 home with a plain store, reads it back
+//            after a barrier, and only the records that lost a slot collision
+//            move to the next level (their level-1 slot gets a collision
+//            flag); the few level-3 losers go to a short list.  No shared
 //            atomics on this path: they cost ~2 cycles per lane on this part.
-//   B side   the same windows over B (negated, shifted keys); each emitted B
-//            lane reads its home slots in the three levels and checks the
-//            records it finds for exact window matches (the reference's
-//            windowed probe, recombine.py:328-358).
-//   Outers whose run fills its window continue one window at a time.
+//   B side   the same runs over B (negated, shifted keys); each emitted B
+//            record reads its level-1 home and the record it names and checks
+//            it exactly (the reference's windowed probe, recombine.py:
+//            328-358); records that meet a flagged slot (or span > 2 homes)
+//            are staged and probed at levels 2-3 out of line.
+//   Outers whose run outlasts the chunks in flight continue in
+//   continue_pass.  Loop state lives in shared memory and the shared base is
+//   re-derived at each use, so the pass calls (which may clobber every
+//   register) cost no local-memory reloads.
 // Pairs across a bucket boundary are found once: (A in c, B in c+1) by a B
 // halo record, (A in c+1, B in c) by an A halo record; halo x halo is skipped
 // (bucket c+1 finds it).  A bucket whose A side overflows its shared-memory
