@@ -113,11 +113,21 @@ def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
     return prof.keys3, KEY_SAFETY * prof.key_err3 + prof.n + 64
 
 
+_PRIMES: tuple[int, ...] | None = None
+
+
 def _p_mod(p: IntPolynomial) -> np.ndarray:
-    primes = np.zeros(3, dtype=np.uint64)
-    lib = _lib.load()
-    lib.rfr_verify_primes(primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
-    return np.array([[c % int(q) for c in p.coeffs] for q in primes], dtype=np.uint64)
+    """p's coefficients modulo the three verification primes (3 x (d+1))."""
+    global _PRIMES
+    if _PRIMES is None:
+        primes = np.zeros(3, dtype=np.uint64)
+        _lib.load().rfr_verify_primes(primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+        _PRIMES = tuple(int(q) for q in primes)
+    co = p.coeffs
+    if max(co) < (1 << 62) and min(co) > -(1 << 62):  # int64 fast path (Python sign rule)
+        a = np.array(co, dtype=np.int64)
+        return np.stack([np.remainder(a, np.int64(q)) for q in _PRIMES]).astype(np.uint64)
+    return np.array([[c % q for c in co] for q in _PRIMES], dtype=np.uint64)
 
 
 def verify_candidates(prof: RootProfile, p: IntPolynomial, pats: np.ndarray):
