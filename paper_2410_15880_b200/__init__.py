@@ -59,5 +59,6 @@ from .verify import (
     selected_degree,
     verify_candidates,
 )
+from .report import CSV_HEADER, BenchRecord, bench_rows
 
 __version__ = "0.1.0"
