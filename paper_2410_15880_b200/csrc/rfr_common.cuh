@@ -12,7 +12,7 @@ namespace rfr {
 // Largest quarter list walked by the join (2^23 entries = 64 MB of keys).
 constexpr int kMaxInnerBits = 28;  // inner lists up to 2^28 entries (12 B each, x2 ping-pong)
 // Outer lists live in shared memory of the join kernel.
-constexpr int kMaxOuterBits = 8;
+constexpr int kMaxOuterBits = 7;
 // Join geometry: RFR_JOIN_CTAS CTAs per SM, each walking buckets of
 // ~2^kJoinRecLog A records (the plan picks r = alpha - kJoinRecLog).
 #ifndef RFR_JOIN_CTAS

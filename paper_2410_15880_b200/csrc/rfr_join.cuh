@@ -61,9 +61,12 @@ constexpr int kStageB = kUB * 32;                     // staged B records per wa
 constexpr uint16_t kNone = 0xffffu;
 constexpr uint32_t kFlagCont = 0x80000000u;
 
+static_assert(kL2Log == kL1Log - 2 && kL3Log == kL1Log - 4,
+              "the level-2/3 homes are the level-1 home shifted right by 2 / 4");
 struct JoinSmem {
   uint64_t recK[kCapRec];  // A records: key
   uint32_t recI[kCapRec];  // A records: outer << inner_bits | inner index
+  uint16_t rh[kCapRec];     // A records: level-1 home (levels 2, 3: rh >> 2, rh >> 4)
   uint16_t t1[1 << kL1Log];
   uint16_t t2[1 << kL2Log];
   uint16_t t3[1 << kL3Log];
@@ -374,7 +377,9 @@ __device__ __noinline__ PassSt window_pass(const JoinArgs& a, uint64_t cW,
             const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
             S.recK[r] = sv[u];
             S.recI[r] = (i << aib) | jv[u];
-            S.t1[home_of(sv[u] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
+            const uint32_t h1 = home_of(sv[u] - cW, sh - kL1Log, kL1Log);
+            S.t1[h1] = (uint16_t)r;
+            S.rh[r] = (uint16_t)h1;
           }
           wfill += ne;
         }
@@ -457,7 +462,9 @@ __device__ __noinline__ PassSt continue_pass(const JoinArgs& a, uint64_t cW,
               const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
               S.recK[r] = s;
               S.recI[r] = (i << aib) | j;
-              S.t1[home_of(rel, sh - kL1Log, kL1Log)] = (uint16_t)r;
+              const uint32_t h1 = home_of(rel, sh - kL1Log, kL1Log);
+              S.t1[h1] = (uint16_t)r;
+              S.rh[r] = (uint16_t)h1;
             }
             wfill += ne;
           }
@@ -585,7 +592,9 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
             const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
             S.recK[r] = sv;
             S.recI[r] = (i << aib) | j;
-            S.t1[home_of(rel, K.sh - kL1Log, kL1Log)] = (uint16_t)r;
+            const uint32_t h1 = home_of(rel, K.sh - kL1Log, kL1Log);
+            S.t1[h1] = (uint16_t)r;
+            S.rh[r] = (uint16_t)h1;
           }
           if (!overflow) wfill += ne;
         } else {
@@ -624,12 +633,11 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
 // Build levels 2 and 3 from the level-1 losers (plain stores + read-back).
 // Called by every thread after the barrier that follows the level-1 stores;
 // returns after a barrier with S.n4 / S.ovf valid.
-__device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) {
+__device__ __noinline__ void build_index_levels() {
   JoinSmem& S = join_smem();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int sh = 64 - P.r;
   const uint32_t nw = S.wcnt[wid];
   uint16_t* lose = S.lose[wid];
   // level 1 read-back: losers go to level 2.  Four 32-record groups per
@@ -638,13 +646,11 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   uint32_t nl = 0;
   auto group = [&](uint32_t e0, auto Gc) {
     constexpr int G = decltype(Gc)::value;
-    uint64_t rel[G];
     uint32_t h1[G], occ[G];
 #pragma unroll
     for (int u = 0; u < G; u++) {
       const uint32_t e = e0 + u * 32 + lane;
-      rel[u] = (e < nw ? S.recK[wid * kPart + e] : cW) - cW;
-      h1[u] = home_of(rel[u], sh - kL1Log, kL1Log);
+      h1[u] = e < nw ? S.rh[wid * kPart + e] : 0u;
     }
 #pragma unroll
     for (int u = 0; u < G; u++) occ[u] = S.t1[h1[u]];
@@ -657,7 +663,7 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
       if (lost) {
         const uint32_t k = nl + __popc(lm & lt_mask);
         if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
-        S.t2[home_of(rel[u], sh - kL2Log, kL2Log)] = (uint16_t)r;
+        S.t2[h1[u] >> 2] = (uint16_t)r;
         S.t1[h1[u]] = (uint16_t)(occ[u] | 0x8000u);  // collision flag: B also probes levels 2-3
       }
       nl += __popc(lm);
@@ -677,18 +683,17 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   for (uint32_t e0 = 0; e0 < nlc; e0 += 32) {
     const uint32_t e = e0 + lane;
     bool lost = false;
-    uint32_t r = 0;
-    uint64_t rel = 0;
+    uint32_t r = 0, h1 = 0;
     if (e < nlc) {
       r = lose[e];
-      rel = S.recK[r] - cW;
-      lost = S.t2[home_of(rel, sh - kL2Log, kL2Log)] != (uint16_t)r;
+      h1 = S.rh[r];
+      lost = S.t2[h1 >> 2] != (uint16_t)r;
     }
     const uint32_t lm = __ballot_sync(FULL, lost);
     __syncwarp();
     if (lost) {
       lose[nl2 + __popc(lm & lt_mask)] = (uint16_t)r;  // compact in place (target <= e)
-      S.t3[home_of(rel, sh - kL3Log, kL3Log)] = (uint16_t)r;
+      S.t3[h1 >> 4] = (uint16_t)r;
     }
     nl2 += __popc(lm);
     __syncwarp();
@@ -698,7 +703,7 @@ __device__ __noinline__ void build_index_levels(const JoinPlan& P, uint64_t cW) 
   // level 3 read-back: losers go to the short list (rare: shared atomic)
   for (uint32_t e = lane; e < nl2; e += 32) {
     const uint32_t r = lose[e];
-    if (S.t3[home_of(S.recK[r] - cW, sh - kL3Log, kL3Log)] != (uint16_t)r) {
+    if (S.t3[S.rh[r] >> 4] != (uint16_t)r) {
       const unsigned k = atomicAdd(&S.n4, 1u);
       if (k < (unsigned)kList4) S.list4[k] = (uint16_t)r;
       else S.ovf = 1;
@@ -811,11 +816,13 @@ __device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_
       const uint32_t nw = S.wcnt[wid];
       for (uint32_t e = lane; e < nw; e += 32) {
         const uint32_t r = wid * kPart + e;
-        S.t1[home_of(S.recK[r] - cW, sh - kL1Log, kL1Log)] = (uint16_t)r;
+        const uint32_t h1 = home_of(S.recK[r] - cW, sh - kL1Log, kL1Log);
+        S.t1[h1] = (uint16_t)r;
+        S.rh[r] = (uint16_t)h1;
       }
     }
     __syncthreads();
-    build_index_levels(P, cW);
+    build_index_levels();
     if (S.ovf) {  // too many colliding records: redo this chunk with half the records
       __syncthreads();
       if (tid == 0) {
@@ -929,7 +936,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     __syncthreads();
     bool overflowed = join_smem().ovf != 0;
     if (!overflowed) {
-      build_index_levels(P, cW);
+      build_index_levels();
       overflowed = join_smem().ovf != 0;
     }
     RFR_MARK();
