@@ -109,7 +109,7 @@ namespace {
 int bit_length(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
 
 // Plan the quarter lists and buckets of one search.
-int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
+int make_plan(int n, uint64_t lo, uint64_t width, int nshards, JoinPlan* P) {
   memset(P, 0, sizeof *P);
   const int m = n - 1;
   const int alpha = (m + 1) / 2, beta = m - alpha;
@@ -131,8 +131,12 @@ int make_plan(int n, uint64_t lo, uint64_t width, JoinPlan* P) {
   }
   int warps_log = 0;
   while ((1 << (warps_log + 1)) <= 512 / kJoinCtasPerSm / 32) warps_log++;
+  // every shard rebuilds the whole quarter lists while the join is split
+  // nshards ways, so shorter runs (smaller inner lists) pay off on many GPUs
+  // (measured at n = 55: 256 is best up to 2 shards, 128 at 4, 64-128 at 8)
+  const int lam_s = lam - (nshards >= 4 ? 1 : 0) - (nshards >= 16 ? 1 : 0);
   auto outer_bits = [&](int side) {
-    const int want = side - r - lam > warps_log ? side - r - lam : warps_log;
+    const int want = side - r - lam_s > warps_log ? side - r - lam_s : warps_log;
     return clampi(want, side > kMaxInnerBits ? side - kMaxInnerBits : 0,
                   side < kMaxOuterBits ? side : kMaxOuterBits);
   };
@@ -227,7 +231,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
   *nwin = (int)wins.size();
   JoinPlan P0;
-  int rc = make_plan(n, wins[0].first, wins[0].second, &P0);
+  int rc = make_plan(n, wins[0].first, wins[0].second, nshards, &P0);
   if (rc) return rc;
   *r_bits = P0.r;
   rc = ensure_list_buffers(P0);
