@@ -130,7 +130,7 @@ int make_plan(int n, uint64_t lo, uint64_t width, int nshards, JoinPlan* P) {
     lam = e ? atoi(e) : 8;
   }
   int warps_log = 0;
-  while ((1 << (warps_log + 1)) <= 512 / kJoinCtasPerSm / 32) warps_log++;
+  while ((1 << (warps_log + 1)) <= kJoinThreadsPerCta / 32) warps_log++;
   // every shard rebuilds the whole quarter lists while the join is split
   // nshards ways, so shorter runs (smaller inner lists) pay off on many GPUs
   // (measured at n = 55: 256 is best up to 2 shards, 128 at 4, 64-128 at 8)

@@ -12,13 +12,20 @@ namespace rfr {
 // Largest quarter list walked by the join (2^23 entries = 64 MB of keys).
 constexpr int kMaxInnerBits = 28;  // inner lists up to 2^28 entries (12 B each, x2 ping-pong)
 // Outer lists live in shared memory of the join kernel.
-constexpr int kMaxOuterBits = 7;
+constexpr int kMaxOuterBits = 6;
 // Join geometry: RFR_JOIN_CTAS CTAs per SM, each walking buckets of
 // ~2^kJoinRecLog A records (the plan picks r = alpha - kJoinRecLog).
 #ifndef RFR_JOIN_CTAS
 #define RFR_JOIN_CTAS 2
 #endif
 constexpr int kJoinCtasPerSm = RFR_JOIN_CTAS;
+// threads per join CTA (default 256: 16 warps/SM at 128 registers).  A
+// 512-thread variant (32 warps/SM, 64 registers, lambda 128) spills in the
+// B pass and measured 60 % slower.
+#ifndef RFR_JOIN_THREADS
+#define RFR_JOIN_THREADS (512 / RFR_JOIN_CTAS)
+#endif
+constexpr int kJoinThreadsPerCta = RFR_JOIN_THREADS;
 constexpr int kJoinRecLog = RFR_JOIN_CTAS == 1 ? 12 : 11;
 // Sorted base block built in shared memory by the list builder.
 constexpr int kBaseBits = 12;

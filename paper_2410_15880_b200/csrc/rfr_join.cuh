@@ -46,18 +46,18 @@
 #define RFR_JOIN_TRACE 0
 #endif
 
-constexpr int kJoinThreads = 512 / kJoinCtasPerSm;
+constexpr int kJoinThreads = kJoinThreadsPerCta;
 constexpr int kJoinWarps = kJoinThreads / 32;
 // index levels (slots): 8, 2 and 1/2 slots per expected record
 constexpr int kL1Log = kJoinRecLog + 3, kL2Log = kJoinRecLog + 1, kL3Log = kJoinRecLog - 1;
-constexpr int kPart = 384;                   // A records per warp partition
+constexpr int kPart = (3 << kJoinRecLog) / 2 / kJoinWarps;  // A records per warp partition
 constexpr int kCapRec = kPart * kJoinWarps;  // A records per chunk (1.5x the expected)
-constexpr int kLose = 128;                            // per-warp level-1 loser list
+constexpr int kLose = kJoinWarps > 8 ? 64 : 128;                          // per-warp level-1 loser list
 constexpr int kList4 = 256;                           // level-3 losers (CTA list)
 constexpr int kMaxOuter = 1 << kMaxOuterBits;
 constexpr int kU = 8;                                 // A windows in flight per lane
-constexpr int kUB = 4;                                // B windows in flight per lane
-constexpr int kStageB = kUB * 32;                     // staged B records per warp
+constexpr int kUB = kJoinWarps > 8 ? 2 : 4;                             // B windows in flight per lane
+constexpr int kStageB = kJoinWarps > 8 ? 64 : kUB * 32;  // staged B records per warp
 constexpr uint16_t kNone = 0xffffu;
 constexpr uint32_t kFlagCont = 0x80000000u;
 
@@ -535,7 +535,7 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // offsets [32k, 32k + 32)); nch covers the expected run plus ~3 sigma.  An
 // outer whose last chunk is still full is flagged for continue_pass
 // (off = 32 * nch).  Same record semantics as window_pass.
-constexpr int kMaxCh = 12;
+constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
 template <bool SIDE_A>
 __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t lo, uint32_t hi,
                                       int nch, PassSt st) {
