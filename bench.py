@@ -56,19 +56,49 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    every 10 ms (a query takes ~1 ms), nvidia-smi every 200 ms as fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of active reason names)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self.source = None
+
+    def _run_nvml(self) -> bool:
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.device)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        except Exception:
+            return False
+        self.source = "nvml"
+        while not self._stop.is_set():
+            try:
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                r = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((sm, mx, {k for k, v in bits.items() if r & v}))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+        return True
 
     def _run(self):
+        if self._run_nvml():
+            return
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -76,7 +106,12 @@ class ClockSampler:
                      "--format=csv,noheader,nounits"],
                     capture_output=True, text=True, timeout=5).stdout.strip()
                 if out:
-                    self.samples.append([c.strip() for c in out.split(",")])
+                    c = [x.strip() for x in out.split(",")]
+                    sm = float(c[1]) if c[1].replace(".", "").isdigit() else None
+                    mx = float(c[2]) if c[2].replace(".", "").isdigit() else None
+                    rs = {nm for k, nm in enumerate(self.NAMES)
+                          if len(c) > 5 + k and c[5 + k].lower().startswith("active")}
+                    self.samples.append((sm, mx, rs))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -90,18 +125,15 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = sorted(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        mx = max((float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = sorted(x[0] for x in self.samples if x[0] is not None)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        mx = max((x[1] for x in self.samples if x[1] is not None), default=None)
         reasons = set()
-        for s in self.samples:
-            for k, nm in enumerate(names):
-                if len(s) > 5 + k and s[5 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        for x in self.samples:
+            reasons |= x[2]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": self.source}
 
 
 def load_inputs():
