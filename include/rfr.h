@@ -163,6 +163,19 @@ enum {
 int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const uint64_t* p_mod,
                int d, uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride,
                rfr_stats* st);
+/*
+ * Fused factor-mode search and verification (one call per factor() search on
+ * one device): rfr_search_keys2's candidate set, each candidate then verified
+ * on the device exactly as rfr_verify does, without the patterns leaving HBM
+ * in between.  Writes min(count, cap) patterns with their verdict / side /
+ * coefficients (layouts as rfr_verify; coeffs valid for PASS); *nout = true
+ * count (regrow and call again when it exceeds cap).  prof->n must equal n.
+ */
+int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                      uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
+                      int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
+                      int stride, int64_t cap, int64_t* nout, rfr_stats* st);
+
 /* The three primes of the modular division test (p_mod residues). */
 int rfr_verify_primes(uint64_t* primes3);
 

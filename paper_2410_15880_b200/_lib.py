@@ -31,6 +31,7 @@ EXPORTS = (
     "rfr_recombine_e",
     "rfr_search_keys",
     "rfr_search_keys2",
+    "rfr_search_verify",
     "rfr_search_keys_dev",
     "rfr_verify",
     "rfr_verify_primes",
@@ -136,6 +137,11 @@ def load():
         L.rfr_verify.argtypes = [
             ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int64, U64_P, ctypes.c_int, U8_P, U8_P,
             I64_P, ctypes.c_int, ctypes.POINTER(RfrStats),
+        ]
+        L.rfr_search_verify.argtypes = [
+            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
+            ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
+            I64_P, ctypes.c_int, ctypes.c_int64, I64_P, ctypes.POINTER(RfrStats),
         ]
         L.rfr_verify_primes.argtypes = [U64_P]
         L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]

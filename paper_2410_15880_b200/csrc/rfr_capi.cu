@@ -20,28 +20,6 @@
 
 using namespace rfr;
 
-namespace rfr {
-struct VerifyArgs {
-  int n, r, c, d;
-  const double* real_hi;
-  const double* real_lo;
-  const double* sum_hi;
-  const double* sum_lo;
-  const double* prod_hi;
-  const double* prod_lo;
-  const int32_t* perm;
-  double root_err;
-  const uint64_t* pats;
-  long long m;
-  const uint64_t* p_mod;
-  uint64_t primes[3];
-  uint8_t* verdict;
-  uint8_t* side;
-  long long* coeffs;
-  int stride;
-};
-cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s);
-}  // namespace rfr
 
 namespace {
 
@@ -495,6 +473,170 @@ int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, in
   return run_search_host(keys, nullptr, n, lo, width, 0.0, shard, nshards, out, cap, nout, st);
 }
 
+// Fused factor-mode search + verification: lists, join, secondary key window
+// and the verify kernel back to back on the device (the candidate patterns
+// never round-trip through the host); one staged H2D in, one batch of D2H out.
+int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                      uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
+                      int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
+                      int stride, int64_t cap, int64_t* nout, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if ((rc = check_n(n))) return rc;
+  if (!nout || cap < 0 || stride < 1 || !prof || !p_mod || d < 1 || d > 128)
+    return rfr_fail(RFR_E_ARG, "bad search_verify arguments");
+  if (prof->n != n || prof->r + 2 * prof->c != d || prof->r + prof->c != prof->n)
+    return rfr_fail(RFR_E_ARG, "profile does not match the keys / degree");
+  if (n == 0) {
+    *nout = 0;
+    fill_stats(st, DevCounters{}, 0, 0, 0);
+    return RFR_OK;
+  }
+  if (!keys || !keys2) return rfr_fail(RFR_E_ARG, "null keys");
+  cudaSetDevice(g.device);
+  cudaStream_t s = g.stream;
+  // ---- inputs: [keys | keys2 | profile doubles | perm | p_mod], one H2D
+  const int r = prof->r, c = prof->c;
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t nd = (size_t)(2 * r + 4 * c + 1);
+  const size_t o_keys2 = al((size_t)n * 8);
+  const size_t o_prof = o_keys2 + al((size_t)n * 8);
+  const size_t o_perm = o_prof + al(nd * sizeof(double));
+  const size_t o_pmod = o_perm + al((size_t)n * sizeof(int32_t));
+  const size_t in_bytes = o_pmod + al((size_t)3 * (d + 1) * sizeof(uint64_t));
+  if (g.h_stage_bytes < in_bytes) {
+    if (g.h_stage) cudaFreeHost(g.h_stage);
+    g.h_stage = nullptr;
+    g.h_stage_bytes = 0;
+    RFR_CUDA_OK(cudaMallocHost(&g.h_stage, in_bytes));
+    g.h_stage_bytes = in_bytes;
+  }
+  char* hs = (char*)g.h_stage;
+  memcpy(hs, keys, (size_t)n * 8);
+  memcpy(hs + o_keys2, keys2, (size_t)n * 8);
+  double* hp = (double*)(hs + o_prof);
+  for (int i = 0; i < r; i++) {
+    hp[i] = prof->real_hi[i];
+    hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
+  }
+  for (int j = 0; j < c; j++) {
+    hp[2 * r + j] = prof->sum_hi[j];
+    hp[2 * r + c + j] = prof->sum_lo ? prof->sum_lo[j] : 0.0;
+    hp[2 * r + 2 * c + j] = prof->prod_hi[j];
+    hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
+  }
+  hp[nd - 1] = 0.0;
+  memcpy(hs + o_perm, prof->perm, (size_t)n * sizeof(int32_t));
+  memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
+  RFR_CUDA_OK(g.vprof.ensure(in_bytes));
+  char* base = (char*)g.vprof.p;
+  RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
+  const uint64_t* d_keys = (const uint64_t*)base;
+  const uint64_t* d_keys2 = (const uint64_t*)(base + o_keys2);
+  // ---- search (grow-and-retry of the raw buffer, as run_search_host)
+  int r_bits = 0, nwin = 0;
+  unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  for (int attempt = 0; attempt < 3; attempt++) {
+    RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
+    rc = search_core(d_keys, n, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &r_bits, &nwin, true);
+    if (rc) return rc;
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    if (g.h_ctr->out_count <= raw_cap) break;
+    if (attempt == 2) return rfr_fail(RFR_E_CAP, "raw hit buffer regrow failed");
+    unsigned long long want = g.h_ctr->out_count + (g.h_ctr->out_count >> 3) + 1024;
+    if (want > (1ull << 31)) return rfr_fail(RFR_E_CAP, "%llu raw hits exceed the 2^31 limit",
+                                             (unsigned long long)g.h_ctr->out_count);
+    RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
+    raw_cap = g.raw.bytes / sizeof(uint64_t);
+  }
+  const unsigned long long raw = g.h_ctr->out_count;
+  // ---- secondary window, then verification of the survivors in place
+  RFR_CUDA_OK(g.post.ensure((raw ? raw : 1) * sizeof(uint64_t)));
+  RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2,
+                               width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
+                               g.nsm, s));
+  const size_t mb = raw ? (size_t)raw : 1;
+  const size_t q_side = al(mb), q_coef = q_side + al(mb);
+  const size_t out_dev = q_coef + mb * (size_t)stride * sizeof(int64_t);
+  RFR_CUDA_OK(g.vcoef.ensure(out_dev));
+  char* obase = (char*)g.vcoef.p;
+  g_launches += 1;
+  if (raw) {
+    VerifyArgs A;
+    A.n = n;
+    A.r = r;
+    A.c = c;
+    A.d = d;
+    const double* dp = (const double*)(base + o_prof);
+    A.real_hi = dp;
+    A.real_lo = dp + r;
+    A.sum_hi = dp + 2 * r;
+    A.sum_lo = dp + 2 * r + c;
+    A.prod_hi = dp + 2 * r + 2 * c;
+    A.prod_lo = dp + 2 * r + 3 * c;
+    A.perm = (const int32_t*)(base + o_perm);
+    A.root_err = prof->root_err;
+    A.pats = (const uint64_t*)g.post.p;
+    A.m = (long long)raw;
+    A.m_dev = &d_ctr->post_count;
+    A.p_mod = (const uint64_t*)(base + o_pmod);
+    for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
+    A.verdict = (uint8_t*)obase;
+    A.side = (uint8_t*)(obase + q_side);
+    A.coeffs = (long long*)(obase + q_coef);
+    A.stride = stride;
+    RFR_CUDA_OK(launch_verify(A, s));
+    g_launches += 1;
+  }
+  RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+  // ---- outputs: counters + min(raw, cap) candidates with their verdicts
+  const size_t mc = raw < (unsigned long long)cap ? (size_t)raw : (size_t)cap;
+  const size_t h_pats = 0, h_verd = al(mc * 8), h_side = h_verd + al(mc), h_coef = h_side + al(mc);
+  const size_t out_bytes = h_coef + mc * (size_t)stride * sizeof(int64_t);
+  if (g.h_stage_bytes < out_bytes) {  // the staged inputs were consumed by the H2D above
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+    cudaFreeHost(g.h_stage);
+    g.h_stage = nullptr;
+    g.h_stage_bytes = 0;
+    RFR_CUDA_OK(cudaMallocHost(&g.h_stage, out_bytes));
+    g.h_stage_bytes = out_bytes;
+  }
+  hs = (char*)g.h_stage;
+  RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+  if (mc) {
+    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_pats, g.post.p, mc * 8, cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_verd, obase, mc, cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_side, obase + q_side, mc, cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_coef, obase + q_coef, mc * (size_t)stride * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+  }
+  RFR_CUDA_OK(cudaStreamSynchronize(s));
+  const DevCounters cc = *g.h_ctr;
+  const size_t m = cc.post_count < (unsigned long long)mc ? (size_t)cc.post_count : mc;
+  if (m) {
+    memcpy(pats, hs + h_pats, m * 8);
+    if (verdict) memcpy(verdict, hs + h_verd, m);
+    if (side) memcpy(side, hs + h_side, m);
+    if (coeffs) {
+      const int64_t* src = (const int64_t*)(hs + h_coef);
+      memcpy(coeffs, src, m * (size_t)stride * sizeof(int64_t));
+    }
+  }
+  *nout = (int64_t)cc.post_count;
+  if (st) {
+    fill_stats(st, cc, n, r_bits, nwin);
+    st->raw_hits = (int64_t)cc.out_count;
+    st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
+    st->ms_join = ev_ms(g.ev[1], g.ev[2]);
+    st->ms_post = ev_ms(g.ev[2], g.ev[3]);
+    st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+  }
+  return RFR_OK;
+}
+
 int rfr_search_keys2(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                      uint64_t lo2, uint64_t width2, int shard, int nshards, uint64_t* out,
                      int64_t cap, int64_t* nout, rfr_stats* st) {
@@ -616,6 +758,7 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
   A.root_err = prof->root_err;
   A.pats = (const uint64_t*)(base + o_pats);
   A.m = m;
+  A.m_dev = nullptr;
   A.p_mod = (const uint64_t*)(base + o_pmod);
   for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
   A.verdict = (uint8_t*)obase;

@@ -21,7 +21,28 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            DevCounters* d_ctr, int nsm, cudaStream_t s);
 cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaStream_t s);
 
-struct VerifyArgs;
+// Batched candidate verification (rfr_verify.cu): one warp per candidate.
+struct VerifyArgs {
+  int n, r, c, d;
+  const double* real_hi;
+  const double* real_lo;
+  const double* sum_hi;
+  const double* sum_lo;
+  const double* prod_hi;
+  const double* prod_lo;
+  const int32_t* perm;
+  double root_err;
+  const uint64_t* pats;
+  long long m;                            // candidates (grid bound)
+  const unsigned long long* m_dev;        // optional device count (<= m), or null
+  const uint64_t* p_mod;  // 3 x (d+1)
+  uint64_t primes[3];
+  uint8_t* verdict;
+  uint8_t* side;
+  long long* coeffs;
+  int stride;
+};
+cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s);
 // Primes of the modular division test, P = 2^k - c with small c (fast
 // reduction in the verify kernel): 2^61 - 1, 2^62 - 57, 2^63 - 25.
 constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 4611686018427387847ull,

@@ -18,6 +18,7 @@
 
 #include "../../include/rfr.h"
 #include "rfr_common.cuh"
+#include "rfr_internal.h"
 
 namespace rfr {
 
@@ -56,25 +57,7 @@ constexpr int kVerifyWarps = 4;
 constexpr int kMaxE = 64;          // smaller side degree <= 64 (n <= 64 roots of p, d <= 128)
 constexpr int kMaxD = 128;
 
-struct VerifyArgs {
-  int n, r, c, d;
-  const double* real_hi;
-  const double* real_lo;
-  const double* sum_hi;
-  const double* sum_lo;
-  const double* prod_hi;
-  const double* prod_lo;
-  const int32_t* perm;
-  double root_err;
-  const uint64_t* pats;
-  long long m;
-  const uint64_t* p_mod;  // 3 x (d+1)
-  uint64_t primes[3];
-  uint8_t* verdict;
-  uint8_t* side;
-  long long* coeffs;
-  int stride;
-};
+
 
 struct WarpBuf {
   ddv c[2][kMaxE + 2];
@@ -126,7 +109,9 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   __syncthreads();
   WarpBuf& B = bufs[w];
   const long long k = (long long)blockIdx.x * kVerifyWarps + w;
-  if (k >= A.m) return;
+  long long mm = A.m;
+  if (A.m_dev) mm = min(mm, (long long)*A.m_dev);
+  if (k >= mm) return;
   const uint64_t full = A.n >= 64 ? ~0ull : ((1ull << A.n) - 1ull);
   const uint64_t s = A.pats[k] & full;
   int deg_s = 0;

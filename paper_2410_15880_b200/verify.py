@@ -130,6 +130,30 @@ def _p_mod(p: IntPolynomial) -> np.ndarray:
     return np.array([[c % q for c in co] for q in _PRIMES], dtype=np.uint64)
 
 
+def _rfr_profile(prof: RootProfile):
+    """The profile as an rfr_profile struct (plus the arrays it points into,
+    which the caller keeps alive for the duration of the call)."""
+    D = ctypes.POINTER(ctypes.c_double)
+    keep = []
+
+    def dptr(a):
+        a = np.ascontiguousarray(a if a is not None else np.zeros(0), dtype=np.float64)
+        keep.append(a)
+        return a.ctypes.data_as(D)
+
+    perm = np.ascontiguousarray(prof.perm, dtype=np.int32)
+    keep.append(perm)
+    rp = _lib.RfrProfile(
+        n=prof.n, r=prof.r, c=prof.c,
+        real_hi=dptr(prof.real_roots), real_lo=dptr(prof.real_lo),
+        sum_hi=dptr(prof.pair_sums), sum_lo=dptr(prof.sum_lo),
+        prod_hi=dptr(prof.pair_products), prod_lo=dptr(prof.prod_lo),
+        perm=perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        root_err=float(prof.root_err),
+    )
+    return rp, keep
+
+
 def verify_candidates(prof: RootProfile, p: IntPolynomial, pats: np.ndarray):
     """Device verification of candidate patterns (one warp each).
     Returns (verdict uint8[m], side uint8[m], coeffs int64[m, 65])."""
@@ -141,6 +165,59 @@ def verify_candidates(prof: RootProfile, p: IntPolynomial, pats: np.ndarray):
     coeffs = np.zeros((m, _STRIDE), dtype=np.int64)
     if m == 0:
         return verdict, side, coeffs
+    rp, keep = _rfr_profile(prof)
+    pats = np.ascontiguousarray(pats, dtype=np.uint64)
+    pm = np.ascontiguousarray(_p_mod(p))
+    _lib.check(
+        lib.rfr_verify(ctypes.byref(rp), _lib.ptr(pats, _lib.U64_P), m,
+                       _lib.ptr(pm, _lib.U64_P), p.degree,
+                       verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
+                       coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, None),
+        "rfr_verify",
+    )
+    return verdict, side, coeffs
+
+
+def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
+                      keys3: np.ndarray, half_width3: int, stats=None):
+    """One device call (rfr_search_verify): the key-window search, the third
+    power-sum window and the verification of every survivor, without the
+    candidates leaving the GPU in between.  Returns (pats, verdict, side,
+    coeffs) like search_keys + verify_candidates (patterns unsorted)."""
+    from .recombine import _fill_stats, _window
+
+    lib = _lib.load()
+    _lib.device()
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    keys3 = np.ascontiguousarray(keys3, dtype=np.uint64)
+    n = len(keys)
+    lo, width = _window(half_width)
+    lo2, width2 = _window(half_width3)
+    rp, keep = _rfr_profile(prof)
+    pm = np.ascontiguousarray(_p_mod(p))
+    cap = 1 << 8
+    while True:
+        pats = np.empty(cap, dtype=np.uint64)
+        verdict = np.empty(cap, dtype=np.uint8)
+        side = np.empty(cap, dtype=np.uint8)
+        coeffs = np.empty((cap, _STRIDE), dtype=np.int64)
+        nout = ctypes.c_int64(0)
+        st = _lib.RfrStats()
+        _lib.check(
+            lib.rfr_search_verify(
+                _lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
+                ctypes.byref(rp), _lib.ptr(pm, _lib.U64_P), p.degree, _lib.ptr(pats, _lib.U64_P),
+                verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
+                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap, ctypes.byref(nout),
+                ctypes.byref(st)),
+            "rfr_search_verify",
+        )
+        if nout.value <= cap:
+            break
+        cap = int(nout.value)
+    _fill_stats(stats, st)
+    m = int(nout.value)
+    return pats[:m], verdict[:m], side[:m], coeffs[:m]
     D = ctypes.POINTER(ctypes.c_double)
     keep = []  # keep numpy buffers alive for the call
 
@@ -232,19 +309,30 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     t0 = time.perf_counter()
     keys, T = _search_window(prof)
     keys3, T3 = _secondary_window(prof)
-    if workers > 1:
-        from .parallel import sharded_search_keys
-
-        pats = sharded_search_keys(keys, T, workers, stats.recombine, keys2=keys3, half_width2=T3)
+    if workers == 1 and keys3 is not None:
+        # one device call: search, Tr3 window and verification back to back
+        # (recombine_seconds then covers the device verification too)
+        pats, verdict, side, coeffs = search_and_verify(prof, p, keys, T, keys3, T3,
+                                                        stats.recombine)
+        keep = pats != 0
+        pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]
+        stats.recombine_seconds += time.perf_counter() - t0
+        stats.candidates += len(pats)
+        t0 = time.perf_counter()
     else:
-        pats = search_keys(keys, T, stats.recombine, keys2=keys3, half_width2=T3)
-    pats = pats[pats != 0]
-    stats.recombine_seconds += time.perf_counter() - t0
-    stats.candidates += len(pats)
+        if workers > 1:
+            from .parallel import sharded_search_keys
 
-    t0 = time.perf_counter()
+            pats = sharded_search_keys(keys, T, workers, stats.recombine, keys2=keys3,
+                                       half_width2=T3)
+        else:
+            pats = search_keys(keys, T, stats.recombine, keys2=keys3, half_width2=T3)
+        pats = pats[pats != 0]
+        stats.recombine_seconds += time.perf_counter() - t0
+        stats.candidates += len(pats)
+        t0 = time.perf_counter()
+        verdict, side, coeffs = verify_candidates(prof, p, pats)
     full = (1 << n) - 1
-    verdict, side, coeffs = verify_candidates(prof, p, pats)
     found: dict[int, IntPolynomial] = {}  # side pattern -> monic integer factor
     for k in range(len(pats)):
         s = int(pats[k])

@@ -136,3 +136,28 @@ def test_device_verification_agrees_with_reference_verdicts(verify_cases):
                 t = (~s & full) if side[k] else s
                 q = accepted[t]
                 assert [int(x) for x in coeffs[k, : len(q)]] == [int(x) for x in q]
+
+
+def test_fused_search_verify_matches_the_two_call_path(big_inputs, factor_cases):
+    """rfr_search_verify (one device call) == rfr_search_keys2 + rfr_verify."""
+    from paper_2410_15880_b200 import search_keys
+    from paper_2410_15880_b200 import verify as V
+
+    polys = [poly_of(c["p"]) for c in big_inputs["c3"][:2]]
+    polys += [poly_of(c["input"]) for c in factor_cases if c["tag"].startswith("c1_")][:3]
+    for p in polys:
+        prof = V._profile_cached(p.primitive_part().coeffs)
+        keys, T = V._search_window(prof)
+        keys3, T3 = V._secondary_window(prof)
+        pats, verdict, side, coeffs = V.search_and_verify(prof, p.primitive_part(), keys, T, keys3, T3)
+        ref = search_keys(keys, T, keys2=keys3, half_width2=T3)
+        order = np.argsort(pats)
+        assert np.array_equal(pats[order], ref)
+        rv, rs, rc = V.verify_candidates(prof, p.primitive_part(), ref)
+        assert np.array_equal(verdict[order], rv) and np.array_equal(side[order], rs)
+        full = (1 << prof.n) - 1
+        for k in np.nonzero(rv == _lib.V_PASS)[0]:
+            t = int(ref[k])
+            e = V.selected_degree((~t & full) if rs[k] else t, prof)
+            # only coefficients 0..e are written (the rest of the row is scratch)
+            assert np.array_equal(coeffs[order][k][: e + 1], rc[k][: e + 1])
