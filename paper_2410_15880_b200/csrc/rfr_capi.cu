@@ -52,7 +52,8 @@ struct Ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  DevVec keys, keys2, rho, raw, post, ctr, rotc, splits;
+  DevVec keys, keys2, rho, raw, post, ctr, rotc;
+  DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
@@ -165,10 +166,11 @@ int ensure_list_buffers(const JoinPlan& P) {
   for (int i = 0; i < 4; i++) {
     size_t len = (size_t)1 << P.list[i].bits;
     if (len < 4096) len = 4096;
-    for (int w = 0; w < 2; w++) {
-      RFR_CUDA_OK(g.lk[i][w].ensure(len * sizeof(uint64_t)));
-      RFR_CUDA_OK(g.lp[i][w].ensure(len * sizeof(uint32_t)));
-    }
+    for (int w = 0; w < 2; w++) RFR_CUDA_OK(g.lk[i][w].ensure(len * sizeof(uint64_t)));
+    // patterns live only at the base level (longer lists keep a merge history)
+    RFR_CUDA_OK(g.lp[i][0].ensure(((size_t)1 << kBaseBits) * sizeof(uint32_t)));
+    const size_t hb = list_hist_bytes(P.list[i].bits);
+    RFR_CUDA_OK(g.hist[i].ensure(hb ? hb : 16));
   }
   return RFR_OK;
 }
@@ -216,9 +218,10 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   if (rc) return rc;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
   RFR_CUDA_OK(g.rotc.ensure(4 * kRotSlots * sizeof(uint32_t)));
-  RFR_CUDA_OK(g.splits.ensure(lists_split_words(P0) * sizeof(uint32_t)));
-  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p,
-                           (uint32_t*)g.splits.p, s));
+  char* hb[4];
+  for (int i = 0; i < 4; i++) hb[i] = (char*)g.hist[i].p;
+  const ListHist H = list_hist_layout(P0, hb);
+  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p, H, s));
   {
     int maxbits = 0;
     for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
@@ -242,6 +245,10 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
     g_launches += 1;
   }
+  // the join emits quarter-list indices; rewrite every hit as its pattern
+  RFR_CUDA_OK(launch_index_to_pattern(P0, bufs(0), H, (const uint32_t*)g.rotc.p, d_out,
+                                      &((DevCounters*)g.ctr.p)->out_count, cap, g.nsm, s));
+  g_launches += 1;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
   return RFR_OK;
 }
@@ -318,7 +325,7 @@ int rfr_shutdown(void) {
   g.post.release();
   g.keys2.release();
   g.rotc.release();
-  g.splits.release();
+  for (auto& h : g.hist) h.release();
   g.vprof.release();
   g.vpats.release();
   g.vpmod.release();
@@ -558,7 +565,12 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2,
                                width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
                                g.nsm, s));
-  const size_t mb = raw ? (size_t)raw : 1;
+  // verification rows: the survivors are a subset of the raw hits and the
+  // caller regrows when they exceed its cap, so min(raw, max(cap, 4096))
+  // rows suffice (sizing by the raw count cost 12 GB on Swinnerton-Dyer f6)
+  const unsigned long long vcap_ull =
+      raw < (unsigned long long)(cap > 4096 ? cap : 4096) ? raw : (unsigned long long)(cap > 4096 ? cap : 4096);
+  const size_t mb = vcap_ull ? (size_t)vcap_ull : 1;
   const size_t q_side = al(mb), q_coef = q_side + al(mb);
   const size_t out_dev = q_coef + mb * (size_t)stride * sizeof(int64_t);
   RFR_CUDA_OK(g.vcoef.ensure(out_dev));
@@ -580,7 +592,7 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
     A.perm = (const int32_t*)(base + o_perm);
     A.root_err = prof->root_err;
     A.pats = (const uint64_t*)g.post.p;
-    A.m = (long long)raw;
+    A.m = (long long)vcap_ull;
     A.m_dev = &d_ctr->post_count;
     A.p_mod = (const uint64_t*)(base + o_pmod);
     for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];

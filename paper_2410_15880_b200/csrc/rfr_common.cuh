@@ -61,6 +61,30 @@ struct ListBufs {
   uint32_t* p[4];
 };
 
+// Merge history of the lists (levels kBaseBits .. bits-1): instead of a
+// pattern per entry, every doubling level L_k -> L_k+1 keeps one provenance
+// bit per output (0: from L_k, 1: from rotate(L_k + v_k)), a 16-bit rank
+// directory per 64 outputs (1-bits in the 2048-output tile before that word)
+// and the tile splits (# L_k entries before each tile).  A list entry's
+// pattern is recovered by walking the levels down (emit time only), so the
+// levels move 8-byte keys instead of 12-byte key + pattern pairs.
+constexpr int kHistTileLog = 11;  // 2048 outputs per merge tile
+struct ListHist {
+  uint8_t* bm[4];
+  uint16_t* dir[4];
+  uint32_t* sp[4];
+};
+__host__ __device__ inline size_t hist_bm_off(int k) {  // bytes before level k
+  return (((size_t)1 << (k + 1)) - ((size_t)1 << (kBaseBits + 1))) / 8;
+}
+__host__ __device__ inline size_t hist_dir_off(int k) {  // directory entries before level k
+  return (((size_t)1 << (k + 1)) - ((size_t)1 << (kBaseBits + 1))) / 64;
+}
+__host__ __device__ inline size_t hist_sp_off(int k) {  // split words before level k
+  return (((size_t)1 << (k + 1 - kHistTileLog)) - ((size_t)1 << (kBaseBits + 1 - kHistTileLog))) +
+         (size_t)(k - kBaseBits);
+}
+
 // Device-side counters (one slot each, accumulated with atomics).
 struct DevCounters {
   unsigned long long out_count;      // emitted pairs (may exceed capacity)

@@ -6,11 +6,16 @@
 
 namespace rfr {
 size_t join_smem_bytes();
-size_t lists_split_words(const JoinPlan& P);
+size_t list_hist_bytes(int bits);
+ListHist list_hist_layout(const JoinPlan& P, char* const base[4]);
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
-                         uint32_t* d_rot, uint32_t* d_split, cudaStream_t s);
+                         uint32_t* d_rot, ListHist H, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s);
+cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
+                                    const uint32_t* d_rot, uint64_t* d_out,
+                                    const unsigned long long* d_count, unsigned long long cap, int nsm,
+                                    cudaStream_t s);
 cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_in,
                              const unsigned long long* d_in_count, unsigned long long cap_in,
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,

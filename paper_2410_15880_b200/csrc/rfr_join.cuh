@@ -126,20 +126,20 @@ __device__ __forceinline__ uint32_t home_of(uint64_t rel, int shift, int lg) {
   return (uint32_t)(rel >> shift) & ((1u << lg) - 1u);
 }
 
-// Emit the full pattern of a matching (A record r, B record) pair.
-__device__ __noinline__ void emit_match(const JoinArgs& a, uint32_t r,
-                                        uint32_t ib, uint32_t jb) {
+// Emit a matching (A record r, B record) pair as its four quarter-list
+// INDICES packed at the patterns' bit offsets (they sum to n - 1 <= 63 bits);
+// index_to_pattern_kernel turns them into patterns after the join, so the
+// emit site stays small (its register footprint is paid at every call site).
+__device__ __noinline__ void emit_match(const JoinArgs& a, uint32_t r, uint32_t ib, uint32_t jb) {
   JoinSmem& S = join_smem();
   const JoinPlan& P = a.P;
   const uint32_t id = S.recI[r];
   const int aib = P.list[1].bits;
   const uint32_t ia = id >> aib, ja = id & ((1u << aib) - 1u);
-  const uint64_t pa = (uint64_t)__ldg(a.pat[0] + ia) |
-                      ((uint64_t)__ldg(a.pat[1] + ja) << P.list[1].pat_shift);
-  const uint64_t pb = ((uint64_t)__ldg(a.pat[2] + ib) << P.list[2].pat_shift) |
-                      ((uint64_t)__ldg(a.pat[3] + jb) << P.list[3].pat_shift);
+  const uint64_t v = (uint64_t)ia | ((uint64_t)ja << P.list[1].pat_shift) |
+                     ((uint64_t)ib << P.list[2].pat_shift) | ((uint64_t)jb << P.list[3].pat_shift);
   const unsigned long long k = atomicAdd(&a.ctr->out_count, 1ull);
-  if (k < a.cap) a.out[k] = pa | pb;
+  if (k < a.cap) a.out[k] = v;
 }
 
 // Running counters of one warp threaded through the passes by value (by

@@ -207,11 +207,12 @@ __device__ __forceinline__ uint32_t rot_of(const uint32_t* rc, int k, uint32_t n
 // Merge-path splits of one doubling level, one warp per tile boundary
 // (32-ary search: ~5 dependent steps for 2^23-entry lists); all boundaries of
 // all lists are searched concurrently so the merge CTAs start at their loads.
-// split[li * stride + t] = # A elements before output tile t.
+// H.sp[li][hist_sp_off(k) + t] = # A elements before output tile t (kept:
+// it is also the rank directory of the level's provenance bits).
 __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __restrict__ keys,
                                                           JoinPlan P, int k, ListBufs in,
                                                           const uint32_t* __restrict__ rot,
-                                                          uint32_t* __restrict__ split, int stride) {
+                                                          ListHist H) {
   const int lane = threadIdx.x & 31;
   const uint32_t w = blockIdx.x * 8u + (threadIdx.x >> 5);
   const int li = blockIdx.y;
@@ -244,17 +245,15 @@ __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __rest
     if (c > 0) lo = qc1 + 1;
     if (c < 32) hi = qc;
   }
-  if (lane == 0) split[li * stride + w] = lo;
+  if (lane == 0) pick4(H.sp, li)[hist_sp_off(k) + w] = lo;
 }
 
 __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64_t* __restrict__ keys,
                                                                     JoinPlan P, int k,
                                                                     ListBufs in, ListBufs out,
-                                                                    uint32_t* rot,
-                                                                    const uint32_t* __restrict__ split,
-                                                                    int stride) {
+                                                                    uint32_t* rot, ListHist H) {
   __shared__ uint64_t sK[kMergeTile];
-  __shared__ uint32_t sP[kMergeTile];
+  __shared__ uint32_t wsum[kMergeThreads / 32];
   const int li = blockIdx.y;
   const ListSpec L = pick_list(P, li);
   if (L.bits <= k) return;
@@ -262,29 +261,20 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t d0 = blockIdx.x * (uint32_t)kMergeTile;
   if (d0 >= 2u * n) return;
   const uint64_t* __restrict__ A = pick4(in.k, li);
-  const uint32_t* __restrict__ Ap = pick4(in.p, li);
   uint64_t* __restrict__ O = pick4(out.k, li);
-  uint32_t* __restrict__ Op = pick4(out.p, li);
   uint32_t* rc = rot + li * kRotSlots;
   const uint64_t v = elem_key(keys, L, k);
-  const uint32_t bit = 1u << k;
   const uint32_t r0 = rot_of(rc, k, n);
   const uint32_t mask = n - 1;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t a0 = __ldg(split + li * stride + blockIdx.x);
-  const uint32_t a1 = __ldg(split + li * stride + blockIdx.x + 1);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t* sp = pick4(H.sp, li) + hist_sp_off(k);
+  const uint32_t a0 = __ldg(sp + blockIdx.x);
+  const uint32_t a1 = __ldg(sp + blockIdx.x + 1);
   const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
   const uint32_t na = a1 - a0, nb = tile - na;
   const uint32_t b0 = d0 - a0;
-  for (uint32_t t = tid; t < na; t += kMergeThreads) {
-    sK[kswz(t)] = __ldg(A + a0 + t);
-    sP[pswz(t)] = __ldg(Ap + a0 + t);
-  }
-  for (uint32_t t = tid; t < nb; t += kMergeThreads) {
-    const uint32_t jj = (r0 + b0 + t) & mask;
-    sK[kswz(na + t)] = __ldg(A + jj) + v;
-    sP[pswz(na + t)] = __ldg(Ap + jj) | bit;
-  }
+  for (uint32_t t = tid; t < na; t += kMergeThreads) sK[kswz(t)] = __ldg(A + a0 + t);
+  for (uint32_t t = tid; t < nb; t += kMergeThreads) sK[kswz(na + t)] = __ldg(A + ((r0 + b0 + t) & mask)) + v;
   __syncthreads();
   // per-thread merge of kMergeItems outputs from the staged tile
   const uint32_t dt = min((uint32_t)(tid * kMergeItems), tile);
@@ -296,7 +286,7 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   }
   uint32_t i = lo, j = dt - lo;
   uint64_t ok[kMergeItems];
-  uint32_t op[kMergeItems];
+  uint32_t from_b = 0;  // provenance bits of this thread's outputs
   // both run heads held in registers: one shared key load per output
   const uint64_t kInf = ~0ull;
   uint64_t ka = i < na ? sK[kswz(i)] : kInf, kb = j < nb ? sK[kswz(na + j)] : kInf;
@@ -305,34 +295,45 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
     const bool takeA = j >= nb || (i < na && ka <= kb);
     if (takeA) {
       ok[t] = ka;
-      op[t] = sP[pswz(i)];
       i++;
       ka = i < na ? sK[kswz(i)] : kInf;
     } else {
       ok[t] = kb;
-      op[t] = sP[pswz(na + j)];
+      from_b |= 1u << t;
       j++;
       kb = j < nb ? sK[kswz(na + j)] : kInf;
     }
   }
   // each thread's run of outputs is contiguous and 64-byte aligned: store it
-  // directly with 16-byte vector stores (no staging round trip)
+  // directly with 16-byte vector stores
   const uint32_t cnt = dt < tile ? min((uint32_t)kMergeItems, tile - dt) : 0u;
+  if (cnt < (uint32_t)kMergeItems) from_b &= (1u << cnt) - 1u;
   if (cnt == (uint32_t)kMergeItems) {
     ulonglong2* ko = reinterpret_cast<ulonglong2*>(O + d0 + dt);
 #pragma unroll
     for (int t = 0; t < kMergeItems / 2; t++) ko[t] = make_ulonglong2(ok[2 * t], ok[2 * t + 1]);
-    uint4* po = reinterpret_cast<uint4*>(Op + d0 + dt);
-#pragma unroll
-    for (int t = 0; t < kMergeItems / 4; t++)
-      po[t] = make_uint4(op[4 * t], op[4 * t + 1], op[4 * t + 2], op[4 * t + 3]);
   } else {
 #pragma unroll
     for (int t = 0; t < kMergeItems; t++)
-      if ((uint32_t)t < cnt) {
-        O[d0 + dt + t] = ok[t];
-        Op[d0 + dt + t] = op[t];
-      }
+      if ((uint32_t)t < cnt) O[d0 + dt + t] = ok[t];
+  }
+  // provenance byte and the rank directory (1-bits in the tile before each
+  // 64-output word): block exclusive scan of the per-thread popcounts
+  static_assert(kMergeItems == 8 && kMergeTile == (1 << kHistTileLog), "history layout");
+  const uint32_t c1 = __popc(from_b);
+  uint32_t incl = c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  uint32_t woff = 0;
+  for (int w2 = 0; w2 < wid; w2++) woff += wsum[w2];
+  if (cnt) {
+    pick4(H.bm, li)[hist_bm_off(k) + ((d0 + dt) >> 3)] = (uint8_t)from_b;
+    if ((tid & 7) == 0) pick4(H.dir, li)[hist_dir_off(k) + ((d0 + dt) >> 6)] = (uint16_t)(woff + incl - c1);
   }
   // next level's rotation start: # outputs < -v_{k+1}
   if (L.bits > k + 1) {
@@ -349,7 +350,6 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
 struct JoinArgs {
   JoinPlan P;
   const uint64_t* key[4];
-  const uint32_t* pat[4];
   uint64_t* out;
   unsigned long long cap;
   DevCounters* ctr;
@@ -357,6 +357,81 @@ struct JoinArgs {
 };
 
 #include "rfr_join.cuh"
+
+// ------------------------------------------------- indices -> patterns
+// The join emits each hit as its four quarter-list indices (packed at the
+// patterns' bit offsets); this pass rewrites every hit as its pattern.
+struct PatArgs {
+  JoinPlan P;
+  const uint32_t* pat[4];  // base-level patterns (lists of <= 2^kBaseBits entries: all of them)
+  ListHist hist;           // merge history of the longer lists
+  const uint32_t* rot;     // per-list rotation counters of the merge levels
+};
+
+static_assert(kMaxOuterBits <= kBaseBits, "outer lists are base-level lists (patterns stored)");
+// Local pattern of entry d of quarter list li: lists of at most 2^kBaseBits
+// entries store it; longer lists walk their merge history down (one tile
+// split, one rank-directory entry and one 64-bit provenance word per level).
+__device__ __forceinline__ uint32_t list_pattern(const PatArgs& a, int li, uint32_t d) {
+  const int bits = pick_list(a.P, li).bits;
+  const uint32_t* base = pick4(a.pat, li);
+  if (bits <= kBaseBits) return __ldg(base + d);
+  const uint8_t* bm = pick4(a.hist.bm, li);
+  const uint16_t* dir = pick4(a.hist.dir, li);
+  const uint32_t* sp = pick4(a.hist.sp, li);
+  const uint32_t* rc = a.rot + li * kRotSlots;
+  uint32_t pat = 0;
+  for (int k = bits - 1; k >= kBaseBits; k--) {
+    const uint32_t n = 1u << k;
+    const uint32_t t = d >> kHistTileLog, d0 = t << kHistTileLog;
+    const uint32_t a0 = __ldg(sp + hist_sp_off(k) + t);
+    const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(bm + hist_bm_off(k)) + (d >> 6));
+    const uint32_t pre = __ldg(dir + hist_dir_off(k) + (d >> 6));
+    const uint32_t c1 = pre + __popcll(w & ((1ull << (d & 63)) - 1ull));  // 1-bits in [d0, d)
+    if (!((w >> (d & 63)) & 1ull)) {
+      d = a0 + (d - d0 - c1);  // from L_k
+    } else {                   // from rotate(L_k + v_k)
+      const uint32_t c = __ldg(rc + k);
+      const uint32_t r0 = c >= n ? 0u : c;
+      d = (r0 + (d0 - a0) + c1) & (n - 1);
+      pat |= 1u << k;
+    }
+  }
+  return pat | __ldg(base + d);
+}
+
+__global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, uint64_t* out,
+                                                               const unsigned long long* count,
+                                                               unsigned long long cap) {
+  unsigned long long m = *count;
+  if (m > cap) m = cap;
+  const JoinPlan& P = a.P;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t v = out[i];
+    uint64_t pat = 0;
+#pragma unroll
+    for (int li = 0; li < 4; li++) {
+      const ListSpec L = pick_list(P, li);
+      const uint32_t idx = (uint32_t)((v >> L.pat_shift) & ((1ull << L.bits) - 1ull));
+      pat |= (uint64_t)list_pattern(a, li, idx) << L.pat_shift;
+    }
+    out[i] = pat;
+  }
+}
+
+cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
+                                    const uint32_t* d_rot, uint64_t* d_out,
+                                    const unsigned long long* d_count, unsigned long long cap, int nsm,
+                                    cudaStream_t s) {
+  PatArgs a;
+  a.P = P;
+  for (int i = 0; i < 4; i++) a.pat[i] = base.p[i];
+  a.hist = hist;
+  a.rot = d_rot;
+  index_to_pattern_kernel<<<nsm * 4, 256, 0, s>>>(a, d_out, d_count, cap);
+  return cudaGetLastError();
+}
 
 // ------------------------------------------------------------- recheck
 // Parity mode: keep a hit t iff accept(value(t), eps), value() accumulated in
@@ -435,15 +510,28 @@ namespace rfr {
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
 
-// d_split: 4 * split_stride(P) words of scratch.
-size_t lists_split_words(const JoinPlan& P) {
-  int maxbits = 0;
-  for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
-  return 4 * ((((2ull << maxbits) + kMergeTile - 1) / kMergeTile) + 1);
+// Bytes of one list's merge history (bitmaps, rank directory, splits).
+size_t list_hist_bytes(int bits) {
+  if (bits <= kBaseBits) return 0;
+  const size_t bm = hist_bm_off(bits), dir = hist_dir_off(bits) * 2, sp = hist_sp_off(bits) * 4;
+  return ((bm + 15) & ~(size_t)15) + ((dir + 15) & ~(size_t)15) + sp + 16;
+}
+ListHist list_hist_layout(const JoinPlan& P, char* const base[4]) {
+  ListHist H;
+  for (int i = 0; i < 4; i++) {
+    const int bits = P.list[i].bits;
+    char* b = base[i];
+    const size_t bm = bits > kBaseBits ? hist_bm_off(bits) : 0;
+    const size_t dir = bits > kBaseBits ? hist_dir_off(bits) * 2 : 0;
+    H.bm[i] = (uint8_t*)b;
+    H.dir[i] = (uint16_t*)(b + ((bm + 15) & ~(size_t)15));
+    H.sp[i] = (uint32_t*)(b + ((bm + 15) & ~(size_t)15) + ((dir + 15) & ~(size_t)15));
+  }
+  return H;
 }
 
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
-                         uint32_t* d_rot, uint32_t* d_split, cudaStream_t s) {
+                         uint32_t* d_rot, ListHist H, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(lists_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -458,11 +546,10 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
     const int parity = (k - kBaseBits) & 1;
     const uint64_t outputs = 2ull << k;
     const unsigned int blocks = (unsigned int)((outputs + kMergeTile - 1) / kMergeTile);
-    const int stride = (int)(((2ull << maxbits) + kMergeTile - 1) / kMergeTile) + 1;
     lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
-                                                                 d_rot, d_split, stride);
+                                                                 d_rot, H);
     lists_merge_kernel<<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
-        d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, d_split, stride);
+        d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
   }
   return cudaGetLastError();
 }
@@ -478,10 +565,7 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
   }
   JoinArgs a;
   a.P = P;
-  for (int i = 0; i < 4; i++) {
-    a.key[i] = fin.k[i];
-    a.pat[i] = fin.p[i];
-  }
+  for (int i = 0; i < 4; i++) a.key[i] = fin.k[i];
   a.out = d_out;
   a.cap = cap;
   a.ctr = d_ctr;

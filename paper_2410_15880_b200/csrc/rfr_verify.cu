@@ -108,10 +108,13 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   }
   __syncthreads();
   WarpBuf& B = bufs[w];
-  const long long k = (long long)blockIdx.x * kVerifyWarps + w;
   long long mm = A.m;
   if (A.m_dev) mm = min(mm, (long long)*A.m_dev);
-  if (k >= mm) return;
+  // grid-stride over the candidates (one warp each): the fused search+verify
+  // sizes the grid by SMs, the count being known on the device only
+  for (long long k = (long long)blockIdx.x * kVerifyWarps + w; k < mm;
+       k += (long long)gridDim.x * kVerifyWarps) {
+  __syncwarp();  // the warp's buffer is reused candidate after candidate
   const uint64_t full = A.n >= 64 ? ~0ull : ((1ull << A.n) - 1ull);
   const uint64_t s = A.pats[k] & full;
   int deg_s = 0;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   if (lane == 0) A.side[k] = use_comp ? 1 : 0;
   if (e < 1 || e >= A.d || e > kMaxE) {
     if (lane == 0) A.verdict[k] = (e > kMaxE) ? RFR_V_HOST : RFR_V_REJECT;
-    return;
+    continue;
   }
 
   // ---- expand prod (x - u) * prod (x^2 - t x + m) over the selected entities
@@ -204,16 +207,16 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   host = __any_sync(0xffffffffu, host);
   if (reject) {
     if (lane == 0) A.verdict[k] = RFR_V_REJECT;
-    return;
+    continue;
   }
   if (host) {
     if (lane == 0) A.verdict[k] = RFR_V_HOST;
-    return;
+    continue;
   }
   __syncwarp();
   if (B.q[e] != 1) {
     if (lane == 0) A.verdict[k] = RFR_V_REJECT;
-    return;
+    continue;
   }
 
   // ---- trial division of p by q modulo three primes, the three divisions
@@ -266,12 +269,20 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
   if (divides)
     for (int j = lane; j <= e && j < A.stride; j += 32) A.coeffs[k * A.stride + j] = B.q[j];
+  __syncwarp();
+  }
 }
 
 cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s) {
   if (A.m <= 0) return cudaSuccess;
-  const unsigned blocks = (unsigned)((A.m + kVerifyWarps - 1) / kVerifyWarps);
-  verify_kernel<<<blocks, kVerifyWarps * 32, 0, s>>>(A);
+  long long blocks = (A.m + kVerifyWarps - 1) / kVerifyWarps;
+  if (A.m_dev) {  // count on the device: enough warps to cover a typical set, grid-stride beyond
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks > 8LL * nsm) blocks = 8LL * nsm;
+  }
+  verify_kernel<<<(unsigned)blocks, kVerifyWarps * 32, 0, s>>>(A);
   return cudaGetLastError();
 }
 

@@ -195,7 +195,7 @@ def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, hal
     lo2, width2 = _window(half_width3)
     rp, keep = _rfr_profile(prof)
     pm = np.ascontiguousarray(_p_mod(p))
-    cap = 1 << 8
+    cap = 1 << 12  # a regrow reruns the whole search: start where the survivors fit
     while True:
         pats = np.empty(cap, dtype=np.uint64)
         verdict = np.empty(cap, dtype=np.uint8)
