@@ -406,17 +406,23 @@ __global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, 
   unsigned long long m = *count;
   if (m > cap) m = cap;
   const JoinPlan& P = a.P;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint64_t v = out[i];
-    uint64_t pat = 0;
-#pragma unroll
-    for (int li = 0; li < 4; li++) {
-      const ListSpec L = pick_list(P, li);
+  // four lanes per hit, one per quarter list: the two long history walks
+  // (the inner lists) run side by side instead of back to back
+  const int li = threadIdx.x & 3;
+  const ListSpec L = pick_list(P, li);
+  const unsigned long long lanes = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long wbase = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  for (unsigned long long tb = wbase; tb < 4 * m; tb += lanes) {  // warp-uniform trip count
+    const unsigned long long i = (tb + (threadIdx.x & 31u)) >> 2;
+    uint64_t part = 0;
+    if (i < m) {
+      const uint64_t v = out[i];
       const uint32_t idx = (uint32_t)((v >> L.pat_shift) & ((1ull << L.bits) - 1ull));
-      pat |= (uint64_t)list_pattern(a, li, idx) << L.pat_shift;
+      part = (uint64_t)list_pattern(a, li, idx) << L.pat_shift;
     }
-    out[i] = pat;
+    part |= __shfl_xor_sync(0xffffffffu, part, 1);
+    part |= __shfl_xor_sync(0xffffffffu, part, 2);
+    if (li == 0 && i < m) out[i] = part;
   }
 }
 
