@@ -536,7 +536,9 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // outer whose last chunk is still full is flagged for continue_pass
 // (off = 32 * nch).  Same record semantics as window_pass.
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
-template <bool SIDE_A>
+// SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
+// so "in bucket" and "in halo" are 32-bit tests on the high / low words.
+template <bool SIDE_A, bool SMALLH>
 __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t lo, uint32_t hi,
                                       int nch, PassSt st) {
   JoinSmem& S = join_smem();
@@ -578,8 +580,16 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
         const uint64_t sv = x + kv[k];
         const uint64_t rel = sv - cW;
         const bool valid = q < Mi;
-        const bool m = valid && o < Mi && rel < K.W;
-        const bool e = m || (valid && (rel - K.W) < K.H);
+        bool m, e;
+        if (SMALLH) {
+          const uint32_t rh = (uint32_t)(rel >> 32), rl = (uint32_t)rel;
+          const uint32_t wh = (uint32_t)(K.W >> 32);
+          m = valid && o < Mi && rh < wh;
+          e = m || (valid && rh == wh && rl < (uint32_t)K.H);
+        } else {
+          m = valid && o < Mi && rel < K.W;
+          e = m || (valid && (rel - K.W) < K.H);
+        }
         em = __ballot_sync(FULL, e);
         mc += __popc(__ballot_sync(FULL, m));
         n_stat += e ? 1u : 0u;
@@ -837,7 +847,7 @@ __device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_
     }
     const bool done = S.cur_i >= MoA;
     PassSt sb{0u, n_q, n_qprobe, false, false};
-    sb = gsB > 32 ? run_pass<false>(a, cW, bLo, bHi, gsB >> 5, sb)
+    sb = gsB > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<false, true>(a, cW, bLo, bHi, gsB >> 5, sb) : run_pass<false, false>(a, cW, bLo, bHi, gsB >> 5, sb))
                   : window_pass<false>(a, cW, bLo, bHi, gsB, sb);
     __syncwarp();
     sb = continue_pass<false>(a, cW, bLo, bHi, gsB, sb);
@@ -919,7 +929,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     {
       const int t = tid_now(), w = t >> 5;
       PassSt sa{0u, join_smem().cnt[0][t], join_smem().cnt[2][t], false, false};
-      sa = gsA > 32 ? run_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa)
+      sa = gsA > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<true, true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa) : run_pass<true, false>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa))
                     : window_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
       if (sa.cont) {
         __syncwarp();
@@ -944,7 +954,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       {
         const int t = tid_now(), w = t >> 5;
         PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
-        sb = gsB > 32 ? run_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb)
+        sb = gsB > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
                       : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
