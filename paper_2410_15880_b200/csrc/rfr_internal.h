@@ -5,7 +5,6 @@
 #include "rfr_common.cuh"
 
 namespace rfr {
-size_t join_smem_bytes();
 size_t list_hist_bytes(int bits);
 ListHist list_hist_layout(const JoinPlan& P, char* const base[4]);
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,

@@ -514,7 +514,19 @@ __global__ void rho_keys_kernel(const double* __restrict__ rho, int n, uint64_t*
 // ------------------------------------------------------ host-side launchers
 namespace rfr {
 
-size_t join_smem_bytes() { return sizeof(JoinSmem); }
+// cudaFuncSetAttribute is per device context: remember, per device, which
+// kernels have had their dynamic shared-memory limit raised.
+template <typename K>
+static cudaError_t raise_smem_limit(K kernel, size_t bytes, uint64_t& done_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? 1ull << dev : 0;
+  if (bit && (done_mask & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done_mask |= bit;
+  return e;
+}
 
 // Bytes of one list's merge history (bitmaps, rank directory, splits).
 size_t list_hist_bytes(int bits) {
@@ -538,13 +550,9 @@ ListHist list_hist_layout(const JoinPlan& P, char* const base[4]) {
 
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
                          uint32_t* d_rot, ListHist H, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(lists_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(BaseSmem));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static uint64_t attr_done = 0;
+  cudaError_t e = raise_smem_limit(lists_base_kernel, sizeof(BaseSmem), attr_done);
+  if (e != cudaSuccess) return e;
   lists_base_kernel<<<4, 1024, sizeof(BaseSmem), s>>>(d_keys, P, buf0, d_rot);
   int maxbits = 0;
   for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
@@ -562,13 +570,9 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
 
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(join_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(JoinSmem));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static uint64_t attr_done = 0;
+  cudaError_t e = raise_smem_limit(join_kernel, sizeof(JoinSmem), attr_done);
+  if (e != cudaSuccess) return e;
   JoinArgs a;
   a.P = P;
   for (int i = 0; i < 4; i++) a.key[i] = fin.k[i];
