@@ -194,8 +194,10 @@ int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double
 
 /*
  * Square-free screen for the exact normalisation (R/polynomial.py:221-247):
- * 1 when gcd(p mod q, p' mod q) = 1 for a 61-bit prime q not dividing the
- * leading coefficient (then p is square-free over Z), 0 when undecided.
+ * 1 when gcd(p mod q, p' mod q) = 1 for a prime q dividing neither the
+ * leading coefficient nor d (then p is square-free over Z), 0 when
+ * undecided (q may divide the discriminant: try another prime).  Primes
+ * below 2^25 take a double-precision path; larger ones 128-bit products.
  * coeffs_mod: p's coefficients reduced mod q (d+1), lead_mod != 0.
  */
 int rfr_squarefree_mod(const uint64_t* coeffs_mod, int d, uint64_t q);

@@ -271,6 +271,21 @@ void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin
   st->launches = g_launches;
 }
 
+// Shape and pointer checks shared by rfr_verify and rfr_search_verify.
+int check_profile(const rfr_profile* prof, int d) {
+  if (!prof) return rfr_fail(RFR_E_ARG, "null profile");
+  if (prof->n < 0 || prof->r < 0 || prof->c < 0) return rfr_fail(RFR_E_ARG, "negative profile sizes");
+  if (prof->n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits");
+  if (prof->r + 2 * prof->c != d || prof->r + prof->c != prof->n)
+    return rfr_fail(RFR_E_ARG, "profile does not match the degree");
+  if ((prof->r && !prof->real_hi) || (prof->c && (!prof->sum_hi || !prof->prod_hi)) ||
+      (prof->n && !prof->perm))
+    return rfr_fail(RFR_E_ARG, "null profile array");
+  if (!(prof->root_err >= 0.0))  // +inf is allowed: every candidate comes back undecided
+    return rfr_fail(RFR_E_ARG, "root_err must be >= 0 (got NaN or a negative bound)");
+  return RFR_OK;
+}
+
 int check_n(int n) {
   if (n < 0) return rfr_fail(RFR_E_ARG, "negative width");
   if (n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits, got %d", n);
@@ -287,19 +302,33 @@ const char* rfr_last_error(void) { return g_err.c_str(); }
 
 int rfr_num_sms(void) { return g.nsm; }
 
-int rfr_init(int device) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (g.ready && g.device == device) return RFR_OK;
-  if (g.ready) return rfr_fail(RFR_E_ARG, "already initialised on device %d", g.device);
-  int ndev = 0;
-  RFR_CUDA_OK(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return rfr_fail(RFR_E_ARG, "no CUDA device %d", device);
+// Free everything the context holds (safe on a partially initialised one).
+static void release_ctx() {
+  if (g.stream) cudaStreamSynchronize(g.stream);
+  DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc,
+                    &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef};
+  for (DevVec* v : vecs) v->release();
+  for (auto& h : g.hist) h.release();
+  for (auto& a : g.lk)
+    for (auto& v : a) v.release();
+  for (auto& a : g.lp)
+    for (auto& v : a) v.release();
+  for (auto& e : g.ev)
+    if (e) cudaEventDestroy(e);
+  if (g.h_ctr) cudaFreeHost(g.h_ctr);
+  if (g.h_stage) cudaFreeHost(g.h_stage);
+  if (g.stream) cudaStreamDestroy(g.stream);
+  g = Ctx();
+}
+
+static int init_ctx(int device) {
   RFR_CUDA_OK(cudaSetDevice(device));
   cudaDeviceProp prop;
   RFR_CUDA_OK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10)
     return rfr_fail(RFR_E_CUDA, "librfr is built for sm_100a; device %d is sm_%d%d", device,
                     prop.major, prop.minor);
+  g.device = device;
   g.nsm = prop.multiProcessorCount;
   RFR_CUDA_OK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   for (auto& e : g.ev) RFR_CUDA_OK(cudaEventCreate(&e));
@@ -309,7 +338,23 @@ int rfr_init(int device) {
   RFR_CUDA_OK(g.rho.ensure(64 * sizeof(double)));
   RFR_CUDA_OK(g.raw.ensure((1u << 20) * sizeof(uint64_t)));
   RFR_CUDA_OK(g.post.ensure((1u << 20) * sizeof(uint64_t)));
-  g.device = device;
+  return RFR_OK;
+}
+
+int rfr_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.ready && g.device == device) return RFR_OK;
+  if (g.ready) return rfr_fail(RFR_E_ARG, "already initialised on device %d", g.device);
+  int ndev = 0;
+  RFR_CUDA_OK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return rfr_fail(RFR_E_ARG, "no CUDA device %d", device);
+  const int rc = init_ctx(device);
+  if (rc) {
+    const std::string why = g_err;  // release_ctx must not mask the first error
+    release_ctx();
+    g_err = why;
+    return rc;
+  }
   g.ready = true;
   return RFR_OK;
 }
@@ -318,30 +363,7 @@ int rfr_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g.ready) return RFR_OK;
   cudaSetDevice(g.device);
-  cudaStreamSynchronize(g.stream);
-  g.keys.release();
-  g.rho.release();
-  g.raw.release();
-  g.post.release();
-  g.keys2.release();
-  g.rotc.release();
-  for (auto& h : g.hist) h.release();
-  g.vprof.release();
-  g.vpats.release();
-  g.vpmod.release();
-  g.vverd.release();
-  g.vside.release();
-  g.vcoef.release();
-  g.ctr.release();
-  for (auto& a : g.lk)
-    for (auto& v : a) v.release();
-  for (auto& a : g.lp)
-    for (auto& v : a) v.release();
-  for (auto& e : g.ev) cudaEventDestroy(e);
-  cudaFreeHost(g.h_ctr);
-  if (g.h_stage) cudaFreeHost(g.h_stage);
-  cudaStreamDestroy(g.stream);
-  g = Ctx();
+  release_ctx();
   return RFR_OK;
 }
 
@@ -491,10 +513,10 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   int rc = ensure_ready();
   if (rc) return rc;
   if ((rc = check_n(n))) return rc;
-  if (!nout || cap < 0 || stride < 1 || !prof || !p_mod || d < 1 || d > 128)
+  if (!nout || cap < 0 || stride < 1 || !p_mod || d < 1 || d > 128 || (cap > 0 && !pats))
     return rfr_fail(RFR_E_ARG, "bad search_verify arguments");
-  if (prof->n != n || prof->r + 2 * prof->c != d || prof->r + prof->c != prof->n)
-    return rfr_fail(RFR_E_ARG, "profile does not match the keys / degree");
+  if ((rc = check_profile(prof, d))) return rc;
+  if (prof->n != n) return rfr_fail(RFR_E_ARG, "profile does not match the keys");
   if (n == 0) {
     *nout = 0;
     fill_stats(st, DevCounters{}, 0, 0, 0);
@@ -541,42 +563,47 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
   const uint64_t* d_keys = (const uint64_t*)base;
   const uint64_t* d_keys2 = (const uint64_t*)(base + o_keys2);
-  // ---- search (grow-and-retry of the raw buffer, as run_search_host)
+  // ---- search, secondary window and verification back to back with no host
+  // round trip: every kernel clamps to the counts the previous one left on
+  // the device, and the first rows come back with the counters (one
+  // synchronisation for a typical call).  A raw-hit overflow regrows and
+  // reruns; more survivors than the speculative rows cost a second copy.
+  constexpr size_t kSpecRows = 64;
   int r_bits = 0, nwin = 0;
-  unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
   DevCounters* d_ctr = (DevCounters*)g.ctr.p;
-  for (int attempt = 0; attempt < 3; attempt++) {
+  // verification rows: the caller regrows beyond its cap, so max(cap, 4096)
+  // rows bound every useful call (sizing by the raw count cost 12 GB on
+  // Swinnerton-Dyer f6)
+  const size_t vrows = (size_t)(cap > 4096 ? cap : 4096);
+  const size_t q_side = al(vrows), q_coef = q_side + al(vrows);
+  RFR_CUDA_OK(g.vcoef.ensure(q_coef + vrows * (size_t)stride * sizeof(int64_t)));
+  char* obase = (char*)g.vcoef.p;
+  const size_t spec = (size_t)cap < kSpecRows ? (size_t)cap : kSpecRows;
+  const size_t h_verd = al(vrows * 8), h_side = h_verd + al(vrows), h_coef = h_side + al(vrows);
+  auto copy_rows = [&](size_t from, size_t to) -> cudaError_t {  // device rows [from, to) -> staging
+    if (to <= from) return cudaSuccess;
+    const size_t k = to - from;
+    cudaError_t e = cudaMemcpyAsync(hs + from * 8, (const char*)g.post.p + from * 8, k * 8,
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hs + h_verd + from, obase + from, k, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hs + h_side + from, obase + q_side + from, k, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hs + h_coef + from * stride * 8, obase + q_coef + from * stride * 8,
+                          k * (size_t)stride * 8, cudaMemcpyDeviceToHost, s);
+    return e;
+  };
+  for (int attempt = 0;; attempt++) {
+    const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
+    RFR_CUDA_OK(g.post.ensure(raw_cap * sizeof(uint64_t)));
     RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
     rc = search_core(d_keys, n, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &r_bits, &nwin, true);
     if (rc) return rc;
-    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
-    RFR_CUDA_OK(cudaStreamSynchronize(s));
-    if (g.h_ctr->out_count <= raw_cap) break;
-    if (attempt == 2) return rfr_fail(RFR_E_CAP, "raw hit buffer regrow failed");
-    unsigned long long want = g.h_ctr->out_count + (g.h_ctr->out_count >> 3) + 1024;
-    if (want > (1ull << 31)) return rfr_fail(RFR_E_CAP, "%llu raw hits exceed the 2^31 limit",
-                                             (unsigned long long)g.h_ctr->out_count);
-    RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
-    raw_cap = g.raw.bytes / sizeof(uint64_t);
-  }
-  const unsigned long long raw = g.h_ctr->out_count;
-  // ---- secondary window, then verification of the survivors in place
-  RFR_CUDA_OK(g.post.ensure((raw ? raw : 1) * sizeof(uint64_t)));
-  RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2,
-                               width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
-                               g.nsm, s));
-  // verification rows: the survivors are a subset of the raw hits and the
-  // caller regrows when they exceed its cap, so min(raw, max(cap, 4096))
-  // rows suffice (sizing by the raw count cost 12 GB on Swinnerton-Dyer f6)
-  const unsigned long long vcap_ull =
-      raw < (unsigned long long)(cap > 4096 ? cap : 4096) ? raw : (unsigned long long)(cap > 4096 ? cap : 4096);
-  const size_t mb = vcap_ull ? (size_t)vcap_ull : 1;
-  const size_t q_side = al(mb), q_coef = q_side + al(mb);
-  const size_t out_dev = q_coef + mb * (size_t)stride * sizeof(int64_t);
-  RFR_CUDA_OK(g.vcoef.ensure(out_dev));
-  char* obase = (char*)g.vcoef.p;
-  g_launches += 1;
-  if (raw) {
+    RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2,
+                                 width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
+                                 g.nsm, s));
+    g_launches += 1;
     VerifyArgs A;
     A.n = n;
     A.r = r;
@@ -592,7 +619,7 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
     A.perm = (const int32_t*)(base + o_perm);
     A.root_err = prof->root_err;
     A.pats = (const uint64_t*)g.post.p;
-    A.m = (long long)vcap_ull;
+    A.m = (long long)vrows;
     A.m_dev = &d_ctr->post_count;
     A.p_mod = (const uint64_t*)(base + o_pmod);
     for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
@@ -602,40 +629,41 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
     A.stride = stride;
     RFR_CUDA_OK(launch_verify(A, s));
     g_launches += 1;
-  }
-  RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
-  // ---- outputs: counters + min(raw, cap) candidates with their verdicts
-  const size_t mc = raw < (unsigned long long)cap ? (size_t)raw : (size_t)cap;
-  const size_t h_pats = 0, h_verd = al(mc * 8), h_side = h_verd + al(mc), h_coef = h_side + al(mc);
-  const size_t out_bytes = h_coef + mc * (size_t)stride * sizeof(int64_t);
-  if (g.h_stage_bytes < out_bytes) {  // the staged inputs were consumed by the H2D above
+    RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
+    // outputs: counters plus the first rows (the staged inputs were consumed
+    // by the H2D above, so the staging block takes the results)
+    const size_t out_bytes = h_coef + vrows * (size_t)stride * 8;
+    if (g.h_stage_bytes < out_bytes) {
+      RFR_CUDA_OK(cudaStreamSynchronize(s));
+      cudaFreeHost(g.h_stage);
+      g.h_stage = nullptr;
+      g.h_stage_bytes = 0;
+      RFR_CUDA_OK(cudaMallocHost(&g.h_stage, out_bytes));
+      g.h_stage_bytes = out_bytes;
+    }
+    hs = (char*)g.h_stage;
+    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    RFR_CUDA_OK(copy_rows(0, spec));
     RFR_CUDA_OK(cudaStreamSynchronize(s));
-    cudaFreeHost(g.h_stage);
-    g.h_stage = nullptr;
-    g.h_stage_bytes = 0;
-    RFR_CUDA_OK(cudaMallocHost(&g.h_stage, out_bytes));
-    g.h_stage_bytes = out_bytes;
+    if (g.h_ctr->out_count <= raw_cap) break;
+    if (attempt == 2) return rfr_fail(RFR_E_CAP, "raw hit buffer regrow failed");
+    const unsigned long long want = g.h_ctr->out_count + (g.h_ctr->out_count >> 3) + 1024;
+    if (want > (1ull << 31))
+      return rfr_fail(RFR_E_CAP, "%llu raw hits exceed the 2^31 limit",
+                      (unsigned long long)g.h_ctr->out_count);
+    RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
   }
-  hs = (char*)g.h_stage;
-  RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
-  if (mc) {
-    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_pats, g.post.p, mc * 8, cudaMemcpyDeviceToHost, s));
-    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_verd, obase, mc, cudaMemcpyDeviceToHost, s));
-    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_side, obase + q_side, mc, cudaMemcpyDeviceToHost, s));
-    RFR_CUDA_OK(cudaMemcpyAsync(hs + h_coef, obase + q_coef, mc * (size_t)stride * sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, s));
-  }
-  RFR_CUDA_OK(cudaStreamSynchronize(s));
   const DevCounters cc = *g.h_ctr;
-  const size_t m = cc.post_count < (unsigned long long)mc ? (size_t)cc.post_count : mc;
+  const size_t m = cc.post_count < (unsigned long long)cap ? (size_t)cc.post_count : (size_t)cap;
+  if (m > spec) {  // more survivors than the speculative rows
+    RFR_CUDA_OK(copy_rows(spec, m));
+    RFR_CUDA_OK(cudaStreamSynchronize(s));
+  }
   if (m) {
-    memcpy(pats, hs + h_pats, m * 8);
+    memcpy(pats, hs, m * 8);
     if (verdict) memcpy(verdict, hs + h_verd, m);
     if (side) memcpy(side, hs + h_side, m);
-    if (coeffs) {
-      const int64_t* src = (const int64_t*)(hs + h_coef);
-      memcpy(coeffs, src, m * (size_t)stride * sizeof(int64_t));
-    }
+    if (coeffs) memcpy(coeffs, hs + h_coef, m * (size_t)stride * sizeof(int64_t));
   }
   *nout = (int64_t)cc.post_count;
   if (st) {
@@ -706,11 +734,11 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
   std::lock_guard<std::mutex> lk(g_mu);
   int rc = ensure_ready();
   if (rc) return rc;
-  if (!prof || m < 0 || d < 1 || d > 128 || stride < 1) return rfr_fail(RFR_E_ARG, "bad verify arguments");
-  if (prof->n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits");
-  if (prof->r + 2 * prof->c != d || prof->r + prof->c != prof->n)
-    return rfr_fail(RFR_E_ARG, "profile does not match the degree");
+  if (m < 0 || d < 1 || d > 128 || stride < 1) return rfr_fail(RFR_E_ARG, "bad verify arguments");
+  if ((rc = check_profile(prof, d))) return rc;
   if (m == 0) return RFR_OK;
+  if (!pats || !p_mod || !verdict || !side || !coeffs)
+    return rfr_fail(RFR_E_ARG, "null verify buffer");
   cudaSetDevice(g.device);
   cudaStream_t s = g.stream;
   // one pinned staging block each way: [profile doubles | perm | pats | p_mod]

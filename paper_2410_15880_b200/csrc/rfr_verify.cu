@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   __shared__ WarpBuf bufs[kVerifyWarps];
   __shared__ ProfSmem PS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long mm = A.m;
+  if (A.m_dev) mm = min(mm, (long long)*A.m_dev);
+  // grid sized by a row bound, count on the device: idle CTAs leave before
+  // staging the profile (uniform per CTA, ahead of the barrier)
+  if ((long long)blockIdx.x * kVerifyWarps >= mm) return;
   for (int i = threadIdx.x; i < A.n; i += blockDim.x) PS.perm[i] = (int8_t)A.perm[i];
   for (int i = threadIdx.x; i < A.r; i += blockDim.x) {
     PS.v_hi[i] = A.real_hi[i];
@@ -108,8 +113,6 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A)
   }
   __syncthreads();
   WarpBuf& B = bufs[w];
-  long long mm = A.m;
-  if (A.m_dev) mm = min(mm, (long long)*A.m_dev);
   // grid-stride over the candidates (one warp each): the fused search+verify
   // sizes the grid by SMs, the count being known on the device only
   for (long long k = (long long)blockIdx.x * kVerifyWarps + w; k < mm;

@@ -37,6 +37,7 @@ import numpy as np
 from . import _lib
 from .polynomial import (
     IntPolynomial,
+    _poly,
     divide_exact,
     monic_transform,
     monic_untransform_factor,
@@ -100,7 +101,9 @@ def _profile_cached(coeffs: tuple) -> RootProfile:
 
 def _search_window(prof: RootProfile) -> tuple[np.ndarray, int]:
     """Combined keys (first + second power sum) and the window half-width."""
-    keys = ((prof.keys1.astype(object) + prof.keys2.astype(object)) % (1 << 64)).astype(np.uint64)
+    k1 = np.asarray(prof.keys1, dtype=np.uint64)
+    k2 = np.asarray(prof.keys2, dtype=np.uint64)
+    keys = k1 + k2  # uint64 addition wraps: the sum mod 2^64
     T = KEY_SAFETY * (prof.key_err1 + prof.key_err2) + prof.n + 64
     return keys, T
 
@@ -114,19 +117,21 @@ def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
 
 
 _PRIMES: tuple[int, ...] | None = None
+_PRIMES_I64: np.ndarray | None = None
 
 
 def _p_mod(p: IntPolynomial) -> np.ndarray:
     """p's coefficients modulo the three verification primes (3 x (d+1))."""
-    global _PRIMES
+    global _PRIMES, _PRIMES_I64
     if _PRIMES is None:
         primes = np.zeros(3, dtype=np.uint64)
         _lib.load().rfr_verify_primes(primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
         _PRIMES = tuple(int(q) for q in primes)
+        _PRIMES_I64 = primes.astype(np.int64)
     co = p.coeffs
     if max(co) < (1 << 62) and min(co) > -(1 << 62):  # int64 fast path (Python sign rule)
         a = np.array(co, dtype=np.int64)
-        return np.stack([np.remainder(a, np.int64(q)) for q in _PRIMES]).astype(np.uint64)
+        return np.remainder(a[None, :], _PRIMES_I64[:, None]).astype(np.uint64)
     return np.array([[c % q for c in co] for q in _PRIMES], dtype=np.uint64)
 
 
@@ -340,7 +345,7 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
         if v == _lib.V_PASS:
             t = (~s & full) if side[k] else s
             e = selected_degree(t, prof)
-            found[t] = IntPolynomial([int(x) for x in coeffs[k, : e + 1]])
+            found[t] = _poly(coeffs[k, : e + 1].tolist())
         elif v == _lib.V_HOST:
             stats.host_verified += 1
             for t in (s, ~s & full):

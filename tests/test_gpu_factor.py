@@ -138,6 +138,31 @@ def test_device_verification_agrees_with_reference_verdicts(verify_cases):
                 assert [int(x) for x in coeffs[k, : len(q)]] == [int(x) for x in q]
 
 
+def test_device_verification_root_error_bound_edges(verify_cases):
+    """rfr_verify argument checks: a NaN root error bound is rejected
+    (RFR_E_ARG -> ValueError); an infinite one decides nothing on the device
+    (no PASS: every non-trivial candidate goes to the host)."""
+    vc = verify_cases[0]
+
+    def prof_with(err):
+        return RootProfile(
+            real_roots=np.array(rho_of({"rho": vc["real_roots"]})),
+            pair_sums=np.array(rho_of({"rho": vc["pair_sums"]})),
+            pair_products=np.array(rho_of({"rho": vc["pair_products"]})),
+            rho=np.array(rho_of(vc)), perm=tuple(vc["perm"]),
+            real_lo=np.zeros(len(vc["real_roots"])), sum_lo=np.zeros(len(vc["pair_sums"])),
+            prod_lo=np.zeros(len(vc["pair_products"])), root_err=err,
+        )
+
+    p = poly_of(vc["p"])
+    pats = np.array([row["pattern"] for row in vc["candidates"]], dtype=np.uint64)
+    with pytest.raises(ValueError, match="root_err"):
+        verify_candidates(prof_with(float("nan")), p, pats)
+    verdict, _, _ = verify_candidates(prof_with(float("inf")), p, pats)
+    assert not np.any(verdict == _lib.V_PASS)
+    assert np.any(verdict == _lib.V_HOST)
+
+
 def test_fused_search_verify_matches_the_two_call_path(big_inputs, factor_cases):
     """rfr_search_verify (one device call) == rfr_search_keys2 + rfr_verify."""
     from paper_2410_15880_b200 import search_keys

@@ -155,9 +155,36 @@ def test_kronecker_multiply_and_divide_match_schoolbook():
     assert hits > 100
 
 
-def test_squarefree_screen_never_accepts_a_square():
-    """The native modular screen (rfr_squarefree_mod, pseudo-division Euclid)
-    answers 'square-free' only for square-free inputs (checked with sympy)."""
+def test_divide_exact_base_2_64_carries():
+    """divide_exact tries the 64-bit Kronecker base first: a quotient whose
+    coefficients overflow 64 bits is still found (Mignotte base), and a
+    dividend that equals q * r at x = 2^64 only through a carry (p_k + 2^64,
+    p_{k+1} - 1) is rejected."""
+    from paper_2410_15880_b200.polynomial import divide_exact, multiply
+
+    rng = random.Random(3)
+    for _ in range(60):
+        dq, dr = rng.randint(8, 30), rng.randint(8, 30)
+        q = [rng.randint(-99, 99) for _ in range(dq)] + [1]
+        r = [rng.randint(-99, 99) for _ in range(dr)] + [1]
+        r[rng.randrange(dr)] = rng.choice([1, -1]) * ((1 << 70) + rng.randint(0, 1 << 40))
+        pc = list(multiply(P(q), P(r)).coeffs)
+        got = divide_exact(P(pc), P(q))
+        assert got is not None and list(got.coeffs) == r
+        r_small = [rng.randint(-99, 99) for _ in range(dr)] + [1]
+        pc = list(multiply(P(q), P(r_small)).coeffs)
+        k = rng.randrange(len(pc) - 1)
+        pc[k] += 1 << 64
+        pc[k + 1] -= 1
+        assert divide_exact(P(pc), P(q)) is None
+        assert _school_div(pc, q) is None
+
+
+@pytest.mark.parametrize("q", [33554393, 2305843009213693951])
+def test_squarefree_screen_never_accepts_a_square(q):
+    """The native modular screen (rfr_squarefree_mod, pseudo-division Euclid;
+    double-precision path below 2^25, 128-bit products above) answers
+    'square-free' only for square-free inputs (checked with sympy)."""
     import ctypes
 
     import numpy as np
@@ -168,7 +195,6 @@ def test_squarefree_screen_never_accepts_a_square():
     lib = _lib.load()
     x = sympy.symbols("x")
     rng = random.Random(5)
-    q = 2305843009213693951
     accepted = 0
     for _ in range(120):
         d = rng.randint(2, 30)
