@@ -42,6 +42,9 @@
 
 // Clock64 phase trace of CTA 0 (RFR_TRACE=1 at run time, needs a build with
 // `make TRACE=1`); compiled out of the production kernel.
+#ifndef RFR_JOIN_CHECK  // 1: trap when a run chunk breaks the prefix invariant
+#define RFR_JOIN_CHECK 0
+#endif
 #ifndef RFR_JOIN_TRACE
 #define RFR_JOIN_TRACE 0
 #endif
@@ -538,6 +541,14 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
 // SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
 // so "in bucket" and "in halo" are 32-bit tests on the high / low words.
+// 32-bit bucket/halo classification in the run pass (SMALLH): the halo fits
+// 32 bits and both inner lists are long enough that every chunk lane is a
+// record (q < 32 kMaxCh <= Mi).
+__device__ __forceinline__ bool use_smallh(const JoinPlan& P) {
+  return P.half < (1ull << 32) && P.r <= 32 && (32u * kMaxCh >> P.list[1].bits) == 0u &&
+         (32u * kMaxCh >> P.list[3].bits) == 0u;
+}
+
 template <bool SIDE_A, bool SMALLH>
 __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t lo, uint32_t hi,
                                       int nch, PassSt st) {
@@ -570,28 +581,35 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
       kv[k] = (k < nch && q < Mi) ? ld_stream(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
     }
     if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
-    uint32_t mc = 0, nq = 0, em = 0;
+    // along a run the offset rel = x + key - cW grows with q (one pass over the
+    // rotated list), so the in-bucket records (m) and the records kept (e:
+    // bucket + halo) are both prefixes of the run: a kept record's rank in
+    // its chunk is its lane, and the main count is a per-lane tally reduced
+    // once per outer.  A record at o >= Mi wraps to the head of the list and
+    // has rel >= 2^64 - cW >= W, so it can be halo but never main.
+    const uint32_t lim = Mi - pos;  // o < Mi  <=>  q < lim  (pos <= Mi)
+    uint32_t mcl = 0, nq = 0, em = 0;
 #pragma unroll
     for (int k = 0; k < kMaxCh; k++) {
       if (k < nch) {
         const uint32_t q = (uint32_t)(k * 32 + lane);
-        const uint32_t o = pos + q;
-        const uint32_t j = (rot + o) & (Mi - 1);
+        const uint32_t j = (rot + pos + q) & (Mi - 1);
         const uint64_t sv = x + kv[k];
         const uint64_t rel = sv - cW;
-        const bool valid = q < Mi;
         bool m, e;
-        if (SMALLH) {
+        if (SMALLH) {  // dispatched only when Mi >= 32 kMaxCh: every q is a record
           const uint32_t rh = (uint32_t)(rel >> 32), rl = (uint32_t)rel;
           const uint32_t wh = (uint32_t)(K.W >> 32);
-          m = valid && o < Mi && rh < wh;
-          e = m || (valid && rh == wh && rl < (uint32_t)K.H);
+          m = q < lim && rh < wh;
+          e = m || (rh == wh && rl < (uint32_t)K.H);
         } else {
-          m = valid && o < Mi && rel < K.W;
+          const bool valid = q < Mi;
+          m = q < lim && rel < K.W;
           e = m || (valid && (rel - K.W) < K.H);
         }
         em = __ballot_sync(FULL, e);
-        mc += __popc(__ballot_sync(FULL, m));
+        if (RFR_JOIN_CHECK && (em & (em + 1u)) != 0u) __trap();
+        mcl += m ? 1u : 0u;
         n_stat += e ? 1u : 0u;
         if (em == 0) {
           // chunk entirely past the run (warp-uniform): nothing to store or probe
@@ -599,7 +617,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
           const uint32_t ne = __popc(em);
           if (wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
           if (!overflow && e) {
-            const uint32_t r = wid * kPart + wfill + __popc(em & lt_mask);
+            const uint32_t r = wid * kPart + wfill + lane;  // em is a prefix
             S.recK[r] = sv;
             S.recI[r] = (i << aib) | j;
             const uint32_t h1 = home_of(rel, K.sh - kL1Log, kL1Log);
@@ -625,6 +643,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
       }
     }
     if (!SIDE_A && nq) n_qprobe += process_staged(a, cW, nq);
+    const uint32_t mc = __reduce_add_sync(FULL, mcl);
     const bool sat = em == FULL && can_cont;  // warp-uniform
     if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | (sat ? kFlagCont : 0u);
     cont |= sat;
@@ -847,7 +866,7 @@ __device__ __noinline__ void slow_bucket(const JoinArgs& a, uint64_t cW, uint32_
     }
     const bool done = S.cur_i >= MoA;
     PassSt sb{0u, n_q, n_qprobe, false, false};
-    sb = gsB > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<false, true>(a, cW, bLo, bHi, gsB >> 5, sb) : run_pass<false, false>(a, cW, bLo, bHi, gsB >> 5, sb))
+    sb = gsB > 32 ? (use_smallh(a.P) ? run_pass<false, true>(a, cW, bLo, bHi, gsB >> 5, sb) : run_pass<false, false>(a, cW, bLo, bHi, gsB >> 5, sb))
                   : window_pass<false>(a, cW, bLo, bHi, gsB, sb);
     __syncwarp();
     sb = continue_pass<false>(a, cW, bLo, bHi, gsB, sb);
@@ -874,6 +893,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   const uint64_t* __restrict__ kA = a.key[1];
   const uint64_t* __restrict__ kB = a.key[3];
   const int sh = 64 - P.r;  // bucket = key >> sh
+  const bool smallh = use_smallh(P);
 
   const uint64_t nbk = P.bucket_end - P.bucket_begin;
   const uint64_t c_begin = P.bucket_begin + nbk * blockIdx.x / gridDim.x;
@@ -929,7 +949,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     {
       const int t = tid_now(), w = t >> 5;
       PassSt sa{0u, join_smem().cnt[0][t], join_smem().cnt[2][t], false, false};
-      sa = gsA > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<true, true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa) : run_pass<true, false>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa))
+      sa = gsA > 32 ? (smallh ? run_pass<true, true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa) : run_pass<true, false>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa))
                     : window_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
       if (sa.cont) {
         __syncwarp();
@@ -954,7 +974,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       {
         const int t = tid_now(), w = t >> 5;
         PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
-        sb = gsB > 32 ? (a.P.half < (1ull << 32) && a.P.r <= 32 ? run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
+        sb = gsB > 32 ? (smallh ? run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
                       : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
