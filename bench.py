@@ -57,7 +57,9 @@ def peaks():
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region: NVML
-    every 10 ms (a query takes ~1 ms), nvidia-smi every 200 ms as fallback."""
+    every 2 ms, nvidia-smi every 200 ms as fallback.  Entering the context
+    waits for the sampler's first reading, so NVML start-up does not eat the
+    (short) timed region."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -68,6 +70,7 @@ class ClockSampler:
         self.device = device
         self.samples = []  # (sm_mhz, max_mhz, set of active reason names)
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.source = None
 
@@ -92,7 +95,8 @@ class ClockSampler:
                 self.samples.append((sm, mx, {k for k, v in bits.items() if r & v}))
             except Exception:
                 pass
-            self._stop.wait(0.01)
+            self._ready.set()
+            self._stop.wait(0.002)
         return True
 
     def _run(self):
@@ -114,10 +118,12 @@ class ClockSampler:
                     self.samples.append((sm, mx, rs))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t.start()
+        self._ready.wait(timeout=10)
         return self
 
     def __exit__(self, *a):
