@@ -271,6 +271,48 @@ void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin
   st->launches = g_launches;
 }
 
+// The profile's doubles packed for one H2D copy: [real_hi | real_lo | sum_hi |
+// sum_lo | prod_hi | prod_lo | 0], 2r + 4c + 1 entries (absent lo parts are 0).
+void stage_profile(double* hp, const rfr_profile* prof) {
+  const int r = prof->r, c = prof->c;
+  for (int i = 0; i < r; i++) {
+    hp[i] = prof->real_hi[i];
+    hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
+  }
+  for (int j = 0; j < c; j++) {
+    hp[2 * r + j] = prof->sum_hi[j];
+    hp[2 * r + c + j] = prof->sum_lo ? prof->sum_lo[j] : 0.0;
+    hp[2 * r + 2 * c + j] = prof->prod_hi[j];
+    hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
+  }
+  hp[2 * r + 4 * c] = 0.0;
+}
+
+// Verification arguments over a staged profile on the device (the doubles at
+// d_prof, the permutation at d_perm, p mod the verify primes at d_pmod); the
+// caller fills the candidate and output fields.
+VerifyArgs bind_profile(const rfr_profile* prof, int d, const char* d_prof, const char* d_perm,
+                        const char* d_pmod) {
+  const int r = prof->r, c = prof->c;
+  VerifyArgs A;
+  A.n = prof->n;
+  A.r = r;
+  A.c = c;
+  A.d = d;
+  const double* dp = (const double*)d_prof;
+  A.real_hi = dp;
+  A.real_lo = dp + r;
+  A.sum_hi = dp + 2 * r;
+  A.sum_lo = dp + 2 * r + c;
+  A.prod_hi = dp + 2 * r + 2 * c;
+  A.prod_lo = dp + 2 * r + 3 * c;
+  A.perm = (const int32_t*)d_perm;
+  A.root_err = prof->root_err;
+  A.p_mod = (const uint64_t*)d_pmod;
+  for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
+  return A;
+}
+
 // Shape and pointer checks shared by rfr_verify and rfr_search_verify.
 int check_profile(const rfr_profile* prof, int d) {
   if (!prof) return rfr_fail(RFR_E_ARG, "null profile");
@@ -544,18 +586,7 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   char* hs = (char*)g.h_stage;
   memcpy(hs, keys, (size_t)n * 8);
   memcpy(hs + o_keys2, keys2, (size_t)n * 8);
-  double* hp = (double*)(hs + o_prof);
-  for (int i = 0; i < r; i++) {
-    hp[i] = prof->real_hi[i];
-    hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
-  }
-  for (int j = 0; j < c; j++) {
-    hp[2 * r + j] = prof->sum_hi[j];
-    hp[2 * r + c + j] = prof->sum_lo ? prof->sum_lo[j] : 0.0;
-    hp[2 * r + 2 * c + j] = prof->prod_hi[j];
-    hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
-  }
-  hp[nd - 1] = 0.0;
+  stage_profile((double*)(hs + o_prof), prof);
   memcpy(hs + o_perm, prof->perm, (size_t)n * sizeof(int32_t));
   memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
   RFR_CUDA_OK(g.vprof.ensure(in_bytes));
@@ -604,25 +635,10 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
                                  width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
                                  g.nsm, s));
     g_launches += 1;
-    VerifyArgs A;
-    A.n = n;
-    A.r = r;
-    A.c = c;
-    A.d = d;
-    const double* dp = (const double*)(base + o_prof);
-    A.real_hi = dp;
-    A.real_lo = dp + r;
-    A.sum_hi = dp + 2 * r;
-    A.sum_lo = dp + 2 * r + c;
-    A.prod_hi = dp + 2 * r + 2 * c;
-    A.prod_lo = dp + 2 * r + 3 * c;
-    A.perm = (const int32_t*)(base + o_perm);
-    A.root_err = prof->root_err;
+    VerifyArgs A = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
     A.pats = (const uint64_t*)g.post.p;
     A.m = (long long)vrows;
     A.m_dev = &d_ctr->post_count;
-    A.p_mod = (const uint64_t*)(base + o_pmod);
-    for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
     A.verdict = (uint8_t*)obase;
     A.side = (uint8_t*)(obase + q_side);
     A.coeffs = (long long*)(obase + q_coef);
@@ -762,18 +778,7 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
     g.h_stage_bytes = stage;
   }
   char* hs = (char*)g.h_stage;
-  double* hp = (double*)hs;
-  for (int i = 0; i < r; i++) {
-    hp[i] = prof->real_hi[i];
-    hp[r + i] = prof->real_lo ? prof->real_lo[i] : 0.0;
-  }
-  for (int j = 0; j < c; j++) {
-    hp[2 * r + j] = prof->sum_hi[j];
-    hp[2 * r + c + j] = prof->sum_lo ? prof->sum_lo[j] : 0.0;
-    hp[2 * r + 2 * c + j] = prof->prod_hi[j];
-    hp[2 * r + 3 * c + j] = prof->prod_lo ? prof->prod_lo[j] : 0.0;
-  }
-  hp[nd - 1] = 0.0;
+  stage_profile((double*)hs, prof);
   memcpy(hs + o_perm, prof->perm, (size_t)n * sizeof(int32_t));
   memcpy(hs + o_pats, pats, (size_t)m * sizeof(uint64_t));
   memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
@@ -782,25 +787,10 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
   char* base = (char*)g.vprof.p;
   char* obase = (char*)g.vcoef.p;
   RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
-  VerifyArgs A;
-  A.n = n;
-  A.r = r;
-  A.c = c;
-  A.d = d;
-  const double* dp = (const double*)base;
-  A.real_hi = dp;
-  A.real_lo = dp + r;
-  A.sum_hi = dp + 2 * r;
-  A.sum_lo = dp + 2 * r + c;
-  A.prod_hi = dp + 2 * r + 2 * c;
-  A.prod_lo = dp + 2 * r + 3 * c;
-  A.perm = (const int32_t*)(base + o_perm);
-  A.root_err = prof->root_err;
+  VerifyArgs A = bind_profile(prof, d, base, base + o_perm, base + o_pmod);
   A.pats = (const uint64_t*)(base + o_pats);
   A.m = m;
   A.m_dev = nullptr;
-  A.p_mod = (const uint64_t*)(base + o_pmod);
-  for (int i = 0; i < 3; i++) A.primes[i] = kVerifyPrimes[i];
   A.verdict = (uint8_t*)obase;
   A.side = (uint8_t*)(obase + q_side);
   A.coeffs = (long long*)(obase + q_coef);
