@@ -36,6 +36,33 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name)
 
 
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of rfr_stats and rfr_profile have the header's size
+    and field offsets (a C program compiled against include/rfr.h prints
+    them), so no argument is misread across the boundary."""
+    structs = {"rfr_stats": _lib.RfrStats, "rfr_profile": _lib.RfrProfile}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rfr.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.dirname(HEADER), "-o", str(exe), str(src)],
+                   check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n"):
+        if line:
+            cname, field, val = line.split()
+            got[(cname, field)] = int(val)
+    for cname, cls in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
+
+
 def test_library_is_built_for_sm_100a():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
