@@ -266,7 +266,11 @@ def run_ours(args):
     value = total / args.steps
 
     # ---- e2e through the public API (host buffers; roots cached => excluded)
+    for w in range(max(3, args.warmup)):  # untimed: first-call staging, kernel loading
+        factor(prep[w % len(prep)][1], workers=max(1, world))
+    torch.cuda.synchronize()
     e2e_times = []
+    early_exits = 0
     h2d = d2h = 0
     for s in range(args.steps):
         seed, p, want, prof, keys, T, _ = prep[s % len(prep)]
@@ -280,6 +284,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_times.append((time.perf_counter() - t0 - res.stats.root_seconds) * 1e3)
         assert sorted(list(g.coeffs) for g, _ in res.factors) == sorted(want) and res.certificate
+        early_exits += res.stats.early_exits
         m = res.stats.candidates
         h2d += 8 * prof.n + 8 * (2 * prof.r + 4 * prof.c) + 4 * prof.n + 8 * m + 24 * (p.degree + 1)
         d2h += 8 + 8 * m + 2 * m + 8 * 65 * m
@@ -354,6 +359,8 @@ def run_ours(args):
             "workload": "C3 d=100 random reducible (two degree-50 factors, coeffs in [-100,100]), seeds 0-4 in rotation",
             "n": sorted(set(ns)),
             "key_window": "exact 64-bit first+second power-sum keys, +-T from root error bounds",
+            "value_scope": "device-resident keys, whole pattern space searched (no early "
+                           "termination: the cost of an irreducible input) + verification",
             "l2": "256 MB buffer written between timed steps (flush); the inner quarter lists (2^23-2^24 entries, 12 B each, per half) exceed L2 and are streamed from HBM",
             "parallelism": f"key-range shards x{world}" if world > 1 else "1 GPU",
         },
@@ -371,7 +378,11 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": alg,
         },
         "e2e": {"value": round(e2e, 4), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
-                "d2h_bytes_per_step": d2h // args.steps},
+                "d2h_bytes_per_step": d2h // args.steps,
+                "path": "factor(): fused search + verification with early termination (the join "
+                        "stops once a hit verifies; each piece is then factored over its own "
+                        "roots), warm-up calls untimed",
+                "early_exits": early_exits},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "c4": {"workload": "C4 d=120 irreducible seed 0 (n=63), search only",

@@ -62,6 +62,8 @@ typedef struct rfr_stats {
   double ms_post;         /* device time: recheck / verification                    */
   double ms_total;        /* device time of the whole call                          */
   int64_t launches;       /* kernels launched by the call                            */
+  int64_t buckets_planned; /* buckets the call set out to search; buckets < this     */
+                           /* means the search stopped early (rfr_search_verify)      */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */
@@ -170,11 +172,18 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
  * in between.  Writes min(count, cap) patterns with their verdict / side /
  * coefficients (layouts as rfr_verify; coeffs valid for PASS); *nout = true
  * count (regrow and call again when it exceeds cap).  prof->n must equal n.
+ * early_exit != 0: early termination -- the hits are verified while the
+ * join runs (a one-warp kernel on a second stream) and once one passes the
+ * join stops at its next bucket boundary.  The output then holds the
+ * candidates found so far; st->buckets < st->buckets_planned tells the
+ * caller the search stopped early (the pattern space was not exhausted, so
+ * the passing factors need not be irreducible).  early_exit == 0: the whole
+ * pattern space, as rfr_search_keys2 + rfr_verify.
  */
 int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
-                      int stride, int64_t cap, int64_t* nout, rfr_stats* st);
+                      int stride, int64_t cap, int early_exit, int64_t* nout, rfr_stats* st);
 
 /* The three primes of the modular division test (p_mod residues). */
 int rfr_verify_primes(uint64_t* primes3);

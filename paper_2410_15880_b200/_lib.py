@@ -59,6 +59,7 @@ class RfrStats(ctypes.Structure):
         ("ms_post", ctypes.c_double),
         ("ms_total", ctypes.c_double),
         ("launches", ctypes.c_int64),
+        ("buckets_planned", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -141,7 +142,7 @@ def load():
         L.rfr_search_verify.argtypes = [
             U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
             ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
-            I64_P, ctypes.c_int, ctypes.c_int64, I64_P, ctypes.POINTER(RfrStats),
+            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, I64_P, ctypes.POINTER(RfrStats),
         ]
         L.rfr_verify_primes.argtypes = [U64_P]
         L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -51,8 +52,10 @@ struct Ctx {
   int device = -1;
   int nsm = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // early-exit poller, beside the join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  DevVec keys, keys2, rho, raw, post, ctr, rotc;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevVec keys, keys2, rho, raw, post, ctr, rotc, jstarts;
   DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
@@ -200,14 +203,29 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return (double)ms;
 }
 
-// Core search on device-resident keys.  d_out/cap: raw output; d_count: out
-// counter lives in g.ctr (DevCounters.out_count).  Leaves counters on device.
-int g_launches = 0;  // kernels launched by the last search_core call
+// Early termination for rfr_search_verify: the hits are verified while the
+// join runs (early_exit_poller_kernel on stream2) and the join stops at a
+// bucket boundary once one passes.
+struct EarlyExit {
+  const uint64_t* d_keys2;
+  uint64_t lo2, width2;
+  uint64_t* d_post;
+  unsigned long long post_cap;
+  VerifyArgs V;
+};
+
+// Core search on device-resident keys.  d_out/cap: raw output; counters in
+// g.ctr.  ee (one key window only): early termination as above; the hits the
+// poller did not reach are left from DevCounters.raw_done on (patterns
+// recovered here, filter and verification by the caller).
+int g_launches = 0;                // kernels launched by the last search_core call
+int64_t g_buckets_planned = 0;     // buckets the last search_core call set out to search
 
 int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard, int nshards,
                 uint64_t* d_out, unsigned long long cap, cudaStream_t s, int* r_bits,
-                int* nwin, bool time_it) {
+                int* nwin, bool time_it, const EarlyExit* ee = nullptr) {
   g_launches = 0;
+  g_buckets_planned = 0;
   std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
   *nwin = (int)wins.size();
   JoinPlan P0;
@@ -228,6 +246,8 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     g_launches += 1 + (maxbits > kBaseBits ? 2 * (maxbits - kBaseBits) : 0);
   }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  const bool early = ee != nullptr && wins.size() == 1;
   for (auto& w : wins) {
     // every piece reuses the geometry planned for the widest (first) piece
     JoinPlan P = P0;
@@ -238,16 +258,38 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     const uint64_t nb = 1ull << P.r;
     P.bucket_begin = nb * (uint64_t)shard / (uint64_t)nshards;
     P.bucket_end = nb * (uint64_t)(shard + 1) / (uint64_t)nshards;
-    uint64_t span = P.bucket_end - P.bucket_begin;
+    const uint64_t span = P.bucket_end - P.bucket_begin;
     if (span == 0) continue;
-    const uint64_t ctas = (uint64_t)g.nsm * kJoinCtasPerSm;  // resident join CTAs
-    int grid = (int)(span < ctas ? span : ctas);
-    RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, (DevCounters*)g.ctr.p, grid, s));
+    g_buckets_planned += (int64_t)span;
+    // resident join CTAs; with early exit one slot stays free for the poller
+    const int ctas = g.nsm * kJoinCtasPerSm - (early ? 1 : 0);
+    const int grid = (int)(span < (uint64_t)ctas ? span : (uint64_t)ctas);
+    // rotation starts and the per-CTA start positions, up front
+    const size_t mot = ((size_t)1 << P.list[0].bits) + ((size_t)1 << P.list[2].bits);
+    RFR_CUDA_OK(g.jstarts.ensure(mot * (1 + (size_t)grid) * sizeof(uint32_t)));
+    uint32_t* d_rots = (uint32_t*)g.jstarts.p;
+    RFR_CUDA_OK(launch_join_starts(P, final_bufs(P0), P.bucket_begin, P.bucket_end, 1, grid, d_rots,
+                                   d_rots + mot, s));
     g_launches += 1;
+    if (early) {
+      RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), s));  // kUnsetHit slots
+      RFR_CUDA_OK(cudaEventRecord(g.ev_fork, s));
+      RFR_CUDA_OK(cudaStreamWaitEvent(g.stream2, g.ev_fork, 0));
+      RFR_CUDA_OK(launch_early_exit_poller(P0, bufs(0), H, (const uint32_t*)g.rotc.p, d_out, cap,
+                                           ee->d_keys2, n, ee->lo2, ee->width2, ee->d_post,
+                                           ee->post_cap, ee->V, d_ctr, grid, g.stream2));
+      RFR_CUDA_OK(cudaEventRecord(g.ev_join, g.stream2));
+      g_launches += 1;
+    }
+    RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, d_ctr, grid, s, d_rots, d_rots + mot, early));
+    g_launches += 1;
+    if (early) RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_join, 0));
   }
-  // the join emits quarter-list indices; rewrite every hit as its pattern
+  // the join emits quarter-list indices; rewrite every hit (the poller's
+  // already are, up to raw_done) as its pattern
   RFR_CUDA_OK(launch_index_to_pattern(P0, bufs(0), H, (const uint32_t*)g.rotc.p, d_out,
-                                      &((DevCounters*)g.ctr.p)->out_count, cap, g.nsm, s));
+                                      &d_ctr->out_count, cap, g.nsm, s,
+                                      early ? &d_ctr->raw_done : nullptr));
   g_launches += 1;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
   return RFR_OK;
@@ -269,6 +311,7 @@ void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin
   st->r_bits = r_bits;
   st->windows = nwin;
   st->launches = g_launches;
+  st->buckets_planned = g_buckets_planned;
 }
 
 // The profile's doubles packed for one H2D copy: [real_hi | real_lo | sum_hi |
@@ -347,7 +390,7 @@ int rfr_num_sms(void) { return g.nsm; }
 // Free everything the context holds (safe on a partially initialised one).
 static void release_ctx() {
   if (g.stream) cudaStreamSynchronize(g.stream);
-  DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc,
+  DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts,
                     &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef};
   for (DevVec* v : vecs) v->release();
   for (auto& h : g.hist) h.release();
@@ -357,6 +400,9 @@ static void release_ctx() {
     for (auto& v : a) v.release();
   for (auto& e : g.ev)
     if (e) cudaEventDestroy(e);
+  if (g.ev_fork) cudaEventDestroy(g.ev_fork);
+  if (g.ev_join) cudaEventDestroy(g.ev_join);
+  if (g.stream2) cudaStreamDestroy(g.stream2);
   if (g.h_ctr) cudaFreeHost(g.h_ctr);
   if (g.h_stage) cudaFreeHost(g.h_stage);
   if (g.stream) cudaStreamDestroy(g.stream);
@@ -373,7 +419,10 @@ static int init_ctx(int device) {
   g.device = device;
   g.nsm = prop.multiProcessorCount;
   RFR_CUDA_OK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  RFR_CUDA_OK(cudaStreamCreateWithFlags(&g.stream2, cudaStreamNonBlocking));
   for (auto& e : g.ev) RFR_CUDA_OK(cudaEventCreate(&e));
+  RFR_CUDA_OK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+  RFR_CUDA_OK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
   RFR_CUDA_OK(g.ctr.ensure(sizeof(DevCounters)));
   RFR_CUDA_OK(cudaMallocHost(&g.h_ctr, sizeof(DevCounters)));
   RFR_CUDA_OK(g.keys.ensure(64 * sizeof(uint64_t)));
@@ -550,7 +599,7 @@ int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, in
 int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
-                      int stride, int64_t cap, int64_t* nout, rfr_stats* st) {
+                      int stride, int64_t cap, int early_exit, int64_t* nout, rfr_stats* st) {
   std::lock_guard<std::mutex> lk(g_mu);
   int rc = ensure_ready();
   if (rc) return rc;
@@ -628,23 +677,51 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   for (int attempt = 0;; attempt++) {
     const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
     RFR_CUDA_OK(g.post.ensure(raw_cap * sizeof(uint64_t)));
+    const unsigned long long post_cap = g.post.bytes / sizeof(uint64_t);
     RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
-    rc = search_core(d_keys, n, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &r_bits, &nwin, true);
+    // Tr3 window over the raw hits from *begin on, then verification of the
+    // survivors from *vbegin on (null: all); found: flag a PASS raises
+    auto filter_verify = [&](const unsigned long long* begin, const unsigned long long* vbegin,
+                             unsigned long long* found) -> int {
+      RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap,
+                                   lo2, width2, (uint64_t*)g.post.p, post_cap, d_ctr, g.nsm, s, begin));
+      VerifyArgs A = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
+      A.pats = (const uint64_t*)g.post.p;
+      A.m = (long long)vrows;
+      A.m_dev = &d_ctr->post_count;
+      A.m_begin_dev = vbegin;
+      A.found = found;
+      A.verdict = (uint8_t*)obase;
+      A.side = (uint8_t*)(obase + q_side);
+      A.coeffs = (long long*)(obase + q_coef);
+      A.stride = stride;
+      RFR_CUDA_OK(launch_verify(A, s));
+      g_launches += 2;
+      return RFR_OK;
+    };
+    EarlyExit ee;
+    ee.d_keys2 = d_keys2;
+    ee.lo2 = lo2;
+    ee.width2 = width2;
+    ee.d_post = (uint64_t*)g.post.p;
+    ee.post_cap = post_cap;
+    ee.V = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
+    ee.V.pats = (const uint64_t*)g.post.p;
+    ee.V.m = (long long)vrows;
+    ee.V.m_dev = nullptr;
+    ee.V.found = &d_ctr->found;
+    ee.V.verdict = (uint8_t*)obase;
+    ee.V.side = (uint8_t*)(obase + q_side);
+    ee.V.coeffs = (long long*)(obase + q_coef);
+    ee.V.stride = stride;
+    rc = search_core(d_keys, n, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &r_bits, &nwin, true,
+                     early_exit ? &ee : nullptr);
     if (rc) return rc;
-    RFR_CUDA_OK(launch_keyfilter(d_keys2, n, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2,
-                                 width2, (uint64_t*)g.post.p, g.post.bytes / sizeof(uint64_t), d_ctr,
-                                 g.nsm, s));
-    g_launches += 1;
-    VerifyArgs A = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
-    A.pats = (const uint64_t*)g.post.p;
-    A.m = (long long)vrows;
-    A.m_dev = &d_ctr->post_count;
-    A.verdict = (uint8_t*)obase;
-    A.side = (uint8_t*)(obase + q_side);
-    A.coeffs = (long long*)(obase + q_coef);
-    A.stride = stride;
-    RFR_CUDA_OK(launch_verify(A, s));
-    g_launches += 1;
+    const bool early = early_exit && nwin == 1;
+    // the rest of the hits (all of them without early exit)
+    if ((rc = filter_verify(early ? &d_ctr->raw_done : nullptr, early ? &d_ctr->post_done : nullptr,
+                            nullptr)))
+      return rc;
     RFR_CUDA_OK(cudaEventRecord(g.ev[3], s));
     // outputs: counters plus the first rows (the staged inputs were consumed
     // by the H2D above, so the staging block takes the results)

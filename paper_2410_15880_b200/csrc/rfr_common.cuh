@@ -4,6 +4,7 @@
 // of its per-entity keys (fixed-point fractional parts scaled by 2^64), so an
 // integer sum of fractional parts is a key near 0.  See DESIGN.md section 2.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -95,7 +96,16 @@ struct DevCounters {
   unsigned long long chunks;         // extra A chunks after a bucket overflow
   unsigned long long buckets;        // buckets processed
   unsigned long long post_count;     // survivors of the post-filter
+  // early exit (rfr_search_verify with early_exit): the poller verifies hits
+  // while the join runs and raises found; the join's CTAs stop at their next
+  // bucket boundary.  found is 16-byte aligned (the join copies it with one
+  // 16-byte cp.async).
+  unsigned long long raw_done;       // raw hits the poller turned into patterns and filtered
+  unsigned long long post_done;      // survivors the poller verified
+  unsigned long long found;          // a candidate passed verification
+  unsigned long long ctas_done;      // join CTAs finished (the poller's stop condition)
 };
+static_assert(offsetof(DevCounters, found) % 16 == 0, "found must be 16-byte aligned");
 
 }  // namespace rfr
 

@@ -10,15 +10,19 @@ ListHist list_hist_layout(const JoinPlan& P, char* const base[4]);
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
                          uint32_t* d_rot, ListHist H, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
-                        unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s);
+                        unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s,
+                        const uint32_t* d_rots, const uint32_t* d_starts, bool early = false);
+cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t b0, uint64_t b1,
+                               int nck, int ctas, uint32_t* d_rots, uint32_t* d_starts, cudaStream_t s);
 cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
                                     const uint32_t* d_rot, uint64_t* d_out,
                                     const unsigned long long* d_count, unsigned long long cap, int nsm,
-                                    cudaStream_t s);
+                                    cudaStream_t s, const unsigned long long* d_begin = nullptr);
 cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_in,
                              const unsigned long long* d_in_count, unsigned long long cap_in,
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
-                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s);
+                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
+                             const unsigned long long* d_begin = nullptr);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            const unsigned long long* d_in_count, unsigned long long cap_in,
                            double eps, uint64_t* d_out, unsigned long long cap_out,
@@ -39,6 +43,8 @@ struct VerifyArgs {
   const uint64_t* pats;
   long long m;                            // candidates (grid bound)
   const unsigned long long* m_dev;        // optional device count (<= m), or null
+  const unsigned long long* m_begin_dev = nullptr;  // optional first candidate (chunked search)
+  unsigned long long* found = nullptr;    // optional flag raised by a PASS (early exit)
   const uint64_t* p_mod;  // 3 x (d+1)
   uint64_t primes[3];
   uint8_t* verdict;
@@ -47,6 +53,11 @@ struct VerifyArgs {
   int stride;
 };
 cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s);
+cudaError_t launch_early_exit_poller(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
+                                     const uint32_t* d_rot, uint64_t* d_out, unsigned long long raw_cap,
+                                     const uint64_t* d_keys2, int n, uint64_t lo2, uint64_t width2,
+                                     uint64_t* d_post, unsigned long long post_cap, const VerifyArgs& V,
+                                     DevCounters* d_ctr, int join_ctas, cudaStream_t s);
 // Primes of the modular division test, P = 2^k - c with small c (fast
 // reduction in the verify kernel): 2^61 - 1, 2^62 - 57, 2^63 - 25.
 constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 4611686018427387847ull,

@@ -67,6 +67,9 @@ constexpr uint32_t kFlagCont = 0x80000000u;
 static_assert(kL2Log == kL1Log - 2 && kL3Log == kL1Log - 4,
               "the level-2/3 homes are the level-1 home shifted right by 2 / 4");
 struct JoinSmem {
+  // early exit: DevCounters.found (+ the next word) copied in by cp.async at
+  // the start of each bucket, read after the bucket's last barrier
+  alignas(16) unsigned long long stop_buf[2];
   uint64_t recK[kCapRec];  // A records: key
   uint32_t recI[kCapRec];  // A records: outer << inner_bits | inner index
   uint16_t rh[kCapRec];     // A records: level-1 home (levels 2, 3: rh >> 2, rh >> 4)
@@ -888,17 +891,16 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   const JoinPlan& P = a.P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-  const uint32_t MoA = 1u << P.list[0].bits, MiA = 1u << P.list[1].bits;
-  const uint32_t MoB = 1u << P.list[2].bits, MiB = 1u << P.list[3].bits;
-  const uint64_t* __restrict__ kA = a.key[1];
-  const uint64_t* __restrict__ kB = a.key[3];
-  const int sh = 64 - P.r;  // bucket = key >> sh
+  const uint32_t MoA = 1u << P.list[0].bits, MoB = 1u << P.list[2].bits;
   const bool smallh = use_smallh(P);
 
   const uint64_t nbk = P.bucket_end - P.bucket_begin;
   const uint64_t c_begin = P.bucket_begin + nbk * blockIdx.x / gridDim.x;
   const uint64_t c_end = P.bucket_begin + nbk * (blockIdx.x + 1) / gridDim.x;
-  if (c_begin >= c_end) return;
+  if (c_begin >= c_end) {
+    if (threadIdx.x == 0) atomicAdd(&a.ctr->ctas_done, 1ull);  // the early-exit poller counts CTAs
+    return;
+  }
   unsigned long long* dbg = (RFR_JOIN_TRACE && a.dbg && blockIdx.x == 0 && tid == 0) ? a.dbg : nullptr;
   int dbg_n = 0;
 #define RFR_MARK()                                   \
@@ -907,17 +909,18 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   } while (0)
   RFR_MARK();
 
+  // outer keys, rotation starts and first-bucket positions: precomputed for
+  // every CTA of this launch by join_starts_kernel
+  const uint32_t* __restrict__ st0 = a.starts + (size_t)blockIdx.x * (MoA + MoB);
   for (uint32_t i = tid; i < MoA; i += kJoinThreads) {
-    uint64_t x = __ldg(a.key[0] + i);
-    S.ax[i] = x;
-    S.arot[i] = rotation_start(kA, MiA, x);
-    S.apos[i] = count_below(kA, MiA, x, c_begin << sh);
+    S.ax[i] = __ldg(a.key[0] + i);
+    S.arot[i] = __ldg(a.rots + i);
+    S.apos[i] = __ldg(st0 + i);
   }
   for (uint32_t i = tid; i < MoB; i += kJoinThreads) {
-    uint64_t x = __ldg(a.key[2] + i) + P.shift;
-    S.bx[i] = x;
-    S.brot[i] = rotation_start(kB, MiB, x);
-    S.bpos[i] = count_below(kB, MiB, x, c_begin << sh);
+    S.bx[i] = __ldg(a.key[2] + i) + P.shift;
+    S.brot[i] = __ldg(a.rots + MoA + i);
+    S.bpos[i] = __ldg(st0 + MoA + i);
   }
 
   {
@@ -935,7 +938,8 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   }
   uint32_t n_chunks = 0;
 
-  for (uint64_t c = c_begin; c < c_end; c++) {
+  uint64_t c = c_begin;
+  for (; c < c_end; c++) {
     const uint64_t cW = c << (64 - P.r);
     clear_index();
     if (tid_now() == 0) {
@@ -943,6 +947,15 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       join_smem().ovf = 0;
     }
     __syncthreads();
+    // has a verified factor turned up?  Copied in now, read after this
+    // bucket's last barrier (issued after the barrier above, so no thread is
+    // still reading the previous bucket's copy)
+    if (a.early && tid_now() == 0) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&join_smem().stop_buf[0]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;\n" ::"r"(dst),
+                   "l"(&a.ctr->found)
+                   : "memory");
+    }
     RFR_MARK();
 
     // ---- fast path: A runs (+ continuations) into the warp partitions
@@ -992,8 +1005,13 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
         for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
       }
       RFR_MARK();
+      if (a.early && tid_now() == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncthreads();
       RFR_MARK();
+      if (a.early && join_smem().stop_buf[0]) {
+        c++;
+        break;
+      }
       continue;
     }
 
@@ -1009,7 +1027,12 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       for (uint32_t i = join_smem().wlo[1][w] + l; i < join_smem().whi[1][w]; i += 32) join_smem().bpos[i] += join_smem().bmain[i];
       for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
     }
+    if (a.early && tid_now() == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
+    if (a.early && join_smem().stop_buf[0]) {
+      c++;
+      break;
+    }
   }
   const uint32_t n_ins = S.cnt[0][tid], n_q = S.cnt[1][tid], n_qprobe = S.cnt[2][tid];
   atomicAdd(&a.ctr->inserts, (unsigned long long)n_ins);
@@ -1017,6 +1040,8 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
   atomicAdd(&a.ctr->query_probes, (unsigned long long)n_qprobe);
   if (tid == 0) {
     atomicAdd(&a.ctr->chunks, (unsigned long long)n_chunks);
-    atomicAdd(&a.ctr->buckets, (unsigned long long)(c_end - c_begin));
+    atomicAdd(&a.ctr->buckets, (unsigned long long)(c - c_begin));  // fewer on an early exit
+    __threadfence();  // every hit of this CTA is visible before it counts as done
+    atomicAdd(&a.ctr->ctas_done, 1ull);
   }
 }

@@ -23,6 +23,7 @@
 
 #include "rfr_common.cuh"
 #include "rfr_internal.h"
+#include "rfr_verify.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -147,37 +148,6 @@ __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __rest
   }
 }
 
-// lower_bound over a sorted uint64 array
-__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* __restrict__ a, uint32_t n,
-                                                    uint64_t v) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) < v) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// Rotation start of the sequence (x + a[j]) mod 2^64 over a sorted array:
-// the first j whose sum wraps, or 0 when none does.
-__device__ __forceinline__ uint32_t rotation_start(const uint64_t* __restrict__ a, uint32_t n,
-                                                   uint64_t x) {
-  if (x == 0) return 0;
-  uint32_t j = lower_bound_u64(a, n, 0ull - x);
-  return j == n ? 0 : j;
-}
-
-// Number of j with (x + a[j]) mod 2^64 < bound, for a sorted array.
-__device__ __forceinline__ uint32_t count_below(const uint64_t* __restrict__ a, uint32_t n,
-                                                uint64_t x, uint64_t bound) {
-  if (bound == 0) return 0;
-  uint64_t lo = 0ull - x;          // sums start at key -x
-  uint64_t hi = lo + bound;        // exclusive end, mod 2^64
-  uint32_t l = lower_bound_u64(a, n, lo);
-  if (hi > lo) return lower_bound_u64(a, n, hi) - l;    // no wrap
-  return (n - l) + lower_bound_u64(a, n, hi);            // wraps through 2^64
-}
 
 // One doubling level for every list that has it: L (2^k sorted sums of the
 // list's first k elements) -> merge(L, rotate(L + v_k)), v_k the key of
@@ -350,6 +320,11 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
 struct JoinArgs {
   JoinPlan P;
   const uint64_t* key[4];
+  // per outer (A outers, then B outers): rotation start, and this launch's
+  // start position in each CTA's first bucket (join_starts_kernel)
+  const uint32_t* rots;
+  const uint32_t* starts;  // [cta][MoA + MoB]
+  int early;               // stop at a bucket boundary once DevCounters.found is set
   uint64_t* out;
   unsigned long long cap;
   DevCounters* ctr;
@@ -357,6 +332,76 @@ struct JoinArgs {
 };
 
 #include "rfr_join.cuh"
+
+// lower_bound of v in a sorted array by one warp: 32 probes per round narrow
+// [lo, hi] 32-fold, so ~5 dependent loads for 2^28 entries instead of 28.
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint64_t* __restrict__ a, uint32_t n,
+                                                     uint64_t v, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  uint32_t lo = 0, hi = n;  // the answer lies in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t span = hi - lo;
+    const uint32_t q = lo + (uint32_t)(((uint64_t)span * (uint32_t)(lane + 1)) >> 5) - 1u;
+    const uint32_t c = __popc(__ballot_sync(FULL, __ldg(a + q) < v));  // a prefix of the probes
+    const uint32_t qlo = __shfl_sync(FULL, q, (c ? c : 1u) - 1u);
+    const uint32_t qhi = __shfl_sync(FULL, q, c < 32u ? c : 31u);
+    if (c) lo = qlo + 1u;
+    if (c < 32u) hi = qhi;
+  }
+  const uint32_t q = lo + (uint32_t)lane;
+  return lo + __popc(__ballot_sync(FULL, q < hi && __ldg(a + q) < v));
+}
+
+// Start state of every join launch of one key window, computed up front with
+// one warp per search (the join's CTAs would otherwise each run ~140
+// dependent binary-search loads before their first bucket, per launch).
+// Task t < MoA + MoB: rotation start of outer t; then, for chunk k and CTA c,
+// the outer's count of sums below the CTA's first bucket (count_below).
+__global__ void __launch_bounds__(256) join_starts_kernel(JoinPlan P, const uint64_t* __restrict__ kO_A,
+                                                          const uint64_t* __restrict__ kA,
+                                                          const uint64_t* __restrict__ kO_B,
+                                                          const uint64_t* __restrict__ kB,
+                                                          uint64_t b0, uint64_t b1, int nck, int ctas,
+                                                          uint32_t* __restrict__ rots,
+                                                          uint32_t* __restrict__ starts) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t MoA = 1u << P.list[0].bits, MoB = 1u << P.list[2].bits, MoT = MoA + MoB;
+  const uint64_t task = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t ntask = (uint64_t)MoT * (1ull + (uint64_t)nck * (uint64_t)ctas);
+  if (task >= ntask) return;  // warp-uniform
+  const uint32_t o = (uint32_t)(task % MoT);
+  const bool sideB = o >= MoA;
+  const uint32_t oi = sideB ? o - MoA : o;
+  const uint64_t* __restrict__ inner = sideB ? kB : kA;
+  const uint32_t n = 1u << P.list[sideB ? 3 : 1].bits;
+  const uint64_t x = sideB ? __ldg(kO_B + oi) + P.shift : __ldg(kO_A + oi);
+  const uint64_t l0 = 0ull - x;  // sums start at key -x
+  if (task < MoT) {
+    if (lane == 0) rots[o] = 0;
+    const uint32_t j = x == 0 ? 0u : warp_lower_bound(inner, n, l0, lane);
+    if (lane == 0) rots[o] = j == n ? 0u : j;
+    return;
+  }
+  const uint64_t kc = task / MoT - 1;  // chunk * ctas + cta
+  const int k = (int)(kc / (uint64_t)ctas), c = (int)(kc % (uint64_t)ctas);
+  // the join's own bucket arithmetic (search_core, join_kernel)
+  const uint64_t cb = b0 + (b1 - b0) * (uint64_t)k / (uint64_t)nck;
+  const uint64_t ce = b0 + (b1 - b0) * (uint64_t)(k + 1) / (uint64_t)nck;
+  const uint64_t span = ce - cb;
+  const uint64_t grid = span < (uint64_t)ctas ? span : (uint64_t)ctas;
+  uint32_t pos = 0;
+  if ((uint64_t)c < grid) {
+    const uint64_t c_begin = cb + span * (uint64_t)c / grid;
+    const uint64_t bound = c_begin << (64 - P.r);
+    if (bound != 0) {
+      const uint64_t hi = l0 + bound;  // exclusive end, mod 2^64
+      const uint32_t l = warp_lower_bound(inner, n, l0, lane);
+      const uint32_t h = warp_lower_bound(inner, n, hi, lane);
+      pos = hi > l0 ? h - l : (n - l) + h;  // wraps through 2^64 when hi <= l0
+    }
+  }
+  if (lane == 0) starts[kc * MoT + o] = pos;
+}
 
 // ------------------------------------------------- indices -> patterns
 // The join emits each hit as its four quarter-list indices (packed at the
@@ -402,9 +447,11 @@ __device__ __forceinline__ uint32_t list_pattern(const PatArgs& a, int li, uint3
 
 __global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, uint64_t* out,
                                                                const unsigned long long* count,
-                                                               unsigned long long cap) {
+                                                               unsigned long long cap,
+                                                               const unsigned long long* begin) {
   unsigned long long m = *count;
   if (m > cap) m = cap;
+  const unsigned long long m0 = begin ? min(*begin, m) : 0ull;  // hits [m0, m) are new
   const JoinPlan& P = a.P;
   // four lanes per hit, one per quarter list: the two long history walks
   // (the inner lists) run side by side instead of back to back
@@ -412,8 +459,8 @@ __global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, 
   const ListSpec L = pick_list(P, li);
   const unsigned long long lanes = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned long long wbase = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  for (unsigned long long tb = wbase; tb < 4 * m; tb += lanes) {  // warp-uniform trip count
-    const unsigned long long i = (tb + (threadIdx.x & 31u)) >> 2;
+  for (unsigned long long tb = wbase; tb < 4 * (m - m0); tb += lanes) {  // warp-uniform trip count
+    const unsigned long long i = m0 + ((tb + (threadIdx.x & 31u)) >> 2);
     uint64_t part = 0;
     if (i < m) {
       const uint64_t v = out[i];
@@ -429,13 +476,13 @@ __global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, 
 cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
                                     const uint32_t* d_rot, uint64_t* d_out,
                                     const unsigned long long* d_count, unsigned long long cap, int nsm,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, const unsigned long long* d_begin) {
   PatArgs a;
   a.P = P;
   for (int i = 0; i < 4; i++) a.pat[i] = base.p[i];
   a.hist = hist;
   a.rot = d_rot;
-  index_to_pattern_kernel<<<nsm * 4, 256, 0, s>>>(a, d_out, d_count, cap);
+  index_to_pattern_kernel<<<nsm * 4, 256, 0, s>>>(a, d_out, d_count, cap, d_begin);
   return cudaGetLastError();
 }
 
@@ -474,13 +521,14 @@ __global__ void keyfilter_kernel(const uint64_t* __restrict__ keys2, int n,
                                  const unsigned long long* __restrict__ in_count,
                                  unsigned long long cap_in, uint64_t lo2, uint64_t width2,
                                  uint64_t* __restrict__ out, unsigned long long cap_out,
-                                 DevCounters* ctr) {
+                                 DevCounters* ctr, const unsigned long long* __restrict__ begin) {
   __shared__ uint64_t sk[64];
   for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = keys2[i];
   __syncthreads();
   unsigned long long m = *in_count;
   if (m > cap_in) m = cap_in;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+  const unsigned long long m0 = begin ? min(*begin, m) : 0ull;
+  for (unsigned long long i = m0 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint64_t t = in[i];
     uint64_t sum = 0, u = t;
@@ -568,8 +616,18 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
   return cudaGetLastError();
 }
 
+cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t b0, uint64_t b1,
+                               int nck, int ctas, uint32_t* d_rots, uint32_t* d_starts, cudaStream_t s) {
+  const uint64_t mot = (1ull << P.list[0].bits) + (1ull << P.list[2].bits);
+  const uint64_t warps = mot * (1ull + (uint64_t)nck * (uint64_t)ctas);
+  join_starts_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(P, fin.k[0], fin.k[1], fin.k[2], fin.k[3],
+                                                                b0, b1, nck, ctas, d_rots, d_starts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
-                        unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s) {
+                        unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s,
+                        const uint32_t* d_rots, const uint32_t* d_starts, bool early) {
   static uint64_t attr_done = 0;
   cudaError_t e = raise_smem_limit(join_kernel, sizeof(JoinSmem), attr_done);
   if (e != cudaSuccess) return e;
@@ -579,6 +637,9 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
   a.out = d_out;
   a.cap = cap;
   a.ctr = d_ctr;
+  a.rots = d_rots;
+  a.starts = d_starts;
+  a.early = early ? 1 : 0;
   static unsigned long long* dbg = nullptr;
   a.dbg = nullptr;
   if (getenv("RFR_TRACE")) {
@@ -641,9 +702,129 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in, const unsi
 cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_in,
                              const unsigned long long* d_in_count, unsigned long long cap_in,
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
-                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s) {
+                             unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
+                             const unsigned long long* d_begin) {
   keyfilter_kernel<<<nsm * 4, 256, 0, s>>>(d_keys2, n, d_in, d_in_count, cap_in, lo2, width2, d_out,
-                                          cap_out, d_ctr);
+                                          cap_out, d_ctr, d_begin);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- early exit
+// One warp beside the running join (its own stream, a CTA slot the join
+// leaves free): takes the raw hits in emission order as they appear, turns
+// each into its pattern, applies the Tr3 window and verifies survivors in
+// place; a PASS raises DevCounters.found and the join's CTAs stop at their
+// next bucket boundary.  It publishes how far it got (raw_done, post_done)
+// and leaves as soon as every join CTA has finished (or after a time limit):
+// the batch kernels then finish whatever it did not reach, so a flood of
+// hits (Swinnerton-Dyer f6) costs it nothing.  Raw slots hold kUnsetHit until the
+// join's store lands (the count is bumped first).
+constexpr uint64_t kUnsetHit = ~0ull;
+
+struct PollArgs {
+  PatArgs pa;
+  uint64_t* out;
+  unsigned long long raw_cap;
+  const uint64_t* keys2;
+  int n;
+  uint64_t lo2, width2;
+  uint64_t* post;
+  unsigned long long post_cap;
+  VerifyArgs V;  // V.pats = post, V.m = verification rows
+  DevCounters* ctr;
+  unsigned long long join_ctas;
+  long long max_cycles;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_constant__ PollArgs a) {
+  __shared__ WarpBuf B;
+  __shared__ ProfSmem PS;
+  __shared__ uint64_t sk[64];
+  const int lane = threadIdx.x;
+  stage_profile_smem(PS, a.V, lane, 32);
+  for (int i = lane; i < a.n; i += 32) sk[i] = a.keys2[i];
+  __syncwarp();
+  const long long t0 = clock64();
+  unsigned long long done = 0;
+  while (true) {
+    // once the join is over the batch kernels take the rest (a flood of hits
+    // would keep one warp busy for seconds)
+    if (ld_acquire_u64(&a.ctr->ctas_done) >= a.join_ctas) break;
+    unsigned long long cnt = ld_acquire_u64(&a.ctr->out_count);
+    if (cnt > a.raw_cap) cnt = a.raw_cap;
+    if (done < cnt) {
+      // the slot is written right after the count was bumped
+      uint64_t v = kUnsetHit;
+      while ((v = ld_acquire_u64((const unsigned long long*)a.out + done)) == kUnsetHit &&
+             clock64() - t0 < a.max_cycles) {
+      }
+      if (v == kUnsetHit) break;  // time limit: the batch kernels take over
+      // pattern: lanes 0-3 walk the four quarter lists (index_to_pattern_kernel)
+      uint64_t part = 0;
+      if (lane < 4) {
+        const ListSpec L = pick_list(a.pa.P, lane);
+        const uint32_t idx = (uint32_t)((v >> L.pat_shift) & ((1ull << L.bits) - 1ull));
+        part = (uint64_t)list_pattern(a.pa, lane, idx) << L.pat_shift;
+      }
+      part |= __shfl_xor_sync(0xffffffffu, part, 1);
+      part |= __shfl_xor_sync(0xffffffffu, part, 2);
+      const uint64_t t = __shfl_sync(0xffffffffu, part, 0);
+      // Tr3 window (keyfilter_kernel)
+      uint64_t s3 = 0;
+      for (int i = lane; i < a.n; i += 32) s3 += ((t >> i) & 1ull) ? sk[i] : 0ull;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+      if (lane == 0) a.out[done] = t;
+      if (s3 - a.lo2 <= a.width2) {
+        unsigned long long k = 0;
+        if (lane == 0) k = atomicAdd(&a.ctr->post_count, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k < a.post_cap && lane == 0) a.post[k] = t;
+        __syncwarp();
+        if (k < a.post_cap && (long long)k < a.V.m) verify_one(a.V, PS, B, (long long)k, lane);
+        __syncwarp();
+      }
+      done++;
+      if (lane == 0) {
+        a.ctr->raw_done = done;
+        a.ctr->post_done = *(volatile unsigned long long*)&a.ctr->post_count;
+      }
+      continue;
+    }
+    if (clock64() - t0 > a.max_cycles) break;
+    __nanosleep(1000);
+  }
+}
+
+cudaError_t launch_early_exit_poller(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
+                                     const uint32_t* d_rot, uint64_t* d_out, unsigned long long raw_cap,
+                                     const uint64_t* d_keys2, int n, uint64_t lo2, uint64_t width2,
+                                     uint64_t* d_post, unsigned long long post_cap, const VerifyArgs& V,
+                                     DevCounters* d_ctr, int join_ctas, cudaStream_t s) {
+  PollArgs a;
+  a.pa.P = P;
+  for (int i = 0; i < 4; i++) a.pa.pat[i] = base.p[i];
+  a.pa.hist = hist;
+  a.pa.rot = d_rot;
+  a.out = d_out;
+  a.raw_cap = raw_cap;
+  a.keys2 = d_keys2;
+  a.n = n;
+  a.lo2 = lo2;
+  a.width2 = width2;
+  a.post = d_post;
+  a.post_cap = post_cap;
+  a.V = V;
+  a.ctr = d_ctr;
+  a.join_ctas = (unsigned long long)join_ctas;
+  a.max_cycles = 4000000000ll;  // ~2 s at 2 GHz: never hold the device if the join cannot start
+  early_exit_poller_kernel<<<1, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -64,6 +64,7 @@ class FactorStats:
     rejected: int = 0
     recombine: RecombineStats = field(default_factory=RecombineStats)
     host_verified: int = 0
+    early_exits: int = 0  # searches stopped after a chunk with a verified factor
 
 
 @dataclass(frozen=True)
@@ -189,6 +190,21 @@ def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, hal
     power-sum window and the verification of every survivor, without the
     candidates leaving the GPU in between.  Returns (pats, verdict, side,
     coeffs) like search_keys + verify_candidates (patterns unsorted)."""
+    return _search_and_verify(prof, p, keys, half_width, keys3, half_width3, stats, False)[:4]
+
+
+# Early termination (north star: "results are checked for early termination";
+# SURVEY s8(e)): searches over n >= _EARLY_N entities verify their hits while
+# the join runs and stop once one passes.  Smaller searches take ~0.1 ms and
+# run whole.
+_EARLY_N = 48
+
+
+def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
+                       keys3: np.ndarray, half_width3: int, stats, early_exit: bool):
+    """search_and_verify, optionally with early termination.  Returns (pats,
+    verdict, side, coeffs, complete); complete is False when the search
+    stopped once a candidate passed (the pattern space was not exhausted)."""
     from .recombine import _fill_stats, _window
 
     lib = _lib.load()
@@ -213,7 +229,7 @@ def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, hal
                 _lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
                 ctypes.byref(rp), _lib.ptr(pm, _lib.U64_P), p.degree, _lib.ptr(pats, _lib.U64_P),
                 verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
-                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap, ctypes.byref(nout),
+                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap, int(bool(early_exit)), ctypes.byref(nout),
                 ctypes.byref(st)),
             "rfr_search_verify",
         )
@@ -222,7 +238,37 @@ def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, hal
         cap = int(nout.value)
     _fill_stats(stats, st)
     m = int(nout.value)
-    return pats[:m], verdict[:m], side[:m], coeffs[:m]
+    complete = st.buckets >= st.buckets_planned
+    return pats[:m], verdict[:m], side[:m], coeffs[:m], complete
+
+
+def _sub_profile(prof: RootProfile, t: int) -> RootProfile:
+    """The profile of the factor whose entities pattern t selects, without new
+    root finding (the reference re-runs find_roots on each
+    piece, R/verify.py:257): entities keep their double-double values and
+    their keys in rho order; the key and root error bounds of the whole
+    profile bound every subset sum."""
+    bits = [i for i in range(prof.n) if (t >> i) & 1]
+    ents = [prof.perm[i] for i in bits]
+    reals = np.asarray(sorted(e for e in ents if e < prof.r), dtype=np.int64)
+    pairs = np.asarray(sorted(e - prof.r for e in ents if e >= prof.r), dtype=np.int64)
+    new_id = {int(e): j for j, e in enumerate(reals)}
+    new_id.update({prof.r + int(e): len(reals) + j for j, e in enumerate(pairs)})
+    idx = np.asarray(bits, dtype=np.int64)
+
+    def take(a, sel):
+        return None if a is None else np.asarray(a)[sel]
+
+    return RootProfile(
+        real_roots=prof.real_roots[reals], pair_sums=prof.pair_sums[pairs],
+        pair_products=prof.pair_products[pairs], rho=prof.rho[idx],
+        perm=tuple(new_id[e] for e in ents),
+        real_lo=take(prof.real_lo, reals), sum_lo=take(prof.sum_lo, pairs),
+        prod_lo=take(prof.prod_lo, pairs),
+        keys1=take(prof.keys1, idx), keys2=take(prof.keys2, idx), keys3=take(prof.keys3, idx),
+        key_err1=prof.key_err1, key_err2=prof.key_err2, key_err3=prof.key_err3,
+        root_err=prof.root_err,
+    )
     D = ctypes.POINTER(ctypes.c_double)
     keep = []  # keep numpy buffers alive for the call
 
@@ -302,23 +348,28 @@ def _pmul(a, b):
 
 
 def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
-                             stats: FactorStats) -> list[IntPolynomial]:
+                             stats: FactorStats, prof: RootProfile | None = None,
+                             early_exit: bool = True) -> list[IntPolynomial]:
+    """Irreducible factors of a monic square-free p.  prof: p's root profile
+    when already known (a piece split off by an earlier search)."""
     if p.degree <= 1:
         return [p]
-    t0 = time.perf_counter()
-    prof = _profile_cached(p.coeffs)
-    stats.root_seconds += time.perf_counter() - t0
+    if prof is None:
+        t0 = time.perf_counter()
+        prof = _profile_cached(p.coeffs)
+        stats.root_seconds += time.perf_counter() - t0
     n = prof.n
     stats.n = max(stats.n, n)
 
     t0 = time.perf_counter()
     keys, T = _search_window(prof)
     keys3, T3 = _secondary_window(prof)
+    complete = True
     if workers == 1 and keys3 is not None:
         # one device call: search, Tr3 window and verification back to back
         # (recombine_seconds then covers the device verification too)
-        pats, verdict, side, coeffs = search_and_verify(prof, p, keys, T, keys3, T3,
-                                                        stats.recombine)
+        pats, verdict, side, coeffs, complete = _search_and_verify(
+            prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N)
         keep = pats != 0
         pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]
         stats.recombine_seconds += time.perf_counter() - t0
@@ -357,6 +408,24 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
                 stats.rejected += 1
         else:
             stats.rejected += 1
+    if not complete:
+        # early exit: the searched chunks hold a verified factor q but the
+        # pattern space was not exhausted, so q and p / q are factored in
+        # turn, each over its own entities (no new root finding)
+        for t in sorted(found, key=lambda x: (bin(x).count("1"), x)):
+            q = found[t]
+            rest = divide_exact(p, q)
+            if rest is None:
+                continue
+            stats.verify_seconds += time.perf_counter() - t0
+            stats.early_exits += 1
+            return (_factor_monic_squarefree(q, cfg, workers, stats, _sub_profile(prof, t))
+                    + _factor_monic_squarefree(rest, cfg, workers, stats,
+                                               _sub_profile(prof, ~t & full)))
+        # a device PASS the exact check rejects (not seen in practice): search
+        # the whole space
+        stats.verify_seconds += time.perf_counter() - t0
+        return _factor_monic_squarefree(p, cfg, workers, stats, prof, early_exit=False)
     if not found:
         stats.verify_seconds += time.perf_counter() - t0
         return [p]

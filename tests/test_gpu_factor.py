@@ -186,3 +186,81 @@ def test_fused_search_verify_matches_the_two_call_path(big_inputs, factor_cases)
             e = V.selected_degree((~t & full) if rs[k] else t, prof)
             # only coefficients 0..e are written (the rest of the row is scratch)
             assert np.array_equal(coeffs[order][k][: e + 1], rc[k][: e + 1])
+
+
+def test_early_exit_search_is_a_prefix_of_the_whole_search(big_inputs):
+    """rfr_search_verify with early termination: its candidates and verdicts
+    are a subset of the whole-space call's, the same set when the search ran
+    to the end, and a stopped search holds a passing candidate.  On the
+    d = 100 inputs at least one search stops early."""
+    from paper_2410_15880_b200 import verify as V
+
+    stopped = 0
+    for case in big_inputs["c3"]:
+        p = poly_of(case["p"])
+        prof = V._profile_cached(p.coeffs)
+        keys, T = V._search_window(prof)
+        keys3, T3 = V._secondary_window(prof)
+        whole = V._search_and_verify(prof, p, keys, T, keys3, T3, None, False)
+        part = V._search_and_verify(prof, p, keys, T, keys3, T3, None, True)
+        assert whole[4]
+        wv = {int(s): int(v) for s, v in zip(whole[0], whole[1])}
+        pv = {int(s): int(v) for s, v in zip(part[0], part[1])}
+        assert set(pv) <= set(wv) and all(wv[s] == v for s, v in pv.items())
+        if part[4]:
+            assert pv == wv
+        else:
+            stopped += 1
+            assert _lib.V_PASS in pv.values()
+    assert stopped >= 1
+
+
+def test_factor_with_early_exit_matches_the_reference(big_inputs):
+    """factor() on the d = 100 inputs stops searches early (then factors both
+    pieces over their own entities) and still returns the constructed
+    factors; the irreducible d = 120 input is searched whole."""
+    exits = 0
+    for case in big_inputs["c3"]:
+        res = factor(poly_of(case["p"]))
+        assert sorted(list(g.coeffs) for g, _ in res.factors) == sorted(
+            [int(x) for x in f] for f, _ in case["factors"])
+        assert res.certificate
+        exits += res.stats.early_exits
+    assert exits >= 1
+    res = factor(poly_of(big_inputs["c4"][0]["p"]))
+    assert res.irreducible and res.stats.early_exits == 0
+
+
+def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
+    """If the exact check rejects every verified factor of a stopped search
+    (a false device PASS), factor() searches the whole pattern space and
+    returns the same factorization."""
+    from paper_2410_15880_b200 import verify as V
+
+    for case in big_inputs["c3"]:
+        p = poly_of(case["p"])
+        if factor(p).stats.early_exits:
+            break
+    else:
+        pytest.skip("no d = 100 input stopped early")
+    real_div, real_sav = V.divide_exact, V._search_and_verify
+    state = {"whole": False, "rejected": 0}
+
+    def search(prof, q, *args):
+        if not args[-1] and prof.n >= V._EARLY_N:  # the whole-space fallback has begun
+            state["whole"] = True
+        return real_sav(prof, q, *args)
+
+    def reject_until_fallback(a, b):
+        if not state["whole"]:
+            state["rejected"] += 1
+            return None
+        return real_div(a, b)
+
+    monkeypatch.setattr(V, "_search_and_verify", search)
+    monkeypatch.setattr(V, "divide_exact", reject_until_fallback)
+    res = factor(p)
+    assert state["whole"] and state["rejected"] >= 1
+    assert res.stats.early_exits == 0 and res.certificate
+    assert sorted(list(g.coeffs) for g, _ in res.factors) == sorted(
+        [int(x) for x in f] for f, _ in case["factors"])

@@ -108,3 +108,38 @@ def test_hp_profile_c4_and_sd6_certified(big_inputs):
     assert prof.n == 63 and prof.root_err < 1e-20
     sd6 = hp_profile(poly_of(big_inputs["c5"][0]["p"]))  # multiprecision path
     assert sd6.n == 64 and sd6.r == 64 and sd6.root_err < 1e-20
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_sub_profile_of_a_factor_matches_its_own_profile(big_inputs, seed):
+    """Early exit splits p by a verified factor's pattern and searches each
+    piece over its own entities without new root finding: the sub-profile
+    of the true factor's pattern holds the factor's roots (as its own
+    hp_profile finds them), keys in rho order, and a permutation."""
+    from paper_2410_15880_b200.verify import _sub_profile, selected_degree
+
+    case = big_inputs["c3"][seed]
+    p = poly_of(case["p"])
+    f = poly_of(case["factors"][0][0])
+    prof = hp_profile(p)
+    pat = _factor_pattern(prof, None, f)
+    full = (1 << prof.n) - 1
+    for t, g in ((pat, f), (pat ^ full, poly_of(case["factors"][1][0]))):
+        sub = _sub_profile(prof, t)
+        own = hp_profile(g)
+        assert (sub.n, sub.r, sub.c) == (own.n, own.r, own.c)
+        assert sorted(sub.perm) == list(range(sub.n))
+        assert np.all(np.diff(sub.rho) >= 0)
+        assert selected_degree((1 << sub.n) - 1, sub) == g.degree
+        np.testing.assert_allclose(np.sort(sub.real_roots), np.sort(own.real_roots), rtol=1e-12)
+        np.testing.assert_allclose(np.sort(sub.pair_sums), np.sort(own.pair_sums), rtol=1e-12)
+        np.testing.assert_allclose(np.sort(sub.pair_products), np.sort(own.pair_products), rtol=1e-12)
+        # the whole sub-profile is the factor: its Tr1 key sum is an integer
+        s = sum(int(k) for k in sub.keys1) % TWO64
+        assert min(s, TWO64 - s) <= sub.key_err1 + sub.n
+        # each bit's key is its entity's first power sum (root, or t of a pair)
+        for j in range(sub.n):
+            e = sub.perm[j]
+            v = sub.real_roots[e] if e < sub.r else sub.pair_sums[e - sub.r]
+            frac = v - np.floor(v)
+            assert abs(int(sub.keys1[j]) / TWO64 - frac) < 1e-9 or abs(abs(int(sub.keys1[j]) / TWO64 - frac) - 1) < 1e-9
