@@ -73,13 +73,15 @@ class RfrProfile(ctypes.Structure):
         ("n", ctypes.c_int),
         ("r", ctypes.c_int),
         ("c", ctypes.c_int),
-        ("real_hi", ctypes.POINTER(ctypes.c_double)),
-        ("real_lo", ctypes.POINTER(ctypes.c_double)),
-        ("sum_hi", ctypes.POINTER(ctypes.c_double)),
-        ("sum_lo", ctypes.POINTER(ctypes.c_double)),
-        ("prod_hi", ctypes.POINTER(ctypes.c_double)),
-        ("prod_lo", ctypes.POINTER(ctypes.c_double)),
-        ("perm", ctypes.POINTER(ctypes.c_int32)),
+        # device-visible host addresses of the profile arrays (const double*,
+        # const int32_t* in the header; plain addresses here, set from numpy)
+        ("real_hi", ctypes.c_void_p),
+        ("real_lo", ctypes.c_void_p),
+        ("sum_hi", ctypes.c_void_p),
+        ("sum_lo", ctypes.c_void_p),
+        ("prod_hi", ctypes.c_void_p),
+        ("prod_lo", ctypes.c_void_p),
+        ("perm", ctypes.c_void_p),
         ("root_err", ctypes.c_double),
     ]
 

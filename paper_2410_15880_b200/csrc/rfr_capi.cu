@@ -640,6 +640,9 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
   RFR_CUDA_OK(g.vprof.ensure(in_bytes));
   char* base = (char*)g.vprof.p;
+  // never overlap an early-exit poller of an earlier call (one that ended in
+  // an error after its launch): it still reads the counters (no-op otherwise)
+  RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_join, 0));
   RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
   const uint64_t* d_keys = (const uint64_t*)base;
   const uint64_t* d_keys2 = (const uint64_t*)(base + o_keys2);

@@ -137,27 +137,25 @@ def _p_mod(p: IntPolynomial) -> np.ndarray:
 
 
 def _rfr_profile(prof: RootProfile):
-    """The profile as an rfr_profile struct (plus the arrays it points into,
-    which the caller keeps alive for the duration of the call)."""
-    D = ctypes.POINTER(ctypes.c_double)
-    keep = []
+    """The profile as an rfr_profile struct (plus the buffer it points into,
+    which the caller keeps alive for the duration of the call): the six
+    double arrays packed into one buffer, perm as int32."""
+    r, c = prof.r, prof.c
 
-    def dptr(a):
-        a = np.ascontiguousarray(a if a is not None else np.zeros(0), dtype=np.float64)
-        keep.append(a)
-        return a.ctypes.data_as(D)
+    def lo(a, k):
+        return np.zeros(k) if a is None else a
 
-    perm = np.ascontiguousarray(prof.perm, dtype=np.int32)
-    keep.append(perm)
+    buf = np.concatenate([prof.real_roots, lo(prof.real_lo, r), prof.pair_sums, lo(prof.sum_lo, c),
+                          prof.pair_products, lo(prof.prod_lo, c)]).astype(np.float64, copy=False)
+    perm = np.asarray(prof.perm, dtype=np.int32)
+    base, pbase = buf.ctypes.data, perm.ctypes.data
     rp = _lib.RfrProfile(
-        n=prof.n, r=prof.r, c=prof.c,
-        real_hi=dptr(prof.real_roots), real_lo=dptr(prof.real_lo),
-        sum_hi=dptr(prof.pair_sums), sum_lo=dptr(prof.sum_lo),
-        prod_hi=dptr(prof.pair_products), prod_lo=dptr(prof.prod_lo),
-        perm=perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-        root_err=float(prof.root_err),
+        n=prof.n, r=r, c=c,
+        real_hi=base, real_lo=base + 8 * r, sum_hi=base + 16 * r, sum_lo=base + 16 * r + 8 * c,
+        prod_hi=base + 16 * r + 16 * c, prod_lo=base + 16 * r + 24 * c,
+        perm=pbase, root_err=float(prof.root_err),
     )
-    return rp, keep
+    return rp, (buf, perm)
 
 
 def verify_candidates(prof: RootProfile, p: IntPolynomial, pats: np.ndarray):
@@ -269,34 +267,6 @@ def _sub_profile(prof: RootProfile, t: int) -> RootProfile:
         key_err1=prof.key_err1, key_err2=prof.key_err2, key_err3=prof.key_err3,
         root_err=prof.root_err,
     )
-    D = ctypes.POINTER(ctypes.c_double)
-    keep = []  # keep numpy buffers alive for the call
-
-    def dptr(a):
-        a = np.ascontiguousarray(a if a is not None else np.zeros(0), dtype=np.float64)
-        keep.append(a)
-        return a.ctypes.data_as(D)
-
-    perm = np.ascontiguousarray(prof.perm, dtype=np.int32)
-    keep.append(perm)
-    rp = _lib.RfrProfile(
-        n=prof.n, r=prof.r, c=prof.c,
-        real_hi=dptr(prof.real_roots), real_lo=dptr(prof.real_lo),
-        sum_hi=dptr(prof.pair_sums), sum_lo=dptr(prof.sum_lo),
-        prod_hi=dptr(prof.pair_products), prod_lo=dptr(prof.prod_lo),
-        perm=perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-        root_err=float(prof.root_err),
-    )
-    pats = np.ascontiguousarray(pats, dtype=np.uint64)
-    pm = np.ascontiguousarray(_p_mod(p))
-    _lib.check(
-        lib.rfr_verify(ctypes.byref(rp), _lib.ptr(pats, _lib.U64_P), m,
-                       _lib.ptr(pm, _lib.U64_P), p.degree,
-                       verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
-                       coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, None),
-        "rfr_verify",
-    )
-    return verdict, side, coeffs
 
 
 def _host_candidate(prof: RootProfile, p: IntPolynomial, t: int) -> IntPolynomial | None:
