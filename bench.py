@@ -266,13 +266,13 @@ def run_ours(args):
     value = total / args.steps
 
     # ---- e2e through the public API (host buffers; roots cached => excluded)
-    for w in range(max(3, args.warmup)):  # untimed: first-call staging, kernel loading
+    for w in range(0 if args.no_e2e else max(3, args.warmup)):  # untimed: staging, kernel loading
         factor(prep[w % len(prep)][1], workers=max(1, world))
     torch.cuda.synchronize()
     e2e_times = []
     early_exits = 0
     h2d = d2h = 0
-    for s in range(args.steps):
+    for s in range(0 if args.no_e2e else args.steps):
         seed, p, want, prof, keys, T, _ = prep[s % len(prep)]
         flush.zero_()
         torch.cuda.synchronize()
@@ -288,7 +288,7 @@ def run_ours(args):
         m = res.stats.candidates
         h2d += 8 * prof.n + 8 * (2 * prof.r + 4 * prof.c) + 4 * prof.n + 8 * m + 24 * (p.degree + 1)
         d2h += 8 + 8 * m + 2 * m + 8 * 65 * m
-    e2e = float(np.mean(e2e_times))
+    e2e = float(np.mean(e2e_times)) if e2e_times else float("nan")
     if dist is not None:  # max over ranks, as for the device-timed value
         tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -476,6 +476,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the factor() leg (profiling runs: under ncu the early-exit "
+                         "poller cannot run beside the join)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
