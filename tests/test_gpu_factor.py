@@ -264,3 +264,29 @@ def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
     assert res.stats.early_exits == 0 and res.certificate
     assert sorted(list(g.coeffs) for g, _ in res.factors) == sorted(
         [int(x) for x in f] for f, _ in case["factors"])
+
+
+@pytest.mark.parametrize("k,deg,seed", [(3, 32, 11), (3, 32, 12), (3, 32, 13), (4, 24, 21)])
+def test_early_exit_with_several_factors_matches_sympy(k, deg, seed):
+    """Products of k random irreducible factors (n >= 48: early termination).
+    The search may stop on a pattern that is a union of factors; the pieces
+    are then split further.  The factorization equals sympy's."""
+    import sympy
+
+    x = sympy.symbols("x")
+    rng = random.Random(seed)
+    fs = []
+    while len(fs) < k:
+        co = [rng.randint(-20, 20) for _ in range(deg)] + [1]
+        f = sympy.Poly(list(reversed(co)), x)
+        if f.is_irreducible and all(f != g for g in fs):
+            fs.append(f)
+    prod = fs[0]
+    for f in fs[1:]:
+        prod = prod * f
+    p = P([int(c) for c in reversed(prod.all_coeffs())])
+    res = factor(p)
+    assert res.certificate
+    want = sorted([int(c) for c in reversed(f.all_coeffs())] for f in fs)
+    assert sorted(list(g.coeffs) for g, _ in res.factors) == want
+    assert res.stats.n >= 48
