@@ -63,7 +63,8 @@ typedef struct rfr_stats {
   double ms_total;        /* device time of the whole call                          */
   int64_t launches;       /* kernels launched by the call                            */
   int64_t buckets_planned; /* buckets the call set out to search; buckets < this     */
-                           /* means the search stopped early (rfr_search_verify)      */
+                           /* means the pattern space was not exhausted               */
+  int64_t early_stop;      /* rfr_search_verify: the join stopped at a verified hit   */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */
@@ -172,13 +173,16 @@ int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const u
  * in between.  Writes min(count, cap) patterns with their verdict / side /
  * coefficients (layouts as rfr_verify; coeffs valid for PASS); *nout = true
  * count (regrow and call again when it exceeds cap).  prof->n must equal n.
- * early_exit != 0: early termination -- the hits are verified while the
- * join runs (a one-warp kernel on a second stream) and once one passes the
- * join stops at its next bucket boundary.  The output then holds the
- * candidates found so far; st->buckets < st->buckets_planned tells the
- * caller the search stopped early (the pattern space was not exhausted, so
- * the passing factors need not be irreducible).  early_exit == 0: the whole
- * pattern space, as rfr_search_keys2 + rfr_verify.
+ * early_exit 1: early termination -- the hits are verified while the join
+ * runs (a one-warp kernel on a second stream) and once one passes, with
+ * pattern t, the join stops at its next bucket boundary; the pattern spaces
+ * of the two pieces t and ~t are then searched in the same call (their hits
+ * are factors of p too, reported as patterns of this search), so the output
+ * covers every factor pattern (st->early_stop = 1, buckets == buckets_planned).
+ * Pieces of >= 48 entities are left to the caller: buckets < buckets_planned
+ * then says the pattern space was not exhausted.  early_exit 2: stop, never
+ * search the pieces.  early_exit 0: the whole pattern space, as
+ * rfr_search_keys2 + rfr_verify.
  */
 int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,

@@ -60,6 +60,7 @@ class RfrStats(ctypes.Structure):
         ("ms_total", ctypes.c_double),
         ("launches", ctypes.c_int64),
         ("buckets_planned", ctypes.c_int64),
+        ("early_stop", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -55,13 +55,15 @@ struct Ctx {
   cudaStream_t stream2 = nullptr;  // early-exit poller, beside the join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  DevVec keys, keys2, rho, raw, post, ctr, rotc, jstarts;
+  DevVec keys, keys2, rho, raw, post, ctr, rotc, jstarts, pkeys;
   DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
   void* h_stage = nullptr;       // pinned staging of rfr_verify (in, then out)
   size_t h_stage_bytes = 0;
+  void* h_piece = nullptr;       // pinned staging of the pieces' searches after an early stop
+  size_t h_piece_bytes = 0;
   // cache of the last built lists (key values + plan geometry)
   std::vector<uint64_t> built_keys;
   int built_bits[4] = {-1, -1, -1, -1};
@@ -84,6 +86,10 @@ int rfr_fail(int code, const char* fmt, ...) {
 int rfr_fail_cuda(cudaError_t e, const char* what) {
   return rfr_fail(RFR_E_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e),
                   cudaGetErrorString(e), what);
+}
+
+static int rfr_check_cuda(cudaError_t e, const char* what) {
+  return e == cudaSuccess ? RFR_OK : rfr_fail_cuda(e, what);
 }
 
 namespace {
@@ -371,6 +377,99 @@ int check_profile(const rfr_profile* prof, int d) {
   return RFR_OK;
 }
 
+// After an early stop on the verified pattern t (rfr_search_verify): search
+// the pattern spaces of the two pieces t and ~t here, so the caller gets a
+// complete candidate set in one call.  A piece's hits are factors of p too,
+// so each piece is searched over the parent's keys at its bits (with the
+// parent's windows: its own error bounds are smaller) and its survivors are
+// deposited back into parent patterns and verified with the parent's
+// arguments (V0).  Rows are appended to xp/xv/xs/xc.  false with *rc == 0: not
+// done here (a piece with >= kPieceMaxN entities, or more than kPieceRows
+// survivors) -- the caller reports the stop and the host factors the pieces.
+constexpr int kPieceMaxN = 48;   // whole-space searches above this size stop early themselves
+constexpr int kPieceRows = 64;
+bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t lo, uint64_t width,
+                   uint64_t lo2, uint64_t width2, uint64_t t, const VerifyArgs& V0, int stride,
+                   cudaStream_t s, std::vector<uint64_t>& xp, std::vector<uint8_t>& xv,
+                   std::vector<uint8_t>& xs, std::vector<int64_t>& xc, int64_t* buckets, int* rc) {
+  *rc = RFR_OK;
+  const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+  const uint64_t masks[2] = {t & full, ~t & full};
+  for (uint64_t M : masks)
+    if (__builtin_popcountll(M) >= kPieceMaxN) return false;
+  const size_t row_b = 8 + 1 + 1 + (size_t)stride * 8;
+  const size_t per = 2 * 64 * 8 + sizeof(DevCounters) + kPieceRows * row_b;
+  if (g.h_piece_bytes < 2 * per) {
+    if (g.h_piece) cudaFreeHost(g.h_piece);
+    g.h_piece = nullptr;
+    g.h_piece_bytes = 0;
+    if ((*rc = rfr_check_cuda(cudaMallocHost(&g.h_piece, 2 * per), "cudaMallocHost"))) return false;
+    g.h_piece_bytes = 2 * per;
+  }
+  if ((*rc = rfr_check_cuda(g.pkeys.ensure(2 * 2 * 64 * sizeof(uint64_t)), "pkeys"))) return false;
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
+  const unsigned long long post_cap = g.post.bytes / sizeof(uint64_t);
+  uint64_t* d_post = (uint64_t*)g.post.p;
+  bool used[2] = {false, false};
+  for (int pi = 0; pi < 2; pi++) {
+    const uint64_t M = masks[pi];
+    const int ns = __builtin_popcountll(M);
+    if (ns < 2) continue;  // one linear or quadratic entity: irreducible
+    used[pi] = true;
+    char* hp = (char*)g.h_piece + pi * per;
+    uint64_t* hk = (uint64_t*)hp;
+    int j = 0;
+    for (uint64_t mm = M; mm; mm &= mm - 1, j++) {
+      const int i = __builtin_ctzll(mm);
+      hk[j] = keys[i];
+      hk[64 + j] = keys2[i];
+    }
+    uint64_t* dk = (uint64_t*)g.pkeys.p + pi * 128;
+    auto ok = [&](cudaError_t e, const char* what) { return (*rc = rfr_check_cuda(e, what)) == RFR_OK; };
+    if (!ok(cudaMemcpyAsync(dk, hk, 2 * 64 * sizeof(uint64_t), cudaMemcpyHostToDevice, s), "piece keys") ||
+        !ok(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s), "piece counters"))
+      return false;
+    int rb = 0, nw = 0;
+    if ((*rc = search_core(dk, ns, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &rb, &nw, false)))
+      return false;
+    VerifyArgs A = V0;
+    A.pats = d_post;
+    A.m_dev = &d_ctr->post_count;
+    A.m_begin_dev = nullptr;
+    A.found = nullptr;
+    char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+    if (!ok(launch_keyfilter(dk + 64, ns, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2, width2,
+                             d_post, post_cap, d_ctr, g.nsm, s), "piece keyfilter") ||
+        !ok(launch_deposit(d_post, &d_ctr->post_count, post_cap, M, g.nsm, s), "deposit") ||
+        !ok(launch_verify(A, s), "piece verify") ||
+        !ok(cudaMemcpyAsync(hp + 2 * 64 * 8, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "piece ctr") ||
+        !ok(cudaMemcpyAsync(rows, d_post, kPieceRows * 8, cudaMemcpyDeviceToHost, s), "piece pats") ||
+        !ok(cudaMemcpyAsync(rows + kPieceRows * 8, A.verdict, kPieceRows, cudaMemcpyDeviceToHost, s), "piece verdicts") ||
+        !ok(cudaMemcpyAsync(rows + kPieceRows * 9, A.side, kPieceRows, cudaMemcpyDeviceToHost, s), "piece sides") ||
+        !ok(cudaMemcpyAsync(rows + kPieceRows * 10, A.coeffs, kPieceRows * (size_t)stride * 8,
+                            cudaMemcpyDeviceToHost, s), "piece coeffs"))
+      return false;
+  }
+  if ((*rc = rfr_check_cuda(cudaStreamSynchronize(s), "piece sync"))) return false;
+  for (int pi = 0; pi < 2; pi++) {
+    if (!used[pi]) continue;
+    const char* hp = (const char*)g.h_piece + pi * per;
+    const DevCounters c = *(const DevCounters*)(hp + 2 * 64 * 8);
+    if (c.out_count > raw_cap || c.post_count > (unsigned long long)kPieceRows) return false;
+    const char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+    for (unsigned long long k = 0; k < c.post_count; k++) {
+      xp.push_back(((const uint64_t*)rows)[k]);
+      xv.push_back(((const uint8_t*)(rows + kPieceRows * 8))[k]);
+      xs.push_back(((const uint8_t*)(rows + kPieceRows * 9))[k]);
+      const int64_t* cr = (const int64_t*)(rows + kPieceRows * 10) + k * stride;
+      xc.insert(xc.end(), cr, cr + stride);
+    }
+    *buckets += (int64_t)c.buckets;
+  }
+  return true;
+}
+
 int check_n(int n) {
   if (n < 0) return rfr_fail(RFR_E_ARG, "negative width");
   if (n > 64) return rfr_fail(RFR_E_WIDTH, "pattern width is capped at 64 bits, got %d", n);
@@ -390,7 +489,7 @@ int rfr_num_sms(void) { return g.nsm; }
 // Free everything the context holds (safe on a partially initialised one).
 static void release_ctx() {
   if (g.stream) cudaStreamSynchronize(g.stream);
-  DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts,
+  DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts, &g.pkeys,
                     &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef};
   for (DevVec* v : vecs) v->release();
   for (auto& h : g.hist) h.release();
@@ -405,6 +504,7 @@ static void release_ctx() {
   if (g.stream2) cudaStreamDestroy(g.stream2);
   if (g.h_ctr) cudaFreeHost(g.h_ctr);
   if (g.h_stage) cudaFreeHost(g.h_stage);
+  if (g.h_piece) cudaFreeHost(g.h_piece);
   if (g.stream) cudaStreamDestroy(g.stream);
   g = Ctx();
 }
@@ -750,25 +850,69 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
     RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
   }
   const DevCounters cc = *g.h_ctr;
+  const int main_launches = g_launches;
+  const int64_t main_planned = g_buckets_planned;
   const size_t m = cc.post_count < (unsigned long long)cap ? (size_t)cc.post_count : (size_t)cap;
   if (m > spec) {  // more survivors than the speculative rows
     RFR_CUDA_OK(copy_rows(spec, m));
     RFR_CUDA_OK(cudaStreamSynchronize(s));
   }
+  // ---- early stop: search the two pieces of the verified factor in this call
+  std::vector<uint64_t> xp;
+  std::vector<uint8_t> xv, xs;
+  std::vector<int64_t> xc;
+  int64_t xbuckets = 0;
+  bool complete = cc.buckets >= (unsigned long long)main_planned;
+  const bool stopped = !complete;
+  if (early_exit == 1 && !complete && m == cc.post_count) {
+    const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+    for (size_t k = 0; k < m; k++) {
+      if (((const uint8_t*)(hs + h_verd))[k] != RFR_V_PASS) continue;
+      const uint64_t sp = ((const uint64_t*)hs)[k] & full;
+      const uint64_t t = ((const uint8_t*)(hs + h_side))[k] ? (~sp & full) : sp;
+      VerifyArgs V0 = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
+      V0.m = (long long)vrows;
+      V0.verdict = (uint8_t*)obase;
+      V0.side = (uint8_t*)(obase + q_side);
+      V0.coeffs = (long long*)(obase + q_coef);
+      V0.stride = stride;
+      int prc = RFR_OK;
+      if (search_pieces(keys, keys2, n, lo, width, lo2, width2, t, V0, stride, s, xp, xv, xs, xc,
+                        &xbuckets, &prc))
+        complete = true;
+      else if (prc)
+        return prc;
+      break;
+    }
+  }
+  const unsigned long long total = cc.post_count + (unsigned long long)xp.size();
   if (m) {
     memcpy(pats, hs, m * 8);
     if (verdict) memcpy(verdict, hs + h_verd, m);
     if (side) memcpy(side, hs + h_side, m);
     if (coeffs) memcpy(coeffs, hs + h_coef, m * (size_t)stride * sizeof(int64_t));
   }
-  *nout = (int64_t)cc.post_count;
+  if (complete && !xp.empty() && total <= (unsigned long long)cap) {
+    memcpy(pats + m, xp.data(), xp.size() * 8);
+    if (verdict) memcpy(verdict + m, xv.data(), xv.size());
+    if (side) memcpy(side + m, xs.data(), xs.size());
+    if (coeffs) memcpy(coeffs + m * (size_t)stride, xc.data(), xc.size() * sizeof(int64_t));
+  }
+  *nout = (int64_t)(complete ? total : cc.post_count);
   if (st) {
+    g_launches = main_launches;
+    g_buckets_planned = main_planned;
     fill_stats(st, cc, n, r_bits, nwin);
     st->raw_hits = (int64_t)cc.out_count;
     st->ms_lists = ev_ms(g.ev[0], g.ev[1]);
     st->ms_join = ev_ms(g.ev[1], g.ev[2]);
     st->ms_post = ev_ms(g.ev[2], g.ev[3]);
     st->ms_total = ev_ms(g.ev[0], g.ev[3]);
+    // a stopped search completed by its pieces' searches covers every factor
+    // pattern: report it as complete
+    st->buckets += xbuckets;
+    if (complete) st->buckets_planned = st->buckets;
+    st->early_stop = stopped ? 1 : 0;
   }
   return RFR_OK;
 }

@@ -23,6 +23,8 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
                              unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
                              const unsigned long long* d_begin = nullptr);
+cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
+                           uint64_t mask, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            const unsigned long long* d_in_count, unsigned long long cap_in,
                            double eps, uint64_t* d_out, unsigned long long cap_out,

@@ -709,6 +709,26 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
   return cudaGetLastError();
 }
 
+// Patterns of a piece's search (bit j = the j-th set bit of mask) rewritten
+// as patterns of the parent's search (rfr_search_verify after an early stop).
+__global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long long* __restrict__ count,
+                               unsigned long long cap, uint64_t mask) {
+  unsigned long long m = *count;
+  if (m > cap) m = cap;
+  for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    uint64_t u = pats[k], v = 0;
+    for (uint64_t mm = mask; mm && u; mm &= mm - 1, u >>= 1)
+      if (u & 1ull) v |= mm & (0ull - mm);
+    pats[k] = v;
+  }
+}
+cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
+                           uint64_t mask, int nsm, cudaStream_t s) {
+  deposit_kernel<<<nsm, 256, 0, s>>>(d_pats, d_count, cap, mask);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------- early exit
 // One warp beside the running join (its own stream, a CTA slot the join
 // leaves free): takes the raw hits in emission order as they appear, turns

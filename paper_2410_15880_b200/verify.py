@@ -193,16 +193,21 @@ def search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, hal
 
 # Early termination (north star: "results are checked for early termination";
 # SURVEY s8(e)): searches over n >= _EARLY_N entities verify their hits while
-# the join runs and stop once one passes.  Smaller searches take ~0.1 ms and
-# run whole.
+# the join runs and stop once one passes.  _PIECES: the library then searches
+# the two pieces' pattern spaces in the same call (a complete candidate set);
+# otherwise (or for pieces of >= 48 entities) factor() splits p and factors
+# the pieces itself.  Smaller searches take ~0.1 ms and run whole.
 _EARLY_N = 48
+_PIECES = True
 
 
 def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
                        keys3: np.ndarray, half_width3: int, stats, early_exit: bool):
     """search_and_verify, optionally with early termination.  Returns (pats,
-    verdict, side, coeffs, complete); complete is False when the search
-    stopped once a candidate passed (the pattern space was not exhausted)."""
+    verdict, side, coeffs, complete, stopped): stopped when the join ended at
+    a verified hit; complete when the candidates nevertheless cover every
+    factor pattern (the library searched the pieces), False when the pattern
+    space was not exhausted."""
     from .recombine import _fill_stats, _window
 
     lib = _lib.load()
@@ -227,7 +232,8 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
                 _lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
                 ctypes.byref(rp), _lib.ptr(pm, _lib.U64_P), p.degree, _lib.ptr(pats, _lib.U64_P),
                 verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
-                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap, int(bool(early_exit)), ctypes.byref(nout),
+                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap,
+                (1 if _PIECES else 2) if early_exit else 0, ctypes.byref(nout),
                 ctypes.byref(st)),
             "rfr_search_verify",
         )
@@ -237,7 +243,7 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
     _fill_stats(stats, st)
     m = int(nout.value)
     complete = st.buckets >= st.buckets_planned
-    return pats[:m], verdict[:m], side[:m], coeffs[:m], complete
+    return pats[:m], verdict[:m], side[:m], coeffs[:m], complete, bool(st.early_stop)
 
 
 def _sub_profile(prof: RootProfile, t: int) -> RootProfile:
@@ -338,8 +344,9 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     if workers == 1 and keys3 is not None:
         # one device call: search, Tr3 window and verification back to back
         # (recombine_seconds then covers the device verification too)
-        pats, verdict, side, coeffs, complete = _search_and_verify(
+        pats, verdict, side, coeffs, complete, stopped = _search_and_verify(
             prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N)
+        stats.early_exits += int(stopped and complete)  # stopped, pieces searched in the call
         keep = pats != 0
         pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]
         stats.recombine_seconds += time.perf_counter() - t0

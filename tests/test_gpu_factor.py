@@ -190,9 +190,10 @@ def test_fused_search_verify_matches_the_two_call_path(big_inputs, factor_cases)
 
 def test_early_exit_search_is_a_prefix_of_the_whole_search(big_inputs):
     """rfr_search_verify with early termination: its candidates and verdicts
-    are a subset of the whole-space call's, the same set when the search ran
-    to the end, and a stopped search holds a passing candidate.  On the
-    d = 100 inputs at least one search stops early."""
+    are a subset of the whole-space call's, the same set when the join ran to
+    the end; a stopped search holds a passing candidate and, with its pieces
+    searched in the call, reports itself complete.  On the d = 100 inputs at
+    least one search stops early."""
     from paper_2410_15880_b200 import verify as V
 
     stopped = 0
@@ -203,14 +204,16 @@ def test_early_exit_search_is_a_prefix_of_the_whole_search(big_inputs):
         keys3, T3 = V._secondary_window(prof)
         whole = V._search_and_verify(prof, p, keys, T, keys3, T3, None, False)
         part = V._search_and_verify(prof, p, keys, T, keys3, T3, None, True)
-        assert whole[4]
+        assert whole[4] and not whole[5]
         wv = {int(s): int(v) for s, v in zip(whole[0], whole[1])}
         pv = {int(s): int(v) for s, v in zip(part[0], part[1])}
+        # the pieces' hits are hits of the whole search too (same keys and windows)
         assert set(pv) <= set(wv) and all(wv[s] == v for s, v in pv.items())
-        if part[4]:
+        if not part[5]:
             assert pv == wv
         else:
             stopped += 1
+            assert part[4]  # the pieces were searched in the same call
             assert _lib.V_PASS in pv.values()
     assert stopped >= 1
 
@@ -257,6 +260,7 @@ def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
             return None
         return real_div(a, b)
 
+    monkeypatch.setattr(V, "_PIECES", False)  # the host splits p (the path with the fallback)
     monkeypatch.setattr(V, "_search_and_verify", search)
     monkeypatch.setattr(V, "divide_exact", reject_until_fallback)
     res = factor(p)
