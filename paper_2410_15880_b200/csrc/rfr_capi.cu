@@ -232,6 +232,17 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
                 int* nwin, bool time_it, const EarlyExit* ee = nullptr) {
   g_launches = 0;
   g_buckets_planned = 0;
+  if (nshards == 1 && n >= 2 && n <= kExhaustiveMaxN) {
+    // small search: every folded pattern in one launch (same hit set as the join)
+    *nwin = 1;
+    *r_bits = 0;
+    if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
+    if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
+    RFR_CUDA_OK(launch_exhaustive(d_keys, n, lo, width, d_out, cap, (DevCounters*)g.ctr.p, s));
+    g_launches = 1;
+    if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
+    return RFR_OK;
+  }
   std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
   *nwin = (int)wins.size();
   JoinPlan P0;

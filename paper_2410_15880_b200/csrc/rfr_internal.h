@@ -23,6 +23,10 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
                              unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
                              const unsigned long long* d_begin = nullptr);
+constexpr int kExhaustiveMaxN = 27;  // search_core: exhaustive kernel at or below this width (break-even with the join ~28)
+cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
+                              uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
+                              cudaStream_t s);
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,

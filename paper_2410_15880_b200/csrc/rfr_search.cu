@@ -709,6 +709,107 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------- exhaustive search
+// Small searches (n <= kExhaustiveMaxN, one shard): every folded pattern t <
+// 2^(n-1) in Gray-code order, one key added or removed per step, the window
+// test (sum - lo) mod 2^64 <= width on each -- the same hit set as the
+// quarter-list join (same space, same test), in one launch instead of the
+// list build, the start search and a join that would keep only a few CTAs
+// busy.  Thread T walks patterns [T 2^b, (T+1) 2^b).
+__global__ void __launch_bounds__(256) exhaustive_kernel(const uint64_t* __restrict__ keys, int n,
+                                                         uint64_t lo, uint64_t width, int b,
+                                                         uint64_t* __restrict__ out,
+                                                         unsigned long long cap, DevCounters* ctr) {
+  __shared__ uint64_t sk[64];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = keys[i];
+  __syncthreads();
+  const int m = n - 1;
+  const uint64_t T = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (T == 0) atomicAdd(&ctr->queries, 1ull << m);  // patterns tested (stats)
+  if ((T << b) >> m) return;  // past 2^m patterns
+  const uint64_t i0 = T << b;
+  // sum is kept shifted by -lo: pattern g is a hit iff sum <= width
+  uint64_t g = i0 ^ (i0 >> 1), sum = 0ull - lo;
+  for (uint64_t u = g; u; u &= u - 1) sum += sk[__ffsll((long long)u) - 1];
+  auto hit = [&](uint64_t pat, uint64_t sm) {
+    if (sm <= width) {
+      const unsigned long long k = atomicAdd(&ctr->out_count, 1ull);
+      if (k < cap) out[k] = pat;
+    }
+  };
+  // toggle bit j of g and move sum by +-key (the key's sign follows the bit)
+  auto step = [&](int j, uint64_t key) {
+    g ^= 1ull << j;
+    sum += ((g >> j) & 1ull) ? key : 0ull - key;
+    hit(g, sum);
+  };
+  if (b < 4) {  // tiny spaces: plain Gray-code walk
+    hit(g, sum);
+    for (uint32_t i = 1; i < (1u << b); i++) step(__ffs(i) - 1, sk[__ffs(i) - 1]);
+    return;
+  }
+  // b >= 4: blocks of 16 patterns.  Within a block the toggled bits are fixed
+  // (0 1 0 2 0 1 0 3 0 1 0 2 0 1 0) and each bit's toggles alternate in sign,
+  // so the block runs on 8 signed deltas set up at its start: one 64-bit add
+  // and one compare per pattern, no branch; a block with a hit is replayed
+  // pattern by pattern (rare).
+  const uint64_t k0 = sk[0], k1 = sk[1], k2 = sk[2], k3 = sk[3];
+  const uint32_t nblk = 1u << (b - 4);
+  for (uint32_t blk = 0;;) {
+    const uint64_t p0 = (g & 1ull) ? 0ull - k0 : k0, m0 = 0ull - p0;
+    const uint64_t p1 = (g & 2ull) ? 0ull - k1 : k1, m1 = 0ull - p1;
+    const uint64_t p2 = (g & 4ull) ? 0ull - k2 : k2, m2 = 0ull - p2;
+    const uint64_t p3 = (g & 8ull) ? 0ull - k3 : k3;
+    uint64_t x = sum;
+    bool any = x <= width;
+    x += p0; any |= x <= width;  // bit 0
+    x += p1; any |= x <= width;  // bit 1
+    x += m0; any |= x <= width;  // bit 0
+    x += p2; any |= x <= width;  // bit 2
+    x += p0; any |= x <= width;
+    x += m1; any |= x <= width;
+    x += m0; any |= x <= width;
+    x += p3; any |= x <= width;  // bit 3
+    x += p0; any |= x <= width;
+    x += p1; any |= x <= width;
+    x += m0; any |= x <= width;
+    x += m2; any |= x <= width;
+    x += p0; any |= x <= width;
+    x += m1; any |= x <= width;
+    x += m0; any |= x <= width;
+    if (any) {  // replay the block from its start, emitting each hit
+      uint64_t gg = g, ss = sum;
+      hit(gg, ss);
+      for (uint32_t i = 1; i < 16; i++) {
+        const int j = __ffs(i) - 1;
+        const uint64_t key = j == 0 ? k0 : j == 1 ? k1 : j == 2 ? k2 : k3;
+        gg ^= 1ull << j;
+        ss += ((gg >> j) & 1ull) ? key : 0ull - key;
+        hit(gg, ss);
+      }
+    }
+    g ^= 8ull;  // the block's last pattern differs from its first in bit 3
+    sum = x;
+    if (++blk == nblk) break;
+    const int j = 4 + __ffs(blk) - 1;  // first pattern of the next block
+    const uint64_t key = sk[j];
+    g ^= 1ull << j;
+    sum += ((g >> j) & 1ull) ? key : 0ull - key;
+  }
+}
+cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
+                              uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
+                              cudaStream_t s) {
+  const int m = n - 1;
+  // ~2^18 threads of 2^b patterns each; b >= 4 when the space allows (16-pattern blocks)
+  int b = m > 18 ? m - 18 : 0;
+  if (b < 4) b = m < 4 ? m : 4;
+  const uint64_t threads = 1ull << (m - b);
+  exhaustive_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_keys, n, lo, width, b, d_out, cap,
+                                                                     d_ctr);
+  return cudaGetLastError();
+}
+
 // Patterns of a piece's search (bit j = the j-th set bit of mask) rewritten
 // as patterns of the parent's search (rfr_search_verify after an early stop).
 __global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long long* __restrict__ count,
