@@ -232,7 +232,9 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
                 int* nwin, bool time_it, const EarlyExit* ee = nullptr) {
   g_launches = 0;
   g_buckets_planned = 0;
-  if (nshards == 1 && n >= 2 && n <= kExhaustiveMaxN) {
+  // RFR_FORCE_JOIN (tests): keep small searches on the quarter-list join so
+  // the oracle parity tests cover both paths
+  if (nshards == 1 && n >= 2 && n <= kExhaustiveMaxN && !getenv("RFR_FORCE_JOIN")) {
     // small search: every folded pattern in one launch (same hit set as the join)
     *nwin = 1;
     *r_bits = 0;

@@ -23,7 +23,16 @@ pytestmark = pytest.mark.gpu
 TWO64 = 1 << 64
 
 
-def test_recombine_e_matches_reference_candidate_sets(recombine_cases):
+@pytest.fixture(params=["exhaustive", "join"])
+def search_path(request, monkeypatch):
+    """Searches of n <= 27 run the exhaustive kernel; the parity tests run
+    each case on the quarter-list join as well (RFR_FORCE_JOIN)."""
+    if request.param == "join":
+        monkeypatch.setenv("RFR_FORCE_JOIN", "1")
+    return request.param
+
+
+def test_recombine_e_matches_reference_candidate_sets(recombine_cases, search_path):
     for case in recombine_cases:
         got = recombine_e(RhoVector.from_values(rho_of(case)), case["eps"]).patterns
         assert got == frozenset(case["patterns"]), case["tag"]
@@ -61,7 +70,7 @@ def test_recombine_e_stats_and_shards(recombine_cases):
         assert parallel_recombine_e(rho, case["eps"], g).patterns == whole
 
 
-def test_recombine_e_against_c_oracle_random():
+def test_recombine_e_against_c_oracle_random(search_path):
     rng = random.Random(77)
     for _ in range(40):
         n = rng.randint(1, 24)
@@ -76,7 +85,7 @@ def _oracle_keys(keys, T):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_search_keys_matches_window_oracle(seed):
+def test_search_keys_matches_window_oracle(seed, search_path):
     rng = random.Random(seed)
     for _ in range(12):
         n = rng.randint(1, 26)
@@ -88,7 +97,7 @@ def test_search_keys_matches_window_oracle(seed):
 
 
 @pytest.mark.parametrize("seed", range(4))
-def test_search_keys2_matches_two_window_oracle(seed):
+def test_search_keys2_matches_two_window_oracle(seed, search_path):
     """rfr_search_keys2: the first-window set of the oracle, filtered by the
     second key window (computed here exactly on Python ints)."""
     rng = random.Random(100 + seed)
@@ -110,7 +119,7 @@ def test_search_keys2_matches_two_window_oracle(seed):
         assert np.array_equal(got, want), (n, T, T2)
 
 
-def test_search_keys_skewed_duplicates_match_oracle():
+def test_search_keys_skewed_duplicates_match_oracle(search_path):
     # heavy duplicates: few distinct keys drive buckets past their capacity
     rng = random.Random(9)
     for n in (12, 18, 22, 25):
