@@ -175,19 +175,25 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
   bool reject = false, host = false;
   for (int j = lane; j <= e; j += 32) {
     const ddv v = B.c[cur][j];
-    double rnd = nearbyint(v.hi);
-    double frac = (v.hi - rnd) + v.lo;
+    // nearest integer of hi + lo, kept exactly in int64: above 2^53 hi is
+    // itself an integer and lo may exceed 1/2 (a double cannot hold the
+    // 53..62-bit integer, and rounding hi alone would leave lo's whole part
+    // in the "fraction" -- rejecting true factors with large coefficients)
+    const bool big = fabs(v.hi) >= 4.611686018427388e18;  // beyond 2^62: the host decides
+    const double rh = nearbyint(v.hi), rl = nearbyint(v.lo);
+    double frac = (v.hi - rh) + (v.lo - rl);  // |frac| <= 1
+    long long qv = big ? 0 : (long long)rh + (long long)rl;
     if (frac > 0.5) {
-      rnd += 1.0;
+      qv += 1;
       frac -= 1.0;
     } else if (frac < -0.5) {
-      rnd -= 1.0;
+      qv -= 1;
       frac += 1.0;
     }
     const double bound = (B.magp[cur][j] - B.mag[cur][j]) + B.mag[cur][j] * arith + 1e-300;
-    if (bound > 0.25 || fabs(rnd) >= 4.611686018427388e18) host = true;
+    if (bound > 0.25 || big) host = true;
     else if (fabs(frac) > 2.0 * bound) reject = true;
-    B.q[j] = (long long)rnd;
+    B.q[j] = qv;
   }
   reject = __any_sync(0xffffffffu, reject);
   host = __any_sync(0xffffffffu, host);

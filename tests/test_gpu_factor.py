@@ -294,3 +294,31 @@ def test_early_exit_with_several_factors_matches_sympy(k, deg, seed):
     want = sorted([int(c) for c in reversed(f.all_coeffs())] for f in fs)
     assert sorted(list(g.coeffs) for g, _ in res.factors) == want
     assert res.stats.n >= 48
+
+
+@pytest.mark.parametrize("degs,lead,seed", [((40, 60), 1, 31), ((30, 34, 40), 1, 32), ((46, 50), 3, 33)])
+def test_early_exit_uneven_and_non_monic_products_match_sympy(degs, lead, seed):
+    """Early termination on products with unequal factor degrees (pieces of
+    different sizes, one of them possibly >= 48 entities: the host splits it)
+    and on a non-monic product (monic transform first): same factorization
+    as sympy."""
+    import sympy
+
+    x = sympy.symbols("x")
+    rng = random.Random(seed)
+    fs = []
+    for k, deg in enumerate(degs):
+        while True:
+            co = [rng.randint(-15, 15) for _ in range(deg)] + [lead if k == 0 else 1]
+            f = sympy.Poly(list(reversed(co)), x)
+            if f.is_irreducible and f.primitive()[0] == 1 and all(f != g for g in fs):
+                fs.append(f)
+                break
+    prod = fs[0]
+    for f in fs[1:]:
+        prod = prod * f
+    p = P([int(c) for c in reversed(prod.all_coeffs())])
+    res = factor(p)
+    assert res.certificate
+    want = sorted([int(c) for c in reversed(f.all_coeffs())] for f in fs)
+    assert sorted(list(g.coeffs) for g, _ in res.factors) == want
