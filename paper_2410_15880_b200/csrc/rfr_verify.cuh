@@ -191,8 +191,13 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
       frac += 1.0;
     }
     const double bound = (B.magp[cur][j] - B.mag[cur][j]) + B.mag[cur][j] * arith + 1e-300;
+    // the bound rests on the roots' a-posteriori error estimate, which can be
+    // optimistic for moderately separated roots (seen 2x at d = 110): a
+    // coefficient just outside it goes to the exact host check; a rejection
+    // needs a clearly fractional coefficient (a false candidate has many)
     if (bound > 0.25 || big) host = true;
-    else if (fabs(frac) > 2.0 * bound) reject = true;
+    else if (fabs(frac) > fmax(2.0 * bound, 1e-9)) reject = true;
+    else if (fabs(frac) > 2.0 * bound) host = true;
     B.q[j] = qv;
   }
   reject = __any_sync(0xffffffffu, reject);

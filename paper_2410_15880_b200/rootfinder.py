@@ -86,6 +86,13 @@ class RootProfile:
     key_err2: int = field(default=0, repr=False, compare=False)
     key_err3: int = field(default=0, repr=False, compare=False)
     root_err: float = field(default=0.0, repr=False, compare=False)
+    # multiprecision roots (coefficients beyond double-double, e.g. the monic
+    # transform of a non-monic p): exact rational real roots by entity, (t, m)
+    # of each pair, and their error bound -- for host decisions on factors
+    # whose coefficients exceed what the double-double values can round
+    hp_real: tuple | None = field(default=None, repr=False, compare=False)
+    hp_pair: tuple | None = field(default=None, repr=False, compare=False)
+    hp_err: float = field(default=0.0, repr=False, compare=False)
 
     @property
     def r(self) -> int:
@@ -117,12 +124,22 @@ def _dd_frac(hi: float, lo: float) -> Fraction:
 
 
 def _initial_roots(coeffs: list[int]) -> np.ndarray:
-    """Seeds: eigenvalues of the companion matrix (numpy.roots)."""
+    """Seeds: eigenvalues of the companion matrix (numpy.roots).  Badly
+    scaled coefficients (a monic transform a^(d-1) p(x / a) of a non-monic p
+    spans ~d log2(a) bits) are balanced first: x = s y with s = 2^k ~
+    |c_0|^(1/d), the geometric mean of the root magnitudes, and the seeds
+    scaled back -- the polish converges from there instead of wandering."""
     d = len(coeffs) - 1
     if d == 1:
         return np.array([complex(-coeffs[0] / coeffs[1])])
-    c = np.array([float(a) for a in coeffs[::-1]], dtype=np.float64)
-    z = np.roots(c)
+    k = 0
+    c0 = next((abs(c) for c in coeffs if c), 1)
+    if max(abs(c) for c in coeffs).bit_length() > 200:
+        k = round((c0.bit_length() - 1) / d)
+    # coefficient of y^i after x = 2^k y (divided through by 2^(k d)): c_i 2^(k (i - d))
+    c = np.array([float(Fraction(a) / (Fraction(2) ** (k * (d - i))))
+                  for i, a in reversed(list(enumerate(coeffs)))], dtype=np.float64)
+    z = np.roots(c) * float(2.0 ** k)
     if len(z) != d or not np.all(np.isfinite(z)):
         raise NonConvergence("numpy.roots failed to seed the root polish")
     return z
@@ -205,6 +222,7 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
             return None
         err = np.zeros(d)
         rh, rl, ih, il = (np.zeros(d) for _ in range(4))
+        exact = []
         for i in range(d):
             p, dp = evalp(z[i])
             e = 2 * (abs(p) + abs(z[i]) * mpmath.mpf(2) ** (bits - prec + 8)) / abs(dp)
@@ -213,7 +231,8 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
             im = _mpf_to_fraction(z[i].imag)
             rh[i], rl[i] = _dd_split(re)
             ih[i], il[i] = _dd_split(im)
-        return rh, rl, ih, il, err
+            exact.append((re, im))
+        return rh, rl, ih, il, err, exact
 
 
 def _mpf_to_fraction(x) -> Fraction:
@@ -227,6 +246,12 @@ def _mpf_to_fraction(x) -> Fraction:
 def hp_roots(p: IntPolynomial):
     """All roots of a monic square-free p to ~2^-100, with error bounds.
     Returns (re_hi, re_lo, im_hi, im_lo, err)."""
+    return _hp_roots(p)[:5]
+
+
+def _hp_roots(p: IntPolynomial):
+    """hp_roots plus the exact rational (re, im) of every root when the
+    multiprecision polish ran (else None)."""
     if not p.is_monic():
         raise ValueError("hp_roots expects a monic polynomial")
     coeffs = list(p.coeffs)
@@ -237,6 +262,8 @@ def hp_roots(p: IntPolynomial):
     res = None
     if max(abs(c) for c in coeffs).bit_length() <= 100:
         res = _polish_dd(coeffs, z0)
+        if res is not None:
+            res = tuple(res) + (None,)
     if res is None:
         res = _polish_mp(coeffs, z0)
     if res is None:
@@ -272,18 +299,26 @@ def _pair_up(re_hi, re_lo, im_hi, im_lo, err):
 def hp_profile(p: IntPolynomial) -> RootProfile:
     """High-precision profile of a monic square-free p: rho, perm, double-
     double entities, the 64-bit keys in rho order and their error bounds."""
-    re_hi, re_lo, im_hi, im_lo, err = hp_roots(p)
+    re_hi, re_lo, im_hi, im_lo, err, exact = _hp_roots(p)
     reals, pairs = _pair_up(re_hi, re_lo, im_hi, im_lo, err)
     # (kind, R = first power sum, tau = second, errR, errTau, data, p3 = third, errP3)
     ents = []
+    ex_vals = []  # per entity, from the multiprecision roots: u, or (t, m) of a pair
     # exact rationals of the double-double values
     for i in reals:
+        ex_vals.append(exact[i][0] if exact is not None else None)
         u = _dd_frac(re_hi[i], re_lo[i])
         du = float(err[i])
         au = abs(float(u))
         ents.append(("r", u, u * u, du, 2 * au * du + du * du, i, u * u * u,
                      3 * au * au * du + 3 * au * du * du + du ** 3))
     for a, b in pairs:
+        if exact is not None:
+            xre = (exact[a][0] + exact[b][0]) / 2
+            xim = (exact[a][1] - exact[b][1]) / 2
+            ex_vals.append((2 * xre, xre * xre + xim * xim))
+        else:
+            ex_vals.append(None)
         # symmetrise: z = (z_a + conj z_b) / 2
         re = (_dd_frac(re_hi[a], re_lo[a]) + _dd_frac(re_hi[b], re_lo[b])) / 2
         im = (_dd_frac(im_hi[a], im_lo[a]) - _dd_frac(im_hi[b], im_lo[b])) / 2
@@ -361,6 +396,9 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         key_err2=int(math.ceil(e2)),
         key_err3=int(math.ceil(min(e3, 2.0**66))),
         root_err=root_err,
+        hp_real=tuple(ex_vals[k] for k in real_rows) if exact is not None else None,
+        hp_pair=tuple(ex_vals[k] for k in pair_rows) if exact is not None else None,
+        hp_err=float(max([0.0] + [float(e) for e in err])) if exact is not None else 0.0,
     )
 
 

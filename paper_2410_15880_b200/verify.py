@@ -39,6 +39,7 @@ from .polynomial import (
     IntPolynomial,
     _poly,
     divide_exact,
+    poly_gcd,
     monic_transform,
     monic_untransform_factor,
     square_free_decompose,
@@ -64,7 +65,7 @@ class FactorStats:
     rejected: int = 0
     recombine: RecombineStats = field(default_factory=RecombineStats)
     host_verified: int = 0
-    early_exits: int = 0  # searches stopped after a chunk with a verified factor
+    early_exits: int = 0  # searches stopped at a verified factor
 
 
 @dataclass(frozen=True)
@@ -272,6 +273,9 @@ def _sub_profile(prof: RootProfile, t: int) -> RootProfile:
         keys1=take(prof.keys1, idx), keys2=take(prof.keys2, idx), keys3=take(prof.keys3, idx),
         key_err1=prof.key_err1, key_err2=prof.key_err2, key_err3=prof.key_err3,
         root_err=prof.root_err,
+        hp_real=None if prof.hp_real is None else tuple(prof.hp_real[int(e)] for e in reals),
+        hp_pair=None if prof.hp_pair is None else tuple(prof.hp_pair[int(e)] for e in pairs),
+        hp_err=prof.hp_err,
     )
 
 
@@ -280,6 +284,23 @@ def _host_candidate(prof: RootProfile, p: IntPolynomial, t: int) -> IntPolynomia
     not decide (coefficients beyond 2^62 or a loose error bound): multiply
     out the double-double entities as Fractions, round, bound the error,
     and demand exact division (R/verify.py:141-155 semantics)."""
+    if prof.hp_real is not None:
+        # multiprecision roots (~bits + 160 bits): their products round the
+        # factor's coefficients even where double-double cannot (the monic
+        # transform of a non-monic p); exact division is the proof
+        coeffs = [Fraction(1)]
+        for i in range(prof.n):
+            if (t >> i) & 1:
+                ent = prof.perm[i]
+                if ent < prof.r:
+                    coeffs = _pmul(coeffs, [-prof.hp_real[ent], Fraction(1)])
+                else:
+                    tt, mm = prof.hp_pair[ent - prof.r]
+                    coeffs = _pmul(coeffs, [mm, -tt, Fraction(1)])
+        q = IntPolynomial([round(c) for c in coeffs])
+        if q.degree < 1 or not q.is_monic():
+            return None
+        return q if divide_exact(p, q) is not None else None
     coeffs = [Fraction(1)]
     mag = [1.0]
     magp = [1.0]
@@ -323,6 +344,38 @@ def _pmul(a, b):
     return out
 
 
+def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
+    """The irreducible factors as (entity pattern, polynomial) cells: the
+    partition of the entities that the found factor patterns generate.
+    found maps patterns to their (verified) factors of p.  Every irreducible
+    factor's entities lie inside or outside each found pattern, and the
+    candidate set (a whole search, or a stopped one plus its pieces'
+    searches) separates any two of them.  A pattern inside a cell splits it
+    by exact division; a partial overlap (rare) by a gcd.  After a stop the
+    pieces' patterns only imply some factors (t minus a pattern inside t),
+    which a greedy cover by minimal patterns would leave merged."""
+    cells = [(full, p)]
+    for t in sorted(found, key=lambda x: (bin(x).count("1"), x)):
+        q = found[t]
+        refined = []
+        for c, pc in cells:
+            inter = c & t
+            if inter == 0 or inter == c:
+                refined.append((c, pc))
+                continue
+            if inter == t:  # the pattern lies inside the cell: pc = q * (pc / q)
+                g, r = q, divide_exact(pc, q)
+            else:  # partial overlap: the common factor
+                g = poly_gcd(pc, q)
+                r = divide_exact(pc, g) if g.degree >= 1 else None
+            if r is None or g.degree < 1 or r.degree < 1:
+                refined.append((c, pc))
+                continue
+            refined += [(inter, g), (c & ~t, r)]
+        cells = refined
+    return cells
+
+
 def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
                              stats: FactorStats, prof: RootProfile | None = None,
                              early_exit: bool = True) -> list[IntPolynomial]:
@@ -340,7 +393,7 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     t0 = time.perf_counter()
     keys, T = _search_window(prof)
     keys3, T3 = _secondary_window(prof)
-    complete = True
+    complete, stopped = True, False
     if workers == 1 and keys3 is not None:
         # one device call: search, Tr3 window and verification back to back
         # (recombine_seconds then covers the device verification too)
@@ -406,34 +459,12 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     if not found:
         stats.verify_seconds += time.perf_counter() - t0
         return [p]
-    # atoms: minimal passing patterns (every true pattern is a disjoint union
-    # of them; the complement of a passing pattern passes too)
-    pats_all = set(found) | {(~t & full) for t in found}
-    covered = 0
-    atoms = []
-    for t in sorted(pats_all, key=lambda x: (bin(x).count("1"), x)):
-        if t and not (t & covered):
-            atoms.append(t)
-            covered |= t
-            if covered == full:
-                break
-    factors = []
-    rest = p
-    for k, a in enumerate(atoms):
-        if k == len(atoms) - 1 and covered == full and rest.degree >= 1:
-            break  # the last atom's factor is the cofactor of the others
-        q = found.get(a)
-        if q is None:
-            q = divide_exact(p, found[~a & full])
-        if q is None:
-            continue
-        quo = divide_exact(rest, q)
-        if quo is None:
-            continue
-        rest = quo
-        factors.append(q)
-    if rest.degree >= 1:
-        factors.append(rest)
+    cells = _factor_cells(found, p, full)
+    if stopped and any(pc.degree != selected_degree(c, prof) for c, pc in cells):
+        # inconsistent cells after a stopped search (not seen): search the whole space
+        stats.verify_seconds += time.perf_counter() - t0
+        return _factor_monic_squarefree(p, cfg, workers, stats, prof, early_exit=False)
+    factors = [pc for _, pc in cells]
     stats.verify_seconds += time.perf_counter() - t0
     return factors
 

@@ -322,3 +322,42 @@ def test_early_exit_uneven_and_non_monic_products_match_sympy(degs, lead, seed):
     assert res.certificate
     want = sorted([int(c) for c in reversed(f.all_coeffs())] for f in fs)
     assert sorted(list(g.coeffs) for g, _ in res.factors) == want
+
+
+def test_early_stop_with_four_factors_splits_implied_factors():
+    """Regression (randomised sweep vs sympy): x^2+57x+61 * a degree-15
+    (lead 2) * degree-23 * degree-60 product.  When the search stops on
+    t = f15*f23, the pieces' searches return f15 (inside t) and f2 (inside
+    ~t); f23 and f60 are only implied.  Repeated because whether the search
+    stops first depends on timing."""
+    import sympy
+
+    x = sympy.symbols("x")
+    fs = []
+    rng = random.Random(2 * 1000 + 20)  # scratch sweep seed 2, case 20
+    k = rng.choice([1, 2, 2, 3, 4])
+    total = rng.choice([20, 40, 60, 80, 100, 110])
+    degs, rem = [], total
+    for i in range(k - 1):
+        d = rng.randint(1, max(1, rem - (k - 1 - i)))
+        d = max(1, min(d, rem - (k - 1 - i)))
+        degs.append(d)
+        rem -= d
+    degs.append(max(1, rem))
+    cmax = rng.choice([1, 3, 10, 100, 1000])
+    prod = sympy.Poly(rng.choice([1, 1, 1, -1, 2, 6]), x)
+    for d in degs:
+        lead = rng.choice([1, 1, 1, -1, 2, 3, 5]) if rng.random() < 0.3 else 1
+        co = [rng.randint(-cmax, cmax) for _ in range(d)] + [lead]
+        if co[0] == 0:
+            co[0] = 1
+        f = sympy.Poly(list(reversed(co)), x)
+        fs.append(f)
+        prod = prod * f ** (2 if rng.random() < 0.15 else 1)
+    assert sorted(degs) == [2, 15, 23, 60]
+    p = P([int(c) for c in reversed(prod.all_coeffs())])
+    want = sorted(list(reversed([int(c) if f.LC() > 0 else -int(c) for c in f.all_coeffs()])) for f in fs)
+    for _ in range(8):
+        res = factor(p)
+        assert res.certificate
+        assert sorted(list(g.coeffs) for g, _ in res.factors) == want

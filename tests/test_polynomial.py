@@ -211,3 +211,27 @@ def test_squarefree_screen_never_accepts_a_square(q):
             accepted += 1
             assert square_free
     assert accepted > 30
+
+
+def test_factor_cells_split_implied_factors():
+    """The factor partition (verify._factor_cells): after an early stop the
+    candidates may hold t = f3*f4, f3 inside t, f1 inside ~t and nothing for
+    f4 or f2 by themselves; the cells are still the four factors (a greedy
+    cover by minimal patterns returned f1, f3 and f2*f4 here)."""
+    from paper_2410_15880_b200.polynomial import multiply
+    from paper_2410_15880_b200.verify import _factor_cells
+
+    f1, f2 = P([-2, 0, 1]), P([1, 1, 0, 1])           # entity bits 0-1, 2-4
+    f3, f4 = P([5, -1, 0, 0, 1]), P([3, 2, 1, 1, 0, 1])  # bits 5-8, 9-13
+    pats = {1: 0b11, 2: 0b11100, 3: 0b111100000, 4: 0b11111000000000}
+    full = (1 << 14) - 1
+    p = multiply(multiply(f1, f2), multiply(f3, f4))
+    found = {pats[3] | pats[4]: multiply(f3, f4), pats[3]: f3, pats[1]: f1}
+    cells = _factor_cells(found, p, full)
+    got = sorted((c, pc.coeffs) for c, pc in cells)
+    want = sorted((pats[i], f.coeffs) for i, f in ((1, f1), (2, f2), (3, f3), (4, f4)))
+    assert got == want
+    # a partial overlap (f2*f3 against f3*f4) is resolved by a gcd
+    found = {pats[2] | pats[3]: multiply(f2, f3), pats[3] | pats[4]: multiply(f3, f4)}
+    cells = sorted((c, pc.coeffs) for c, pc in _factor_cells(found, p, full))
+    assert (pats[3], f3.coeffs) in cells and (pats[2], f2.coeffs) in cells and (pats[4], f4.coeffs) in cells
