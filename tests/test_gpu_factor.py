@@ -361,3 +361,55 @@ def test_early_stop_with_four_factors_splits_implied_factors():
         res = factor(p)
         assert res.certificate
         assert sorted(list(g.coeffs) for g, _ in res.factors) == want
+
+
+def _random_product(seed0, case):
+    """The randomised sweep's input (scratch sweep, kept here): 1-4 random
+    factors of random degrees summing to 20..110, coefficients up to 1..1000,
+    some non-monic or negative leads, some squared, a small content."""
+    import sympy
+
+    x = sympy.symbols("x")
+    rng = random.Random(seed0 * 1000 + case)
+    k = rng.choice([1, 2, 2, 3, 4])
+    total = rng.choice([20, 40, 60, 80, 100, 110])
+    degs, rem = [], total
+    for i in range(k - 1):
+        d = rng.randint(1, max(1, rem - (k - 1 - i)))
+        d = max(1, min(d, rem - (k - 1 - i)))
+        degs.append(d)
+        rem -= d
+    degs.append(max(1, rem))
+    cmax = rng.choice([1, 3, 10, 100, 1000])
+    prod = sympy.Poly(rng.choice([1, 1, 1, -1, 2, 6]), x)
+    for d in degs:
+        lead = rng.choice([1, 1, 1, -1, 2, 3, 5]) if rng.random() < 0.3 else 1
+        co = [rng.randint(-cmax, cmax) for _ in range(d)] + [lead]
+        if co[0] == 0:
+            co[0] = 1
+        prod = prod * sympy.Poly(list(reversed(co)), x) ** (2 if rng.random() < 0.15 else 1)
+    want = []
+    for f, m in sympy.factor_list(prod.as_expr(), x)[1]:
+        co = [int(c) for c in reversed(sympy.Poly(f, x).all_coeffs())]
+        want.append(([-c for c in co] if co[-1] < 0 else co, m))
+    return P([int(c) for c in reversed(prod.all_coeffs())]), sorted(want)
+
+
+# inputs that failed during the sweep: an early stop leaving implied factors
+# merged (2/20, 10/5), a monic transform with 496-bit coefficients (7/7: seed
+# scaling, multiprecision host decisions), ill-conditioned roots (10/22, 12/29)
+@pytest.mark.parametrize("seed0,case", [(2, 20), (7, 7), (10, 5), (10, 22), (10, 24), (11, 17),
+                                        (12, 29)])
+def test_sweep_regressions_match_sympy(seed0, case):
+    p, want = _random_product(seed0, case)
+    for _ in range(3):  # early stops depend on timing
+        res = factor(p)
+        assert res.certificate
+        assert sorted((list(g.coeffs), m) for g, m in res.factors) == want
+
+
+def test_randomised_products_match_sympy():
+    for case in range(24):
+        p, want = _random_product(21, case)
+        res = factor(p)
+        assert res.certificate and sorted((list(g.coeffs), m) for g, m in res.factors) == want, case
