@@ -48,7 +48,13 @@ from .recombine import BACKENDS, RecombineStats, search_keys
 from .rootfinder import RootProfile, ToleranceConfig, hp_profile
 
 _STRIDE = 65  # smaller side degree <= 64
-KEY_SAFETY = 4  # window half-width = KEY_SAFETY * (summed key error bounds) + slack
+# window half-width = KEY_SAFETY * (summed key error bounds) + slack.  The
+# per-root bounds are a-posteriori estimates (2 |p| / |p'|) that ill-conditioned
+# roots were seen to exceed 2-4x (a randomised sweep: d = 110, and a Tr3 window
+# that dropped a true factor with 10^6 coefficients), so the margin is wide; a
+# wider window only admits more (cheaply rejected) raw hits.
+KEY_SAFETY = 16
+KEY_SAFETY3 = 64  # the Tr3 window is a filter in front of verification: wider still
 
 
 @dataclass
@@ -115,7 +121,7 @@ def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
     or (None, 0) for a profile without them."""
     if prof.keys3 is None:
         return None, 0
-    return prof.keys3, KEY_SAFETY * prof.key_err3 + prof.n + 64
+    return prof.keys3, KEY_SAFETY3 * prof.key_err3 + prof.n + 64
 
 
 _PRIMES: tuple[int, ...] | None = None
@@ -376,6 +382,36 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
     return cells
 
 
+def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
+    """(pattern bit, factor) for every entity that is a factor of p by itself:
+    a real root that rounds to an integer r with p(r) = 0 (x - r), or a
+    conjugate pair whose sum and product round to integers T, M with
+    x^2 - T x + M dividing p (irreducible over Q: its roots are not real).
+    Checked exactly; a cheap closeness test screens the rest."""
+    out = []
+    for i, ent in enumerate(prof.perm):
+        if ent < prof.r:
+            u = float(prof.real_roots[ent])
+            r = round(u)
+            if abs(u - r) > 1e-6 * max(1.0, abs(u)):
+                continue
+            acc = 0
+            for c in reversed(p.coeffs):
+                acc = acc * r + c
+            if acc == 0:
+                out.append((i, IntPolynomial([-r, 1])))
+        else:
+            j = ent - prof.r
+            t, m = float(prof.pair_sums[j]), float(prof.pair_products[j])
+            tr, mr = round(t), round(m)
+            if abs(t - tr) > 1e-6 * max(1.0, abs(t)) or abs(m - mr) > 1e-6 * max(1.0, abs(m)):
+                continue
+            q = IntPolynomial([mr, -tr, 1])
+            if divide_exact(p, q) is not None:
+                out.append((i, q))
+    return out
+
+
 def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
                              stats: FactorStats, prof: RootProfile | None = None,
                              early_exit: bool = True) -> list[IntPolynomial]:
@@ -388,6 +424,25 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
         prof = _profile_cached(p.coeffs)
         stats.root_seconds += time.perf_counter() - t0
     n = prof.n
+    if n > 1:
+        # one-entity factors first: an integer root, or a conjugate pair with
+        # integral t and m, divides p by itself -- and k of them would make
+        # every one of their 2^k subsets a hit of the search (a product of
+        # linear factors flooded it with 3e10 hits)
+        single = _single_entity_factors(prof, p)
+        if single:
+            t0 = time.perf_counter()
+            rest, mask = p, 0
+            for bit, q in single:
+                rest = divide_exact(rest, q)
+                mask |= 1 << bit
+            stats.verify_seconds += time.perf_counter() - t0
+            out = [q for _, q in single]
+            left = ((1 << n) - 1) & ~mask
+            if rest.degree >= 1:
+                out += _factor_monic_squarefree(rest, cfg, workers, stats, _sub_profile(prof, left),
+                                                early_exit)
+            return out
     stats.n = max(stats.n, n)
 
     t0 = time.perf_counter()
