@@ -45,6 +45,7 @@ from .polynomial import (
     square_free_decompose,
 )
 from .recombine import BACKENDS, RecombineStats, search_keys
+from .errors import NonConvergence
 from .rootfinder import RootProfile, ToleranceConfig, hp_profile
 
 _STRIDE = 65  # smaller side degree <= 64
@@ -412,6 +413,50 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
     return out
 
 
+def _coeff_bits(p: IntPolynomial) -> int:
+    return max(abs(c) for c in p.coeffs).bit_length()
+
+
+def _integer_roots(p: IntPolynomial, scan: bool) -> list:
+    """Integer roots of a monic square-free p (its only rational roots),
+    exactly: the rounded real parts of the float root seeds (and their
+    neighbours), or with scan every integer within Fujiwara's root bound
+    (when it is at most 10^4), prefiltered modulo 2^61 - 1."""
+    from .rootfinder import _initial_roots
+
+    cs = list(p.coeffs)
+    d = len(cs) - 1
+    cand = set()
+    try:
+        for z in _initial_roots(cs):
+            if abs(z.imag) < 1.0 and abs(z.real) < 1e15:
+                r = int(round(z.real))
+                cand.update((r - 1, r, r + 1))
+    except NonConvergence:
+        pass
+    if scan:
+        # Fujiwara: every root has |z| <= 2 max_k |c_{d-k}|^(1/k)
+        bound = 2.0 * max((abs(cs[d - k]) ** (1.0 / k) if cs[d - k] else 0.0) for k in range(1, d + 1))
+        if bound <= 1e4:
+            M = (1 << 61) - 1
+            cm = [c % M for c in cs]
+            for r in range(-int(bound) - 1, int(bound) + 2):
+                acc = 0
+                rm = r % M
+                for c in reversed(cm):
+                    acc = (acc * rm + c) % M
+                if acc == 0:
+                    cand.add(r)
+    out = []
+    for r in sorted(cand):
+        acc = 0
+        for c in reversed(cs):
+            acc = acc * r + c
+        if acc == 0:
+            out.append(r)
+    return out
+
+
 def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
                              stats: FactorStats, prof: RootProfile | None = None,
                              early_exit: bool = True) -> list[IntPolynomial]:
@@ -421,8 +466,25 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
         return [p]
     if prof is None:
         t0 = time.perf_counter()
-        prof = _profile_cached(p.coeffs)
+        # integer roots make the polish ill-conditioned (a Wilkinson-like
+        # product of 39 of them did not converge): split them off exactly
+        # before the multiprecision polish, and as a fallback if it fails
+        ints = _integer_roots(p, scan=False) if _coeff_bits(p) > 100 else []
+        if not ints:
+            try:
+                prof = _profile_cached(p.coeffs)
+            except NonConvergence:
+                ints = _integer_roots(p, scan=True)
+                if not ints:
+                    raise
         stats.root_seconds += time.perf_counter() - t0
+        if ints:
+            rest = p
+            for r in ints:
+                rest = divide_exact(rest, IntPolynomial([-r, 1]))
+            return [IntPolynomial([-r, 1]) for r in ints] + (
+                _factor_monic_squarefree(rest, cfg, workers, stats, None, early_exit)
+                if rest.degree >= 1 else [])
     n = prof.n
     if n > 1:
         # one-entity factors first: an integer root, or a conjugate pair with
