@@ -413,3 +413,68 @@ def test_randomised_products_match_sympy():
         p, want = _random_product(21, case)
         res = factor(p)
         assert res.certificate and sorted((list(g.coeffs), m) for g, m in res.factors) == want, case
+
+
+def _structured_product(seed0, case):
+    """The structured sweep's input: many small factors, x^n -+ 1 / x^n - 2,
+    small Swinnerton-Dyer products, a cubed factor, many integer roots, or
+    10^6-sized coefficients."""
+    import sympy
+
+    from paper_2410_15880_b200 import gen_swinnerton_dyer
+
+    x = sympy.symbols("x")
+    rng = random.Random(77000 + seed0 * 1000 + case)
+    mode = rng.choice(["many_small", "cyclo", "sd", "mult3", "real", "bigcoef"])
+    if mode == "many_small":
+        prod = sympy.Poly(1, x)
+        for _ in range(rng.randint(4, 12)):
+            d = rng.randint(1, 6)
+            co = [rng.randint(-9, 9) for _ in range(d)] + [rng.choice([1, 1, 1, 2, -1])]
+            co[0] = co[0] or 1
+            prod *= sympy.Poly(list(reversed(co)), x)
+    elif mode == "cyclo":
+        prod = sympy.Poly(x ** rng.randint(2, 110) - rng.choice([1, -1, 2]), x)
+    elif mode == "sd":
+        k = rng.randint(2, 5)
+        prod = sympy.Poly(list(reversed([int(c) for c in gen_swinnerton_dyer(k).coeffs])), x)
+        if rng.random() < 0.5 and 2 ** k <= 60:
+            prod *= sympy.Poly(list(reversed([rng.randint(-9, 9) for _ in range(rng.randint(2, 30))] + [1])), x)
+    elif mode == "mult3":
+        f = sympy.Poly(list(reversed([rng.randint(-20, 20) for _ in range(rng.randint(2, 20))] + [1])), x)
+        prod = f ** 3 * sympy.Poly(list(reversed([rng.randint(-20, 20) for _ in range(rng.randint(2, 30))] + [1])), x)
+    elif mode == "real":
+        prod = sympy.Poly(1, x)
+        for r in rng.sample(range(-60, 60), rng.randint(5, 40)):
+            prod *= sympy.Poly(x - r, x)
+        prod *= sympy.Poly(list(reversed([rng.randint(-9, 9) for _ in range(rng.randint(2, 40))] + [1])), x)
+    else:
+        prod = sympy.Poly(1, x)
+        for _ in range(rng.randint(2, 3)):
+            prod *= sympy.Poly(list(reversed([rng.randint(-10**6, 10**6) for _ in range(rng.randint(5, 40))] + [1])), x)
+    want = []
+    for f, m in sympy.factor_list(prod.as_expr(), x)[1]:
+        co = [int(c) for c in reversed(sympy.Poly(f, x).all_coeffs())]
+        want.append(([-c for c in co] if co[-1] < 0 else co, m))
+    return mode, P([int(c) for c in reversed(prod.all_coeffs())]), sorted(want)
+
+
+# structured-sweep faults: 2^35 hits from 35 integer roots (1/9), a Tr3 window
+# that dropped a factor with 10^6 coefficients (2/39), a Wilkinson-like
+# product whose polish did not converge (5/39)
+@pytest.mark.parametrize("seed0,case", [(1, 9), (2, 39), (5, 39), (3, 0)])
+def test_structured_regressions_match_sympy(seed0, case):
+    mode, p, want = _structured_product(seed0, case)
+    if p.degree > 128:
+        pytest.skip("degree beyond the pattern width")
+    res = factor(p)
+    assert res.certificate and sorted((list(g.coeffs), m) for g, m in res.factors) == want, mode
+
+
+def test_structured_products_match_sympy():
+    for case in range(24):
+        mode, p, want = _structured_product(9, case)
+        if p.degree < 1 or p.degree > 128:
+            continue
+        res = factor(p)
+        assert res.certificate and sorted((list(g.coeffs), m) for g, m in res.factors) == want, (case, mode)
