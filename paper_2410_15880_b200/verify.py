@@ -389,27 +389,28 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
     conjugate pair whose sum and product round to integers T, M with
     x^2 - T x + M dividing p (irreducible over Q: its roots are not real).
     Checked exactly; a cheap closeness test screens the rest."""
+    # vectorised screen: only entities within 1e-6 of integral values are tested
+    ru = np.asarray(prof.real_roots, dtype=np.float64)
+    near_r = np.abs(ru - np.round(ru)) <= 1e-6 * np.maximum(1.0, np.abs(ru))
+    pt = np.asarray(prof.pair_sums, dtype=np.float64)
+    pm = np.asarray(prof.pair_products, dtype=np.float64)
+    near_p = ((np.abs(pt - np.round(pt)) <= 1e-6 * np.maximum(1.0, np.abs(pt)))
+              & (np.abs(pm - np.round(pm)) <= 1e-6 * np.maximum(1.0, np.abs(pm))))
+    if not near_r.any() and not near_p.any():
+        return []
+    bit_of = {ent: i for i, ent in enumerate(prof.perm)}
     out = []
-    for i, ent in enumerate(prof.perm):
-        if ent < prof.r:
-            u = float(prof.real_roots[ent])
-            r = round(u)
-            if abs(u - r) > 1e-6 * max(1.0, abs(u)):
-                continue
-            acc = 0
-            for c in reversed(p.coeffs):
-                acc = acc * r + c
-            if acc == 0:
-                out.append((i, IntPolynomial([-r, 1])))
-        else:
-            j = ent - prof.r
-            t, m = float(prof.pair_sums[j]), float(prof.pair_products[j])
-            tr, mr = round(t), round(m)
-            if abs(t - tr) > 1e-6 * max(1.0, abs(t)) or abs(m - mr) > 1e-6 * max(1.0, abs(m)):
-                continue
-            q = IntPolynomial([mr, -tr, 1])
-            if divide_exact(p, q) is not None:
-                out.append((i, q))
+    for ent in np.flatnonzero(near_r):
+        r = int(round(float(ru[ent])))
+        acc = 0
+        for c in reversed(p.coeffs):
+            acc = acc * r + c
+        if acc == 0:
+            out.append((bit_of[int(ent)], IntPolynomial([-r, 1])))
+    for j in np.flatnonzero(near_p):
+        q = IntPolynomial([int(round(float(pm[j]))), -int(round(float(pt[j]))), 1])
+        if divide_exact(p, q) is not None:
+            out.append((bit_of[prof.r + int(j)], q))
     return out
 
 
