@@ -181,7 +181,12 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
 
     d = len(coeffs) - 1
     bits = max(abs(c) for c in coeffs).bit_length()
-    prec = max(256, bits + 160)
+    # near a root the terms c_k z^k reach ~2^bits |z|^d and cancel: the working
+    # precision must cover that magnitude, not only the coefficients (28
+    # quadratics x^2 - p: 142-bit coefficients, |z|^56 ~ 2^190, no convergence
+    # at bits + 160)
+    zmax = max(2.0, float(np.max(np.abs(z0)))) if len(z0) else 2.0
+    prec = max(256, bits + int(math.ceil(d * math.log2(zmax))) + 160)
     with mpmath.workprec(prec):
         cs = [mpmath.mpf(c) for c in coeffs]
         z = [mpmath.mpc(complex(w)) for w in z0]
@@ -200,6 +205,8 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
             return p, dp
 
         tol = mpmath.mpf(2) ** (-(prec - 40))
+        floor = mpmath.mpf(2) ** -120
+        prev = None
         for _ in range(200):
             worst = mpmath.mpf(0)
             new = []
@@ -218,6 +225,12 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
             z = new
             if worst < tol:
                 break
+            # at the evaluation's noise floor (terms c_k z^k far above the
+            # value cancel): corrections stop halving -- the a-posteriori
+            # bound below accounts for the residual
+            if prev is not None and worst < floor and worst > prev / 2:
+                break
+            prev = worst
         else:
             return None
         err = np.zeros(d)
@@ -266,6 +279,19 @@ def _hp_roots(p: IntPolynomial):
             res = tuple(res) + (None,)
     if res is None:
         res = _polish_mp(coeffs, z0)
+    if res is None:
+        # float seeds too far off (real roots seeded ~0.5 off the axis for
+        # 142-bit coefficients): multiprecision seeds, then the same polish
+        import mpmath
+
+        bits = max(abs(c) for c in coeffs).bit_length()
+        with mpmath.workprec(bits + 200):
+            try:
+                rts = mpmath.polyroots([mpmath.mpf(c) for c in reversed(coeffs)], maxsteps=400,
+                                       extraprec=bits + 200)
+                res = _polish_mp(coeffs, np.array([complex(r) for r in rts]))
+            except mpmath.libmp.libhyper.NoConvergence:
+                res = None
     if res is None:
         raise NonConvergence("root polish did not converge")
     return res

@@ -45,7 +45,7 @@ from .polynomial import (
     square_free_decompose,
 )
 from .recombine import BACKENDS, RecombineStats, search_keys
-from .errors import NonConvergence
+from .errors import NonConvergence, RecombineDeviceError
 from .rootfinder import RootProfile, ToleranceConfig, hp_profile
 
 _STRIDE = 65  # smaller side degree <= 64
@@ -210,7 +210,8 @@ _PIECES = True
 
 
 def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
-                       keys3: np.ndarray, half_width3: int, stats, early_exit: bool):
+                       keys3: np.ndarray, half_width3: int, stats, early_exit: bool,
+                       max_rows: int | None = None):
     """search_and_verify, optionally with early termination.  Returns (pats,
     verdict, side, coeffs, complete, stopped): stopped when the join ended at
     a verified hit; complete when the candidates nevertheless cover every
@@ -247,6 +248,8 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
         )
         if nout.value <= cap:
             break
+        if max_rows is not None and nout.value > max_rows:
+            raise RecombineDeviceError(f"{nout.value} raw hits exceed the flood limit {max_rows}")
         cap = int(nout.value)
     _fill_stats(stats, st)
     m = int(nout.value)
@@ -383,6 +386,47 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
     return cells
 
 
+def _small_factors(prof: RootProfile, p: IntPolynomial) -> list:
+    """((pattern,), factor) for factors made of 2 or 3 entities: every such
+    entity subset whose combined keys lie inside both windows (vectorised over
+    all pairs and triples of the <= 64 entities), rebuilt exactly and
+    confirmed by division (smallest first; the caller keeps disjoint ones)."""
+    n = prof.n
+    keys, T = _search_window(prof)
+    keys3, T3 = _secondary_window(prof)
+    k1 = np.asarray(keys, dtype=np.uint64)
+    k3 = np.asarray(keys3, dtype=np.uint64) if keys3 is not None else None
+    TWO = np.uint64
+
+    def close(s, t):
+        d = np.minimum(s, (TWO(0) - s))
+        return d <= TWO(min(t, (1 << 64) - 1))
+
+    out = []
+    i, j = np.triu_indices(n, 1)
+    s1 = k1[i] + k1[j]
+    ok = close(s1, T)
+    if k3 is not None:
+        ok &= close(k3[i] + k3[j], T3)
+    cand = [((1 << int(a)) | (1 << int(b))) for a, b in zip(i[ok], j[ok])]
+    if n <= 64:
+        a, b = np.triu_indices(n, 1)
+        for c in range(2, n):
+            sel = b < c
+            aa, bb = a[sel], b[sel]
+            s = k1[aa] + k1[bb] + k1[c]
+            ok = close(s, T)
+            if k3 is not None:
+                ok &= close(k3[aa] + k3[bb] + k3[c], T3)
+            cand += [((1 << int(x)) | (1 << int(y)) | (1 << c)) for x, y in zip(aa[ok], bb[ok])]
+    full = (1 << n) - 1
+    for t in sorted(set(cand), key=lambda x: (bin(x).count("1"), x)):
+        q = _host_candidate(prof, p, t)
+        if q is not None:
+            out.append(((t,), q))
+    return out
+
+
 def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
     """(pattern bit, factor) for every entity that is a factor of p by itself:
     a real root that rounds to an integer r with p(r) = 0 (x - r), or a
@@ -458,6 +502,36 @@ def _integer_roots(p: IntPolynomial, scan: bool) -> list:
     return out
 
 
+# more survivors than this after the search: look for small multi-entity
+# factors before processing them one by one
+_FLOOD = 512
+
+
+def _split_small_factors(p, prof, small, cfg, workers, stats, early_exit):
+    """Divide the (disjoint, exactly confirmed) small factors out of p and
+    factor the rest over its own entities; None when none applies."""
+    t0 = time.perf_counter()
+    rest, mask, out = p, 0, []
+    for bits, q in small:  # bits: one entity's bit index, or (pattern,) for 2-3 entities
+        pat = bits[0] if isinstance(bits, tuple) else (1 << bits)
+        if pat & mask:
+            continue  # overlaps a factor already split off
+        r = divide_exact(rest, q)
+        if r is None:
+            continue
+        rest = r
+        mask |= pat
+        out.append(q)
+    stats.verify_seconds += time.perf_counter() - t0
+    if not out:
+        return None
+    left = ((1 << prof.n) - 1) & ~mask
+    if rest.degree >= 1:
+        out += _factor_monic_squarefree(rest, cfg, workers, stats, _sub_profile(prof, left),
+                                        early_exit)
+    return out
+
+
 def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: int,
                              stats: FactorStats, prof: RootProfile | None = None,
                              early_exit: bool = True) -> list[IntPolynomial]:
@@ -490,22 +564,12 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     if n > 1:
         # one-entity factors first: an integer root, or a conjugate pair with
         # integral t and m, divides p by itself -- and k of them would make
-        # every one of their 2^k subsets a hit of the search (a product of
-        # linear factors flooded it with 3e10 hits)
-        single = _single_entity_factors(prof, p)
-        if single:
-            t0 = time.perf_counter()
-            rest, mask = p, 0
-            for bit, q in single:
-                rest = divide_exact(rest, q)
-                mask |= 1 << bit
-            stats.verify_seconds += time.perf_counter() - t0
-            out = [q for _, q in single]
-            left = ((1 << n) - 1) & ~mask
-            if rest.degree >= 1:
-                out += _factor_monic_squarefree(rest, cfg, workers, stats, _sub_profile(prof, left),
-                                                early_exit)
-            return out
+        # every one of their 2^k unions a hit of the search (35 linear
+        # factors flooded it with 3e10 hits)
+        split = _split_small_factors(p, prof, _single_entity_factors(prof, p), cfg, workers, stats,
+                                     early_exit)
+        if split is not None:
+            return split
     stats.n = max(stats.n, n)
 
     t0 = time.perf_counter()
@@ -515,8 +579,24 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     if workers == 1 and keys3 is not None:
         # one device call: search, Tr3 window and verification back to back
         # (recombine_seconds then covers the device verification too)
-        pats, verdict, side, coeffs, complete, stopped = _search_and_verify(
-            prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N)
+        search = lambda limit: _search_and_verify(  # noqa: E731
+            prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N, limit)
+        try:
+            pats, verdict, side, coeffs, complete, stopped = search(1 << 16)
+            flood = len(pats) > _FLOOD
+        except RecombineDeviceError as e:
+            if "raw hits exceed" not in str(e):
+                raise
+            flood, pats = True, None
+        if flood and n > 3:
+            # a flood of candidates: many small multi-entity factors (all 2^k
+            # unions of k quadratics x^2 - a are hits) -- split them off first
+            split = _split_small_factors(p, prof, _small_factors(prof, p), cfg, workers, stats,
+                                         early_exit)
+            if split is not None:
+                return split
+        if pats is None:  # no small factors behind the flood: take every candidate
+            pats, verdict, side, coeffs, complete, stopped = search(None)
         stats.early_exits += int(stopped and complete)  # stopped, pieces searched in the call
         keep = pats != 0
         pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]

@@ -249,10 +249,10 @@ def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
     real_div, real_sav = V.divide_exact, V._search_and_verify
     state = {"whole": False, "rejected": 0}
 
-    def search(prof, q, *args):
-        if not args[-1] and prof.n >= V._EARLY_N:  # the whole-space fallback has begun
+    def search(prof, q, keys, T, keys3, T3, stats, early, *rest):
+        if not early and prof.n >= V._EARLY_N:  # the whole-space fallback has begun
             state["whole"] = True
-        return real_sav(prof, q, *args)
+        return real_sav(prof, q, keys, T, keys3, T3, stats, early, *rest)
 
     def reject_until_fallback(a, b):
         if not state["whole"]:
