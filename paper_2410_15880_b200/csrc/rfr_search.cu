@@ -243,8 +243,24 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
   const uint32_t na = a1 - a0, nb = tile - na;
   const uint32_t b0 = d0 - a0;
-  for (uint32_t t = tid; t < na; t += kMergeThreads) sK[kswz(t)] = __ldg(A + a0 + t);
-  for (uint32_t t = tid; t < nb; t += kMergeThreads) sK[kswz(na + t)] = __ldg(A + ((r0 + b0 + t) & mask)) + v;
+  // one pass over the tile: output slot t < na stages A[a0 + t], the rest
+  // stage B'; every thread's kMergeItems loads are independent and issued
+  // before the first shared store (the A and B halves as two loops waited
+  // on HBM twice per tile)
+  auto stage = [&](uint32_t t) {
+    const bool isA = t < na;
+    const uint64_t* src = isA ? A + a0 + t : A + ((r0 + b0 + (t - na)) & mask);
+    return __ldg(src) + (isA ? 0ull : v);
+  };
+  if (tile == (uint32_t)kMergeTile) {
+    uint64_t x[kMergeItems];
+#pragma unroll
+    for (int u = 0; u < kMergeItems; u++) x[u] = stage(tid + u * kMergeThreads);
+#pragma unroll
+    for (int u = 0; u < kMergeItems; u++) sK[kswz(tid + u * kMergeThreads)] = x[u];
+  } else {
+    for (uint32_t t = tid; t < tile; t += kMergeThreads) sK[kswz(t)] = stage(t);
+  }
   __syncthreads();
   // per-thread merge of kMergeItems outputs from the staged tile
   const uint32_t dt = min((uint32_t)(tid * kMergeItems), tile);
