@@ -387,7 +387,7 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
 
 
 def _small_factors(prof: RootProfile, p: IntPolynomial) -> list:
-    """((pattern,), factor) for factors made of 2 or 3 entities: every such
+    """((pattern,), factor) for factors made of 1 to 3 entities: every such
     entity subset whose combined keys lie inside both windows (vectorised over
     all pairs and triples of the <= 64 entities), rebuilt exactly and
     confirmed by division (smallest first; the caller keeps disjoint ones)."""
@@ -403,12 +403,19 @@ def _small_factors(prof: RootProfile, p: IntPolynomial) -> list:
         return d <= TWO(min(t, (1 << 64) - 1))
 
     out = []
+    # single entities first: a one-entity factor the exact screen above missed
+    # must split off before any 2-3 entity union containing it (which would
+    # otherwise be confirmed -- it divides p -- and reported as irreducible)
+    ok1 = close(k1, T)
+    if k3 is not None:
+        ok1 &= close(k3, T3)
+    cand = [1 << int(a) for a in np.flatnonzero(ok1)]
     i, j = np.triu_indices(n, 1)
     s1 = k1[i] + k1[j]
     ok = close(s1, T)
     if k3 is not None:
         ok &= close(k3[i] + k3[j], T3)
-    cand = [((1 << int(a)) | (1 << int(b))) for a, b in zip(i[ok], j[ok])]
+    cand += [((1 << int(a)) | (1 << int(b))) for a, b in zip(i[ok], j[ok])]
     if n <= 64:
         a, b = np.triu_indices(n, 1)
         for c in range(2, n):
@@ -432,7 +439,9 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
     a real root that rounds to an integer r with p(r) = 0 (x - r), or a
     conjugate pair whose sum and product round to integers T, M with
     x^2 - T x + M dividing p (irreducible over Q: its roots are not real).
-    Checked exactly; a cheap closeness test screens the rest."""
+    Checked exactly; a cheap closeness test screens the rest.  The rounding
+    uses the exact double-double value (hi + lo, or the multiprecision one):
+    a value at or above 2^53 is not an integer in its high word alone."""
     # vectorised screen: only entities within 1e-6 of integral values are tested
     ru = np.asarray(prof.real_roots, dtype=np.float64)
     near_r = np.abs(ru - np.round(ru)) <= 1e-6 * np.maximum(1.0, np.abs(ru))
@@ -442,19 +451,33 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
               & (np.abs(pm - np.round(pm)) <= 1e-6 * np.maximum(1.0, np.abs(pm))))
     if not near_r.any() and not near_p.any():
         return []
+
+    def exact(hi, lo, j):
+        v = Fraction(float(hi[j]))
+        if lo is not None:
+            v += Fraction(float(lo[j]))
+        return v
+
     bit_of = {ent: i for i, ent in enumerate(prof.perm)}
     out = []
     for ent in np.flatnonzero(near_r):
-        r = int(round(float(ru[ent])))
+        e = int(ent)
+        u = prof.hp_real[e] if prof.hp_real is not None else exact(ru, prof.real_lo, e)
+        r = round(u)
         acc = 0
         for c in reversed(p.coeffs):
             acc = acc * r + c
         if acc == 0:
-            out.append((bit_of[int(ent)], IntPolynomial([-r, 1])))
+            out.append((bit_of[e], IntPolynomial([-r, 1])))
     for j in np.flatnonzero(near_p):
-        q = IntPolynomial([int(round(float(pm[j]))), -int(round(float(pt[j]))), 1])
+        j = int(j)
+        if prof.hp_pair is not None:
+            tt, mm = prof.hp_pair[j]
+        else:
+            tt, mm = exact(pt, prof.sum_lo, j), exact(pm, prof.prod_lo, j)
+        q = IntPolynomial([round(mm), -round(tt), 1])
         if divide_exact(p, q) is not None:
-            out.append((bit_of[prof.r + int(j)], q))
+            out.append((bit_of[prof.r + j], q))
     return out
 
 

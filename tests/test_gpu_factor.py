@@ -478,3 +478,72 @@ def test_structured_products_match_sympy():
             continue
         res = factor(p)
         assert res.certificate and sorted((list(g.coeffs), m) for g, m in res.factors) == want, (case, mode)
+
+
+def _sympy_factors(p):
+    import sympy
+
+    x = sympy.symbols("x")
+    want = []
+    for f, m in sympy.factor_list(sympy.Poly(list(reversed(p.coeffs)), x).as_expr(), x)[1]:
+        co = [int(c) for c in reversed(sympy.Poly(f, x).all_coeffs())]
+        want.append(([-c for c in co] if co[-1] < 0 else co, m))
+    return sorted(want)
+
+
+def _primes(k, start=2):
+    out, c = [], start
+    while len(out) < k:
+        if all(c % q for q in range(2, int(c ** 0.5) + 1)):
+            out.append(c)
+        c += 1
+    return out
+
+
+def test_flood_of_quadratics_with_mixed_factors_matches_sympy():
+    """9 quadratics x^2 - a (all 2^9 unions are factors: a flood of
+    survivors) next to a cubic and a random degree-12 factor: the flood path
+    splits the small factors off first (verify._small_factors)."""
+    rng = random.Random(5)
+    p = P([1])
+    for a in _primes(9, 3):
+        p = p * P([-a, 0, 1])
+    p = p * P([-2, 0, 0, 1]) * P([rng.randint(-9, 9) for _ in range(12)] + [1])
+    res = factor(p)
+    assert res.certificate
+    assert sorted((list(g.coeffs), m) for g, m in res.factors) == _sympy_factors(p)
+
+
+def test_flood_without_small_factors_matches_sympy():
+    """10 quartics x^4 - 2(a+b) x^2 + (a-b)^2 (roots +-sqrt(a) +-sqrt(b),
+    four real entities each, irreducible): 2^10 unions pass, none of them
+    of 2-3 entities, so the flood path finds no small factor and takes every
+    candidate."""
+    ps = _primes(20, 2)
+    p = P([1])
+    for a, b in zip(ps[0::2], ps[1::2]):
+        p = p * P([(a - b) ** 2, 0, -2 * (a + b), 0, 1])
+    res = factor(p)
+    assert res.certificate and len(res.factors) == 10
+    assert sorted((list(g.coeffs), m) for g, m in res.factors) == _sympy_factors(p)
+
+
+def test_flood_of_large_quadratics_142_bit_coefficients():
+    """28 quadratics x^2 - q for primes q (coefficients of 142 bits: the
+    multiprecision polish, then the flood path)."""
+    p = P([1])
+    for q in _primes(28, 3):
+        p = p * P([-q, 0, 1])
+    assert max(abs(c) for c in p.coeffs).bit_length() > 100
+    res = factor(p)
+    assert res.certificate and len(res.factors) == 28
+    assert sorted((list(g.coeffs), m) for g, m in res.factors) == _sympy_factors(p)
+
+
+def test_factor_big_pair_products_not_merged():
+    """(x^2+x+2^53+1)(x^2+x+2^53+3)(x^2-2)(x^2-3) -- the two
+    large quadratics must come out separately."""
+    p = P([2**53 + 1, 1, 1]) * P([2**53 + 3, 1, 1]) * P([-2, 0, 1]) * P([-3, 0, 1])
+    res = factor(p)
+    assert res.certificate and len(res.factors) == 4
+    assert sorted((list(g.coeffs), m) for g, m in res.factors) == _sympy_factors(p)
