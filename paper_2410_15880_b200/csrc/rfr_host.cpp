@@ -3,7 +3,8 @@
 //
 //  rfr_polish_roots   simultaneous Aberth-Ehrlich corrections in double-double
 //                     complex arithmetic (~106-bit), seeded by any approximate
-//                     roots, with an a-posteriori error bound per root.  It
+//                     roots, with a rigorous inclusion radius per root
+//                     (Rouche on the Taylor expansion, pairwise disjoint discs).  It
 //                     replaces find_roots' iteration (pkg/src/polyfactor/
 //                     rootfinder.py:100-174), whose 64-bit roots would make the
 //                     subset-sum keys ~2^-45 coarse; ~2^-100 roots make them
@@ -144,27 +145,73 @@ int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double
     for (int i = 0; i < d; i++) z[i] = z[i] - corr[i];  // Jacobi-style update
     if (worst < 8.0 * eps_dd) break;
   }
-  // a posteriori bounds: Newton step plus evaluation error, and separation
+  // Rigorous inclusion radii (Lemma 1).  Around each centre z
+  // (the double-double value itself, exactly representable) write
+  // p(z + h) = c0 + c1 h + c2 h^2 + R(h).  If on the circle |h| = r
+  //     |c1| r  >  |c0| + |c2| r^2 + |R|max(r),
+  // Rouche's theorem (p against its linear term c1 h) puts exactly one root
+  // of p in the disc D(z, r).  c0, c1, c2 come from one triple Horner pass
+  // in double-double; each carries an evaluation error of at most
+  // gamma * A_k with A_k = P^(k)(|z|) / k!, P(x) = sum |a_j| x^j, so the test
+  // uses |c0|, |c2| inflated and |c1| deflated by those amounts.  The tail
+  // k >= 3 is bounded by A_k r^k <= P(R) C(d, k) (r / R)^k, R = max(|z|, 1):
+  //     |R|max(r) <= P(R) (d r / R)^3 e^(d r / R) / 6.
+  // Pairwise disjoint discs (checked below) then hold one root each, so they
+  // account for all d roots: the true root is within err[i] of the centre.
+  const double gamma = (32.0 * d + 64.0) * eps_dd;  // complex dd Horner, with room
+  const double fl = 1.0 + (4.0 * d + 8.0) * std::ldexp(1.0, -53);  // double Horner, upward
+  const double cab = std::ldexp(1.0, -50);                           // |.| of a dd complex
+  std::vector<char> ok(d, 0);
   for (int i = 0; i < d; i++) {
-    cdd pz, dpz;
-    double absum;
-    horner(c, z[i], pz, dpz, absum);
-    const double gamma = (4.0 * d + 8.0) * eps_dd;
-    const double num = cabs_d(pz) + gamma * absum;
-    const double den = cabs_d(dpz);
-    double e = den > 0.0 ? 2.0 * num / den : INFINITY;
-    e = std::fmax(e, 4.0 * eps_dd * std::fmax(1.0, cabs_d(z[i])));
-    err[i] = e;
+    const cdd zi = z[i];
+    cdd p0 = {c[d], {0, 0}}, p1 = {{0, 0}, {0, 0}}, p2 = {{0, 0}, {0, 0}};
+    const double rho = cabs_d(zi) * (1.0 + cab);
+    const double R = std::fmax(rho, 1.0);
+    double A0 = std::fabs(to_d(c[d])), A1 = 0.0, A2 = 0.0, PR = A0;
+    for (int k = d - 1; k >= 0; k--) {
+      p2 = p2 * zi + p1;
+      p1 = p1 * zi + p0;
+      p0 = p0 * zi + cdd{c[k], {0, 0}};
+      const double ak = std::fabs(to_d(c[k])) * (1.0 + std::ldexp(1.0, -52));
+      A2 = A2 * rho + A1;
+      A1 = A1 * rho + A0;
+      A0 = A0 * rho + ak;
+      PR = PR * R + ak;
+    }
+    A0 *= fl; A1 *= fl; A2 *= fl; PR *= fl;
+    const double c0 = cabs_d(p0) * (1.0 + cab) + gamma * A0;
+    const double c1 = cabs_d(p1) * (1.0 - cab) - gamma * A1;
+    const double c2 = cabs_d(p2) * (1.0 + cab) + gamma * A2;
+    double r_ok = INFINITY;
+    if (c1 > 0.0 && std::isfinite(c0) && std::isfinite(c2) && std::isfinite(PR)) {
+      const double base = std::fmax(c0 / c1, std::ldexp(1.0, -200) * R);
+      for (double t : {1.125, 1.5, 2.0, 4.0, 16.0}) {
+        const double r = t * base;
+        const double x = d * r / R;
+        const double tail = PR * x * x * x * std::exp(x) / 6.0;
+        const double lhs = c1 * r;
+        const double rhs = c0 + c2 * r * r + tail;
+        if (std::isfinite(lhs) && lhs > rhs * (1.0 + 1e-9)) {
+          r_ok = r;
+          break;
+        }
+      }
+    }
+    ok[i] = std::isfinite(r_ok);
+    err[i] = r_ok;
   }
   int status = RFR_OK;
   for (int i = 0; i < d && status == RFR_OK; i++) {
-    if (!std::isfinite(err[i])) status = RFR_E_NUMERIC;
-    for (int j = i + 1; j < d; j++) {
-      const double sep = cabs_d(z[i] - z[j]);
-      if (sep <= 4.0 * (err[i] + err[j])) {
-        status = RFR_E_NUMERIC;
-        break;
-      }
+    if (!ok[i]) status = RFR_E_NUMERIC;
+    // pairwise disjoint discs: |z_i - z_j| from both words (the high-word
+    // difference is exact for close values, Sterbenz; every other step errs
+    // by 2^-53 relative to what it computes)
+    for (int j = i + 1; j < d && status == RFR_OK; j++) {
+      const double dh = z[i].re.hi - z[j].re.hi, dl = z[i].re.lo - z[j].re.lo;
+      const double eh = z[i].im.hi - z[j].im.hi, el = z[i].im.lo - z[j].im.lo;
+      const double fuzz =
+          std::ldexp(1.0, -50) * (std::fabs(dh) + std::fabs(dl) + std::fabs(eh) + std::fabs(el)) + 1e-300;
+      if (std::hypot(dh + dl, eh + el) - fuzz <= (err[i] + err[j]) * (1.0 + 1e-9)) status = RFR_E_NUMERIC;
     }
   }
   for (int i = 0; i < d; i++) {

@@ -9,7 +9,7 @@ host preprocessing and is not timed (BASELINE.json north_star).
 What is new is ``hp_profile``: the profile ``factor()`` searches with.  Roots
 are seeded by ``numpy.roots`` and polished to ~106 bits in double-double by the
 native Aberth iteration in ``librfr.so`` (``rfr_polish_roots``), which also
-returns an a-posteriori error bound per root.  From the polished roots every
+returns a rigorous inclusion radius per root (Lemma 1).  From the polished roots every
 entity (real root u, or conjugate pair x^2 - t x + m) gets two exact 64-bit
 fixed-point keys -- frac(u or t) and frac(u^2 or t^2 - 2m), the first two
 power sums, both integers for every true factor -- and a window half-width T
@@ -186,66 +186,142 @@ def _polish_mp(coeffs: list[int], z0: np.ndarray):
     # quadratics x^2 - p: 142-bit coefficients, |z|^56 ~ 2^190, no convergence
     # at bits + 160)
     zmax = max(2.0, float(np.max(np.abs(z0)))) if len(z0) else 2.0
-    prec = max(256, bits + int(math.ceil(d * math.log2(zmax))) + 160)
-    with mpmath.workprec(prec):
-        cs = [mpmath.mpf(c) for c in coeffs]
-        z = [mpmath.mpc(complex(w)) for w in z0]
-        # jitter coincident seeds
+    prec0 = max(256, bits + int(math.ceil(d * math.log2(zmax))) + 160)
+    z = [complex(w) for w in z0]
+    # the inclusion radii need |p(z)| small against |p'(z)|^2 / |p''(z)|:
+    # when a root cannot be certified at one precision, polish on at twice it
+    for attempt in range(3):
+        prec = prec0 << attempt
+        with mpmath.workprec(prec):
+            out = _polish_mp_at(coeffs, z, prec, jitter=(attempt == 0))
+            if out is None:
+                return None
+            cs, z = out
+            radii = _mp_inclusion_radii(cs, z, prec)
+            if radii is None:
+                continue
+            err = np.zeros(d)
+            rh, rl, ih, il = (np.zeros(d) for _ in range(4))
+            exact = []
+            for i in range(d):
+                re = _mpf_to_fraction(z[i].real)
+                im = _mpf_to_fraction(z[i].imag)
+                rh[i], rl[i] = _dd_split(re)
+                ih[i], il[i] = _dd_split(im)
+                exact.append((re, im))
+                # the disc is reported around the double-double centre (what the
+                # keys are built from): widen it by the rounding to double-double;
+                # float() rounds to nearest, one ulp up keeps it an upper bound
+                shift = abs(re - _dd_frac(rh[i], rl[i])) + abs(im - _dd_frac(ih[i], il[i]))
+                err[i] = math.nextafter(float(radii[i]) + float(shift), math.inf)
+            return rh, rl, ih, il, err, exact
+    return None
+
+
+def _polish_mp_at(coeffs, z0, prec, jitter):
+    """Aberth iterations in the current mpmath working precision from the
+    centres z0; returns (mp coefficients, mp roots) or None."""
+    import mpmath
+
+    d = len(coeffs) - 1
+    cs = [mpmath.mpf(c) for c in coeffs]
+    z = [mpmath.mpc(w) for w in z0]
+    if jitter:  # jitter coincident seeds
         for i in range(d):
             for j in range(i):
                 if abs(z[i] - z[j]) < mpmath.mpf(2) ** -20:
                     z[i] += mpmath.mpc(0, 1e-6 * (i + 1))
 
-        def evalp(x):
-            p = cs[d]
-            dp = mpmath.mpc(0)
-            for k in range(d - 1, -1, -1):
-                dp = dp * x + p
-                p = p * x + cs[k]
-            return p, dp
+    def evalp(x):
+        p = cs[d]
+        dp = mpmath.mpc(0)
+        for k in range(d - 1, -1, -1):
+            dp = dp * x + p
+            p = p * x + cs[k]
+        return p, dp
 
-        tol = mpmath.mpf(2) ** (-(prec - 40))
-        floor = mpmath.mpf(2) ** -120
-        prev = None
-        for _ in range(200):
-            worst = mpmath.mpf(0)
-            new = []
-            for i in range(d):
-                p, dp = evalp(z[i])
-                if dp == 0:
-                    dp = mpmath.mpf(2) ** -prec
-                w = p / dp
-                s = mpmath.mpc(0)
-                for j in range(d):
-                    if j != i:
-                        s += 1 / (z[i] - z[j])
-                corr = w / (1 - w * s)
-                new.append(z[i] - corr)
-                worst = max(worst, abs(corr) / max(1, abs(z[i])))
-            z = new
-            if worst < tol:
-                break
-            # at the evaluation's noise floor (terms c_k z^k far above the
-            # value cancel): corrections stop halving -- the a-posteriori
-            # bound below accounts for the residual
-            if prev is not None and worst < floor and worst > prev / 2:
-                break
-            prev = worst
-        else:
-            return None
-        err = np.zeros(d)
-        rh, rl, ih, il = (np.zeros(d) for _ in range(4))
-        exact = []
+    tol = mpmath.mpf(2) ** (-(prec - 40))
+    floor = mpmath.mpf(2) ** -120
+    prev = None
+    for _ in range(200):
+        worst = mpmath.mpf(0)
+        new = []
         for i in range(d):
             p, dp = evalp(z[i])
-            e = 2 * (abs(p) + abs(z[i]) * mpmath.mpf(2) ** (bits - prec + 8)) / abs(dp)
-            err[i] = float(max(e, mpmath.mpf(2) ** -110 * max(1, abs(z[i]))))
-            re = _mpf_to_fraction(z[i].real)
-            im = _mpf_to_fraction(z[i].imag)
-            rh[i], rl[i] = _dd_split(re)
-            ih[i], il[i] = _dd_split(im)
-            exact.append((re, im))
-        return rh, rl, ih, il, err, exact
+            if dp == 0:
+                dp = mpmath.mpf(2) ** -prec
+            w = p / dp
+            s = mpmath.mpc(0)
+            for j in range(d):
+                if j != i:
+                    s += 1 / (z[i] - z[j])
+            corr = w / (1 - w * s)
+            new.append(z[i] - corr)
+            worst = max(worst, abs(corr) / max(1, abs(z[i])))
+        z = new
+        if worst < tol:
+            break
+        # at the evaluation's noise floor (terms c_k z^k far above the value
+        # cancel): corrections stop halving -- the inclusion radii account
+        # for the residual (or ask for more precision)
+        if prev is not None and worst < floor and worst > prev / 2:
+            break
+        prev = worst
+    else:
+        return None
+    return cs, z
+
+
+def _mp_inclusion_radii(cs, z, prec):
+    """Rigorous inclusion radius per centre z_i (Lemma 1), in
+    the working precision: p(z + h) = c0 + c1 h + c2 h^2 + R(h) with
+    |c1| r > |c0| + |c2| r^2 + |R|max(r) puts exactly one root in D(z_i, r)
+    (Rouche).  Each c_k carries at most gamma A_k of rounding error, A_k =
+    P^(k)(|z|)/k! for P(x) = sum |a_j| x^j; the tail is bounded by
+    P(R) (d r/R)^3 e^(d r/R) / 6, R = max(|z|, 1).  Returns the radii, or
+    None when a root cannot be certified at this precision."""
+    import mpmath
+
+    d = len(cs) - 1
+    gamma = mpmath.mpf(32 * d + 64) * mpmath.mpf(2) ** (-prec)
+    fl = 1 + mpmath.mpf(4 * d + 8) * mpmath.mpf(2) ** (-prec)
+    out = []
+    for zi in z:
+        p0, p1, p2 = mpmath.mpc(cs[d]), mpmath.mpc(0), mpmath.mpc(0)
+        rho = abs(zi) * fl
+        R = max(rho, mpmath.mpf(1))
+        A0, A1, A2, PR = abs(cs[d]), mpmath.mpf(0), mpmath.mpf(0), abs(cs[d])
+        for k in range(d - 1, -1, -1):
+            p2 = p2 * zi + p1
+            p1 = p1 * zi + p0
+            p0 = p0 * zi + cs[k]
+            ak = abs(cs[k])
+            A2 = A2 * rho + A1
+            A1 = A1 * rho + A0
+            A0 = A0 * rho + ak
+            PR = PR * R + ak
+        A0, A1, A2, PR = A0 * fl, A1 * fl, A2 * fl, PR * fl
+        c0 = abs(p0) * fl + gamma * A0
+        c1 = abs(p1) / fl - gamma * A1
+        c2 = abs(p2) * fl + gamma * A2
+        if c1 <= 0:
+            return None
+        base = max(c0 / c1, mpmath.mpf(2) ** (-(prec - 8)) * R)
+        for t in (1.125, 1.5, 2, 4, 16):
+            r = base * t
+            x = d * r / R
+            tail = PR * x ** 3 * mpmath.exp(x) / 6
+            if c1 * r > (c0 + c2 * r * r + tail) * (1 + mpmath.mpf(2) ** -30):
+                out.append(r)
+                break
+        else:
+            return None
+    # pairwise disjoint discs (in the working precision; the centres are exact)
+    for i in range(d):
+        for j in range(i):
+            if abs(z[i] - z[j]) <= (out[i] + out[j]) * (1 + mpmath.mpf(2) ** -30):
+                return None
+    return out
 
 
 def _mpf_to_fraction(x) -> Fraction:
@@ -272,13 +348,24 @@ def _hp_roots(p: IntPolynomial):
     if d < 1:
         raise ValueError("find_roots requires degree >= 1")
     z0 = _initial_roots(coeffs)
+
+    def certified(res):
+        # the discs must also decide real roots vs conjugate pairs
+        if res is None:
+            return None
+        try:
+            _pair_up(*res[:5])
+        except NonConvergence:
+            return None
+        return res
+
     res = None
     if max(abs(c) for c in coeffs).bit_length() <= 100:
         res = _polish_dd(coeffs, z0)
         if res is not None:
-            res = tuple(res) + (None,)
+            res = certified(tuple(res) + (None,))
     if res is None:
-        res = _polish_mp(coeffs, z0)
+        res = certified(_polish_mp(coeffs, z0))
     if res is None:
         # float seeds too far off (real roots seeded ~0.5 off the axis for
         # 142-bit coefficients): multiprecision seeds, then the same polish
@@ -289,36 +376,76 @@ def _hp_roots(p: IntPolynomial):
             try:
                 rts = mpmath.polyroots([mpmath.mpf(c) for c in reversed(coeffs)], maxsteps=400,
                                        extraprec=bits + 200)
-                res = _polish_mp(coeffs, np.array([complex(r) for r in rts]))
+                res = certified(_polish_mp(coeffs, np.array([complex(r) for r in rts])))
             except mpmath.libmp.libhyper.NoConvergence:
                 res = None
     if res is None:
-        raise NonConvergence("root polish did not converge")
+        raise NonConvergence("root polish did not converge to certified inclusion discs")
     return res
 
 
 def _pair_up(re_hi, re_lo, im_hi, im_lo, err):
-    """Classify real roots / conjugate pairs from polished roots."""
+    """Classify the certified roots into real roots and conjugate pairs.
+
+    The discs D(z_i, err_i) are pairwise disjoint and hold one root each
+    (rfr_polish_roots / _mp_inclusion_radii), so every root of p lies in
+    exactly one of them.  The conjugate of root i is a root in the mirrored
+    disc conj(D_i); when conj(D_i) meets no disc but D_b, the conjugate is
+    root b.  So: real iff D_i meets the real axis and conj(D_i) meets no
+    other disc (then conj(root_i) = root_i); a pair (a, b) iff D_a misses the
+    axis (root_a is not real) and conj(D_a) meets D_b alone.  Anything else
+    is undecided at this precision: NonConvergence, and the caller escalates.
+    The reported real root is Re(z_i), within err_i of the real root (the
+    projection onto the axis does not increase the distance)."""
     d = len(re_hi)
-    reals, uppers, lowers = [], [], []
+    re = np.asarray(re_hi, dtype=np.float64)
+    im = np.asarray(im_hi, dtype=np.float64)
+    rl = np.zeros(d) if re_lo is None else np.asarray(re_lo, dtype=np.float64)
+    il = np.zeros(d) if im_lo is None else np.asarray(im_lo, dtype=np.float64)
+    r = np.asarray(err, dtype=np.float64)
+
+    def gap(sign):
+        # |z_i - z_j| (sign +1) or |conj(z_i) - z_j| (sign -1) from both words,
+        # less a bound on its rounding: the high-word difference is exact for
+        # close values (Sterbenz) and every other step errs by 2^-53 relative
+        # to what it computes, so roots 1e-8 apart at |z| ~ 1e8 still separate
+        dh = re[:, None] - re[None, :]
+        dl = rl[:, None] - rl[None, :]
+        eh = sign * im[:, None] - im[None, :]
+        el = sign * il[:, None] - il[None, :]
+        dist = np.hypot(dh + dl, eh + el)
+        fuzz = 2.0 ** -50 * (np.abs(dh) + np.abs(dl) + np.abs(eh) + np.abs(el)) + 1e-300
+        return dist - fuzz
+
+    rsum = (r[:, None] + r[None, :]) * (1.0 + 1e-9)
+    own = gap(1.0)
+    np.fill_diagonal(own, np.inf)
+    if np.any(own <= rsum):
+        raise NonConvergence("inclusion discs overlap")  # pairwise disjoint, else undecided
+    meets = gap(-1.0) <= rsum  # conj(D_i) meets D_j
+    reals, uppers = [], []
+    partner = {}
     for i in range(d):
-        im = abs(im_hi[i])
-        if im <= 8.0 * err[i] + 1e-300:
+        hits = np.flatnonzero(meets[i])
+        on_axis = abs(im[i] + il[i]) <= r[i] * (1.0 + 1e-9) + 2.0 ** -50 * abs(im[i])
+        if on_axis:
+            if len(hits) != 1 or hits[0] != i:
+                raise NonConvergence(f"root {i}: cannot separate it from its mirror image")
             reals.append(i)
-        elif im_hi[i] > 0:
+            continue
+        if len(hits) != 1 or hits[0] == i:
+            raise NonConvergence(f"root {i}: no unique conjugate partner")
+        partner[i] = int(hits[0])
+        if im[i] > 0:
             uppers.append(i)
-        else:
-            lowers.append(i)
-    if len(uppers) != len(lowers):
-        raise UnpairedComplexRoot(f"{len(uppers)} upper vs {len(lowers)} lower half-plane roots")
     pairs = []
-    free = list(lowers)
     for u in uppers:
-        best = min(free, key=lambda v: abs(complex(re_hi[v] - re_hi[u], im_hi[v] + im_hi[u])))
-        if abs(complex(re_hi[best] - re_hi[u], im_hi[best] + im_hi[u])) > 1e-6 * max(1.0, abs(complex(re_hi[u], im_hi[u]))):
-            raise UnpairedComplexRoot(f"no conjugate partner for root {complex(re_hi[u], im_hi[u])}")
-        free.remove(best)
-        pairs.append((u, best))
+        b = partner[u]
+        if partner.get(b) != u or im[b] >= 0:
+            raise UnpairedComplexRoot(f"no conjugate partner for root {complex(re[u], im[u])}")
+        pairs.append((u, b))
+    if 2 * len(pairs) + len(reals) != d:
+        raise UnpairedComplexRoot(f"{len(uppers)} upper half-plane roots, {d - len(reals)} non-real")
     return reals, pairs
 
 
@@ -418,9 +545,11 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         keys1=np.asarray(keys1, dtype=np.uint64),
         keys2=np.asarray(keys2, dtype=np.uint64),
         keys3=np.asarray(keys3, dtype=np.uint64),
-        key_err1=int(math.ceil(e1)),
-        key_err2=int(math.ceil(e2)),
-        key_err3=int(math.ceil(min(e3, 2.0**66))),
+        # the float sums above round to nearest: a relative 2^-40 and one unit
+        # keep them upper bounds (Lemma 2)
+        key_err1=int(math.ceil(e1 * (1 + 2.0**-40))) + 1,
+        key_err2=int(math.ceil(e2 * (1 + 2.0**-40))) + 1,
+        key_err3=int(math.ceil(min(e3 * (1 + 2.0**-40), 2.0**66))) + 1,
         root_err=root_err,
         hp_real=tuple(ex_vals[k] for k in real_rows) if exact is not None else None,
         hp_pair=tuple(ex_vals[k] for k in pair_rows) if exact is not None else None,

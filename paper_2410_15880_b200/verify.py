@@ -49,13 +49,9 @@ from .errors import NonConvergence, RecombineDeviceError
 from .rootfinder import RootProfile, ToleranceConfig, hp_profile
 
 _STRIDE = 65  # smaller side degree <= 64
-# window half-width = KEY_SAFETY * (summed key error bounds) + slack.  The
-# per-root bounds are a-posteriori estimates (2 |p| / |p'|) that ill-conditioned
-# roots were seen to exceed 2-4x (a randomised sweep: d = 110, and a Tr3 window
-# that dropped a true factor with 10^6 coefficients), so the margin is wide; a
-# wider window only admits more (cheaply rejected) raw hits.
-KEY_SAFETY = 16
-KEY_SAFETY3 = 64  # the Tr3 window is a filter in front of verification: wider still
+# The key windows are rigorous (Lemmas 1-2): every root lies
+# in a certified inclusion disc, so the key sum of every true factor is within
+# key_err of 0 -- no safety factor on top.
 
 
 @dataclass
@@ -113,7 +109,8 @@ def _search_window(prof: RootProfile) -> tuple[np.ndarray, int]:
     k1 = np.asarray(prof.keys1, dtype=np.uint64)
     k2 = np.asarray(prof.keys2, dtype=np.uint64)
     keys = k1 + k2  # uint64 addition wraps: the sum mod 2^64
-    T = KEY_SAFETY * (prof.key_err1 + prof.key_err2) + prof.n + 64
+    # Lemma 2: |sum of a true factor's combined keys| <= key_err1 + key_err2
+    T = prof.key_err1 + prof.key_err2
     return keys, T
 
 
@@ -122,7 +119,7 @@ def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
     or (None, 0) for a profile without them."""
     if prof.keys3 is None:
         return None, 0
-    return prof.keys3, KEY_SAFETY3 * prof.key_err3 + prof.n + 64
+    return prof.keys3, prof.key_err3
 
 
 _PRIMES: tuple[int, ...] | None = None
