@@ -234,7 +234,11 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   g_buckets_planned = 0;
   // RFR_FORCE_JOIN (tests): keep small searches on the quarter-list join so
   // the oracle parity tests cover both paths
-  if (nshards == 1 && n >= 2 && n <= kExhaustiveMaxN && !getenv("RFR_FORCE_JOIN")) {
+  // RFR_FORCE_EXHAUSTIVE (tests): the exhaustive kernel up to n = 44, the
+  // independent checker of the join's hit set at production geometry
+  const bool small = n <= kExhaustiveMaxN && !getenv("RFR_FORCE_JOIN");
+  const bool forced = n <= kExhaustiveForceMaxN && getenv("RFR_FORCE_EXHAUSTIVE") != nullptr;
+  if (nshards == 1 && n >= 2 && (small || forced)) {
     // small search: every folded pattern in one launch (same hit set as the join)
     *nwin = 1;
     *r_bits = 0;

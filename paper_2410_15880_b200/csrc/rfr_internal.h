@@ -24,6 +24,7 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
                              unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
                              const unsigned long long* d_begin = nullptr);
 constexpr int kExhaustiveMaxN = 27;  // search_core: exhaustive kernel at or below this width (break-even with the join ~28)
+constexpr int kExhaustiveForceMaxN = 44;  // RFR_FORCE_EXHAUSTIVE (tests): up to 2^43 patterns, ~1 s
 cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
                               uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
                               cudaStream_t s);
