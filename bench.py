@@ -17,13 +17,16 @@ own split, FactorStats.root_seconds).
   roofline  the bucket-join kernel against the HBM copy peak, with the
           algorithmic bytes of SURVEY.md s8(d): 48 B per folded half-list
           record (DESIGN.md s6 explains why the kernel moves ~0 of them).
-  cpu_baseline  the reference's backend-e search (oracle/ port of
-          recombine.py:297-358) on C3 seed 2, bounded sample, scaled.
+  cpu_baseline  the reference's own factor() path on all host threads
+          (oracle/ref_arm.c: parallel_recombine_e, canonical filter, ordered
+          verification loop, recursion) on the reference's own root profiles
+          of the same five inputs (tests/golden/ref_c3.json), eps = 1e-11.
 
 Multi-GPU (torchrun, one rank per GPU): the search of every step is split
 into key-range shards, one per rank; candidates are all-gathered over NCCL;
 time is the max over ranks (strong scaling of one factorization).
-`--impl reference` times the reference's CPU path (the port) instead.
+`--impl reference` times the reference's CPU path (the same port, every step,
+seeds in the same rotation) instead; it never loads the product library.
 """
 from __future__ import annotations
 
@@ -234,7 +237,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---- timed: device-resident pipeline, one CUDA-event pair per step
-    times, joins, lists, ns = [], [], [], []
+    times, joins, lists, ns, recs, blists, bjoin = [], [], [], [], [], [], []
     launches = 0
     clocks = ClockSampler(local)
     with clocks:
@@ -255,6 +258,9 @@ def run_ours(args):
             joins.append(st.ms_join)
             lists.append(st.ms_lists)
             ns.append(item[3].n)
+            recs.append(st.visited)
+            blists.append(st.bytes_lists)
+            bjoin.append(st.bytes_join)
             launches += int(st.launches) + 1  # search kernels + one verification launch
     t_dev = np.array(times)
     if dist is not None:
@@ -325,15 +331,45 @@ def run_ours(args):
         c4_ms = min(best)
         c4_pairs = 2.0 ** (prof4.n - 1) / (c4_ms * 1e-3)
 
+    # ---- factor() end to end on C4 (irreducible: the whole space) and C5
+    # (Swinnerton-Dyer f6, n = 64): the 1-GPU anchors of the scaling configs
+    anchors = {}
+    if not args.no_c4 and not args.no_e2e:
+        with open(os.path.join(ROOT, "tests", "golden", "big_inputs.json")) as fh:
+            big = json.load(fh)
+        from paper_2410_15880_b200 import IntPolynomial
+
+        for tag, p in (("c4", c4[0][1]), ("c5", IntPolynomial([int(x) for x in big["c5"][0]["p"]]))):
+            res = factor(p, workers=max(1, world))  # warm-up, roots cached
+            runs = []
+            for _ in range(3):
+                if dist is not None:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = factor(p, workers=max(1, world))
+                torch.cuda.synchronize()
+                runs.append((time.perf_counter() - t0 - res.stats.root_seconds) * 1e3)
+            assert res.irreducible and res.certificate
+            ms = float(np.median(runs))
+            if dist is not None:
+                tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                ms = float(tt.item())
+            anchors[tag] = {"factor_e2e_ms": round(ms, 3), "n": res.stats.n,
+                            "candidates": res.stats.candidates,
+                            "pairs_per_s": 2.0 ** (res.stats.n - 1) / (ms * 1e-3)}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    mean_n = float(np.mean(ns))
     join_ms = float(np.mean(joins))
+    list_ms = float(np.mean(lists))
     alg = float(np.mean([algorithmic_bytes(n) for n in ns]))
     peak, peak_kind = peaks()
+    spec = 8000.0  # GB/s, the north star's "~8 TB/s"
     achieved = alg / (join_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -341,7 +377,33 @@ def run_ours(args):
             traffic = json.load(fh).get("dram_bytes_per_launch")
     except Exception:
         pass
-    pairs = float(np.mean([2.0 ** (n - 1) / (j * 1e-3) for n, j in zip(ns, [jl + ll for jl, ll in zip(joins, lists)])]))
+    search = [jl + ll for jl, ll in zip(joins, lists)]
+    pairs = float(np.mean([2.0 ** (n - 1) / (t * 1e-3) for n, t in zip(ns, search)]))
+    keys_per_s = float(np.mean([r / (t * 1e-3) for r, t in zip(recs, search)]))
+
+    def gbps(b, ms):
+        g = float(np.mean(b)) / (ms * 1e-3) / 1e9
+        return {"ms": round(ms, 4), "bytes_per_launch": float(np.mean(b)), "GBps": round(g, 1),
+                "frac_measured_peak": round(g / peak, 4), "frac_8TBps": round(g / spec, 4)}
+
+    phases = {
+        "lists": gbps(blists, list_ms),
+        "join": gbps(bjoin, join_ms),
+        "note": "HBM bytes each phase moves by design (rfr_stats.bytes_lists / bytes_join: "
+                "8 B read + 8 B write per list entry per doubling level; one 8-byte inner "
+                "key per join record) over its device time.  The join is bound by instruction "
+                "issue, not HBM: issue_frac below.",
+    }
+    try:  # warp instructions per join record, from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "join_issue.json")) as fh:
+            ji = json.load(fh)
+        clk = clocks.summary().get("sm_mhz") or 1965.0
+        nsm = lib.rfr_num_sms()
+        inst = ji["warp_inst_per_record"] * float(np.mean(recs))
+        phases["join"]["issue_frac"] = round(inst / (join_ms * 1e-3 * nsm * 4 * clk * 1e6), 4)
+        phases["join"]["issue_source"] = ji.get("source")
+    except Exception:
+        pass
     line = {
         "metric": METRIC,
         "value": round(value, 4),
@@ -355,18 +417,20 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic: reference generator inputs gen_random_reducible_parts(100, 100, seeds 0-4)",
-        "config": {
-            "workload": "C3 d=100 random reducible (two degree-50 factors, coeffs in [-100,100]), seeds 0-4 in rotation",
-            "n": sorted(set(ns)),
-            "key_window": "exact 64-bit first+second power-sum keys, +-T from root error bounds",
+        "config": workload_config([prep[k][3].n for k in range(len(prep))]),
+        "notes": {
+            "key_window": "exact 64-bit first+second power-sum keys, +-T from rigorous root inclusion radii",
             "value_scope": "device-resident keys, whole pattern space searched (no early "
                            "termination: the cost of an irreducible input) + verification",
-            "l2": "256 MB buffer written between timed steps (flush); the inner quarter lists (2^23-2^24 entries, 12 B each, per half) exceed L2 and are streamed from HBM",
+            "l2": "256 MB buffer written between timed steps (flush); the inner quarter lists "
+                  "(2^23-2^24 entries per half) exceed L2 and are streamed from HBM",
             "parallelism": f"key-range shards x{world}" if world > 1 else "1 GPU",
         },
-        "search_ms": round(float(np.mean(np.array(joins) + np.array(lists))), 4),
+        "search_ms": round(float(np.mean(search)), 4),
         "join_ms": round(join_ms, 4),
         "pairs_per_s": pairs,
+        "keys_per_s": keys_per_s,
+        "phases": phases,
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),
@@ -374,8 +438,11 @@ def run_ours(args):
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
+            "traffic_source": "profiles/join_traffic.json (ncu --set full, dram bytes per join launch)",
             "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": alg,
+            "note": "SURVEY s8(d) algorithmic bytes: 48 B per folded half-list record (what a "
+                    "sort-based MITM moves); the join moves ~8 B per record (phases.join)",
         },
         "e2e": {"value": round(e2e, 4), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
@@ -386,68 +453,120 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "c4": {"workload": "C4 d=120 irreducible seed 0 (n=63), search only",
-               "ms": c4_ms, "pairs_per_s": c4_pairs},
+               "ms": c4_ms, "pairs_per_s": c4_pairs, **anchors.get("c4", {})},
+        "c5": {"workload": "C5 Swinnerton-Dyer f6 (n=64), factor() e2e", **anchors.get("c5", {})},
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(prep[2][3], threads=1)
+        line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
 
 
 # -------------------------------------------------------- CPU baseline
-def cpu_baseline(prof, threads: int = 1, frac_log: int = 3):
-    """The reference's backend-e search (splat + stream, recombine.py:
-    297-358, ported in oracle/rfr_oracle.c) on the C3 seed-2 instance
-    (n = 52): the full splat of the B half and 1/2^frac_log of the A queries,
-    the query time scaled to all 2^26 queries.  eps = 1e-11 (the setting at
-    which the reference's C3 run is feasible).  Verification of
-    the resulting ~10^5 candidates (minutes in the reference) is not
-    included, so this is a lower bound on the reference's ms/factorization."""
+REF_EPS = 1e-11  # the tolerance at which the reference completes d = 100
+
+
+def load_ref_cases():
+    """The reference's own inputs for C3: its root profiles of p and of both
+    factors, and its factor() counters at eps = 1e-11 (frozen by running the
+    reference in the build container: tests/golden/make_ref_c3.py)."""
+    with open(os.path.join(ROOT, "tests", "golden", "ref_c3.json")) as fh:
+        cases = {c["seed"]: c for c in json.load(fh)["cases"]}
+    out = {}
+    for seed, c in cases.items():
+        profiles = {tuple(int(x) for x in c["p"]): c["profile"]}
+        for pc, pr in zip(c["pieces"], c["piece_profiles"]):
+            profiles[tuple(int(x) for x in pc)] = pr
+        out[seed] = (c, profiles)
+    return out
+
+
+def ref_factor_ms(case, threads: int):
+    """One factorization through the reference's path on host threads
+    (oracle/ref_arm.py: parallel_recombine_e, the ordered verification loop,
+    recursion on both pieces), from the reference's own profiles; checked
+    against the reference's factors and FactorStats counters.  Returns
+    (ms, stats)."""
+    from oracle import ref_arm
+
+    c, profiles = case
+    st = {}
+    t0 = time.perf_counter()
+    fs = ref_arm.factor_port(c["p"], profiles, REF_EPS, threads, st)
+    ms = (time.perf_counter() - t0) * 1e3
+    assert sorted(fs) == sorted([[int(x) for x in f] for f in c["factors"]]), "reference port: wrong factors"
+    assert (st["candidates"], st["rejected"]) == (c["stats"]["candidates"], c["stats"]["rejected"]), \
+        "reference port: counters differ from the reference's"
+    return ms, st
+
+
+def ref_threads() -> int:
     from oracle import recombine_oracle as O
 
-    L = O.lib()
-    L.orc_set_threads(threads)
-    rho = prof.rho
-    n = len(rho)
-    na = n // 2
-    q_hi = 1 << (na - frac_log)
-    t0 = time.perf_counter()
-    raw, st = O.c_recombine_e_port(rho, 1e-11, 0, q_hi)
-    wall = time.perf_counter() - t0
-    est = st["splat_s"] + st["query_s"] * (1 << frac_log)
-    enum = wall - st["splat_s"] - st["query_s"]  # subset sums + table init (full size)
-    est_ms = (est + enum) * 1e3
+    return O.lib().orc_num_threads()
+
+
+REF_SAMPLE = ("factor(p, ToleranceConfig(eps=1e-11), workers=all host threads) of the reference, "
+              "replayed in C threads (oracle/ref_arm.c: parallel_recombine_e R/parallel.py:255-272, "
+              "canonical filter, ordered build_candidate/trace_test/round_and_divide loop, recursion "
+              "on both pieces R/verify.py:246-286) from the reference's own root profiles "
+              "(tests/golden/ref_c3.json); root finding excluded as in the GPU arm; counters "
+              "(candidates, rejected) equal the reference's own at every step; eps = 1e-11 because "
+              "the reference cannot run d = 100 at its default 1e-6 (~3.6e10 candidates)")
+
+
+def cpu_baseline(seeds=(0, 1, 2, 3, 4)):
+    """The reference arm's factorizations of one seed rotation (one per C3
+    input, all host threads): ms per factorization."""
+    cases = load_ref_cases()
+    T = ref_threads()
+    ms = [ref_factor_ms(cases[s], T)[0] for s in seeds]
     return {
-        "value": round(est_ms, 1),
+        "value": round(float(np.mean(ms)), 1),
         "unit": UNIT,
-        "cores": L.orc_num_threads() if threads == 0 else threads,
+        "cores": T,
         "kind": "port",
-        "sample": (f"backend-e search port on C3 seed 2 (n={n}, eps=1e-11): full splat of 2^{n - na} "
-                   f"B values + 2^{na - frac_log} of 2^{na} A queries, query time x{1 << frac_log}; "
-                   "verification excluded"),
-        "measured_s": round(wall, 2),
+        "sample": f"one factorization of each C3 seed {list(seeds)}: " + REF_SAMPLE,
+        "per_seed_ms": [round(v, 1) for v in ms],
+    }
+
+
+def workload_config(ns):
+    """The config both arms report (identical by construction)."""
+    return {
+        "workload": "C3: d=100 random reducible, gen_random_reducible_parts(100, 100, seed) "
+                    "(two degree-50 factors, coeffs in [-100,100]), seeds 0-4 in rotation, one "
+                    "factorization per step, root finding excluded",
+        "n": sorted(set(int(v) for v in ns)),
+        "seeds": [0, 1, 2, 3, 4],
     }
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path for this metric (the port),
-    all host threads for the query sweep, rank 0 only."""
+    """--impl reference: the reference's CPU path for this metric on the
+    box's host cores (all threads), rank 0 only; the same seeds, config,
+    metric and unit as the GPU arm.  Warm-up steps factor seed 2 (the
+    smallest, n = 52); the K timed steps rotate seeds 0-4 exactly as the GPU
+    arm does."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2410_15880_b200.verify import _profile_cached
-
-    c3, _ = load_inputs()
-    prof = _profile_cached(c3[2][1].coeffs)
-    steps = []
-    for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(prof, threads=0, frac_log=3)
-        if s >= args.warmup:
-            steps.append(cb["value"])
-    v = float(np.mean(steps))
-    cb["value"] = round(v, 1)
+    cases = load_ref_cases()
+    T = ref_threads()
+    # BENCH_REF_SEEDS (CPU tests only): a shorter rotation
+    seeds = [int(x) for x in os.environ.get("BENCH_REF_SEEDS", "0,1,2,3,4").split(",")]
+    for _ in range(max(3, args.warmup)):
+        ref_factor_ms(cases[2], T)
+    times, phases = [], {"search_s": 0.0, "verify_s": 0.0}
+    for s in range(args.steps):
+        ms, st = ref_factor_ms(cases[seeds[s % len(seeds)]], T)
+        times.append(ms)
+        phases["search_s"] += st["search_s"]
+        phases["verify_s"] += st["verify_s"]
+    v = float(np.mean(times))
+    ns = [len(cases[s][0]["profile"]["rho"]) for s in range(5)]
     print(json.dumps({
         "impl": "reference",
         "metric": METRIC,
@@ -455,17 +574,42 @@ def run_reference(args):
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
-        "warmup": args.warmup,
+        "warmup": max(3, args.warmup),
         "ms_per_step": round(v, 1),
         "higher_is_better": False,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: reference generator input, C3 seed 2",
-        "config": {"workload": "C3 d=100 seed 2 (n=52), reference backend-e search (port), eps=1e-11"},
-        "cpu_baseline": cb,
+        "data": "synthetic: reference generator inputs gen_random_reducible_parts(100, 100, seeds 0-4)",
+        "config": workload_config(ns),
+        "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": T, "kind": "port",
+                         "sample": f"{args.steps} timed steps, seeds 0-4 in rotation: " + REF_SAMPLE},
         "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_ms_per_step": {k: round(x * 1e3 / args.steps, 1) for k, x in phases.items()},
+        "per_step_ms": [round(t, 1) for t in times],
+        "native_so_loaded": loaded_repo_libs(),
     }))
+
+
+def loaded_repo_libs():
+    """Shared objects of this repository mapped into the process (the
+    reference arm must show oracle/ only: no product library)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            paths = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT))
+
+
+def self_launch(n: int) -> int:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run
+    with N ranks (one per GPU) and pass its exit code through."""
+    import random
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + random.randint(0, 2000))]
+    return subprocess.call(cmd + [os.path.abspath(__file__)] + sys.argv[1:])
 
 
 def main():
@@ -480,6 +624,12 @@ def main():
                     help="skip the factor() leg (profiling runs: under ncu the early-exit "
                          "poller cannot run beside the join)")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        sys.exit(self_launch(args.gpus))
+    if world is not None and int(world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

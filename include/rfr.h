@@ -65,6 +65,13 @@ typedef struct rfr_stats {
   int64_t buckets_planned; /* buckets the call set out to search; buckets < this     */
                            /* means the pattern space was not exhausted               */
   int64_t early_stop;      /* rfr_search_verify: the join stopped at a verified hit   */
+  int32_t list_bits[4];    /* quarter-list widths of the plan: A outer, A inner,       */
+                           /* B outer, B inner (0 for the exhaustive kernel)           */
+  int64_t bytes_lists;     /* HBM bytes the list build moves by design: 12 B per base- */
+                           /* level entry, then 8 B read + 8 B write per entry of      */
+                           /* every doubling level (each level reads its input twice)  */
+  int64_t bytes_join;      /* HBM bytes the join streams by design: one 8-byte inner   */
+                           /* key per record of this shard's buckets                   */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */
@@ -188,6 +195,36 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
                       int stride, int64_t cap, int early_exit, int64_t* nout, rfr_stats* st);
+
+/*
+ * One rank's share of a sharded fused search (the multi-GPU form of
+ * rfr_search_verify, replacing parallel_recombine_e + the verification loop
+ * on `nshards` workers, R/parallel.py:255-272, R/verify.py:236-284): the
+ * buckets [shard 2^r / nshards, (shard+1) 2^r / nshards) of the same folded
+ * pattern space; the union over shards is rfr_search_verify's output.  With
+ * early_exit, a verified hit of this shard stops this rank's join AND, once
+ * rfr_peer_connect has run, every other rank's join (their stop flags are
+ * written over NVLink); a rank stopped by a peer returns with buckets <
+ * buckets_planned, the rank that found the factor searches its pieces as
+ * rfr_search_verify does.
+ */
+int rfr_search_verify_shard(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
+                            const uint64_t* keys2, uint64_t lo2, uint64_t width2,
+                            const rfr_profile* prof, const uint64_t* p_mod, int d, uint64_t* pats,
+                            uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride, int64_t cap,
+                            int early_exit, int shard, int nshards, int64_t* nout, rfr_stats* st);
+
+/*
+ * Cross-rank early exit (no reference counterpart: its workers share one
+ * process).  rfr_peer_handle writes this process's 64-byte CUDA IPC handle of
+ * its search counters (which hold the stop flag); the ranks all-gather the
+ * handles (torch.distributed) and each calls rfr_peer_connect(handles[nranks
+ * * 64], nranks, self) to map the others' flags.  rfr_peer_disconnect (and
+ * rfr_shutdown) unmap them.
+ */
+int rfr_peer_handle(void* handle64);
+int rfr_peer_connect(const void* handles, int nranks, int self);
+int rfr_peer_disconnect(void);
 
 /* The three primes of the modular division test (p_mod residues). */
 int rfr_verify_primes(uint64_t* primes3);

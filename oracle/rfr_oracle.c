@@ -38,6 +38,8 @@
 #include <time.h>
 #include <unistd.h>
 
+#include "rfr_oracle.h"
+
 static double now_s(void) {
   struct timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -340,7 +342,7 @@ int64_t orc_recombine_e_port(const double *rho, int n, double eps, int64_t q_lo,
 
 /* ---- verification restatement, R/verify.py:48-155 ----------------------- */
 
-typedef long double ld;
+/* ld: long double (rfr_oracle.h) */
 
 /*
  * build_candidate (R/verify.py:60-120): multiply out the selected reals and

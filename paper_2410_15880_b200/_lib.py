@@ -32,6 +32,10 @@ EXPORTS = (
     "rfr_search_keys",
     "rfr_search_keys2",
     "rfr_search_verify",
+    "rfr_search_verify_shard",
+    "rfr_peer_handle",
+    "rfr_peer_connect",
+    "rfr_peer_disconnect",
     "rfr_search_keys_dev",
     "rfr_verify",
     "rfr_verify_primes",
@@ -61,10 +65,15 @@ class RfrStats(ctypes.Structure):
         ("launches", ctypes.c_int64),
         ("buckets_planned", ctypes.c_int64),
         ("early_stop", ctypes.c_int64),
+        ("list_bits", ctypes.c_int32 * 4),
+        ("bytes_lists", ctypes.c_int64),
+        ("bytes_join", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        out = {name: getattr(self, name) for name, _ in self._fields_}
+        out["list_bits"] = list(self.list_bits)
+        return out
 
 
 class RfrProfile(ctypes.Structure):
@@ -147,6 +156,15 @@ def load():
             ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
             I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, I64_P, ctypes.POINTER(RfrStats),
         ]
+        L.rfr_search_verify_shard.argtypes = [
+            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
+            ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
+            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, I64_P,
+            ctypes.POINTER(RfrStats),
+        ]
+        L.rfr_peer_handle.argtypes = [ctypes.c_void_p]
+        L.rfr_peer_connect.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.rfr_peer_disconnect.argtypes = []
         L.rfr_verify_primes.argtypes = [U64_P]
         L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]
         L.rfr_squarefree_mod.argtypes = [U64_P, ctypes.c_int, ctypes.c_uint64]

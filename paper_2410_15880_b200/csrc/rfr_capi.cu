@@ -64,6 +64,10 @@ struct Ctx {
   size_t h_stage_bytes = 0;
   void* h_piece = nullptr;       // pinned staging of the pieces' searches after an early stop
   size_t h_piece_bytes = 0;
+  // cross-rank early exit: the other ranks' DevCounters.found, opened by IPC
+  void* peer_base[kMaxPeers] = {};
+  unsigned long long* peer_found[kMaxPeers] = {};
+  int npeers = 0;
   // cache of the last built lists (key values + plan geometry)
   std::vector<uint64_t> built_keys;
   int built_bits[4] = {-1, -1, -1, -1};
@@ -226,12 +230,14 @@ struct EarlyExit {
 // recovered here, filter and verification by the caller).
 int g_launches = 0;                // kernels launched by the last search_core call
 int64_t g_buckets_planned = 0;     // buckets the last search_core call set out to search
+int g_list_bits[4] = {0, 0, 0, 0}; // quarter-list widths of the last search_core plan
 
 int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int shard, int nshards,
                 uint64_t* d_out, unsigned long long cap, cudaStream_t s, int* r_bits,
                 int* nwin, bool time_it, const EarlyExit* ee = nullptr) {
   g_launches = 0;
   g_buckets_planned = 0;
+  for (int i = 0; i < 4; i++) g_list_bits[i] = 0;
   // RFR_FORCE_JOIN (tests): keep small searches on the quarter-list join so
   // the oracle parity tests cover both paths
   // RFR_FORCE_EXHAUSTIVE (tests): the exhaustive kernel up to n = 44, the
@@ -255,6 +261,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   int rc = make_plan(n, wins[0].first, wins[0].second, nshards, &P0);
   if (rc) return rc;
   *r_bits = P0.r;
+  for (int i = 0; i < 4; i++) g_list_bits[i] = P0.list[i].bits;
   rc = ensure_list_buffers(P0);
   if (rc) return rc;
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
@@ -335,6 +342,18 @@ void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin
   st->windows = nwin;
   st->launches = g_launches;
   st->buckets_planned = g_buckets_planned;
+  int64_t lb = 0;
+  for (int i = 0; i < 4; i++) {
+    st->list_bits[i] = g_list_bits[i];
+    const int b = g_list_bits[i], b0 = b < kBaseBits ? b : kBaseBits;
+    lb += 12ll << b0;                        // base level: key + pattern
+    if (b > b0) lb += 32ll * ((1ll << b) - (1ll << b0));  // doubling levels
+  }
+  st->bytes_lists = g_list_bits[1] + g_list_bits[3] ? lb : 0;
+  // records of the planned buckets (a bucket holds 2^-r of each folded half)
+  st->bytes_join = r_bits > 0 ? (int64_t)((double)st->visited * 8.0 *
+                                          (double)g_buckets_planned / (double)(1ull << r_bits))
+                              : 0;
 }
 
 // The profile's doubles packed for one H2D copy: [real_hi | real_lo | sum_hi |
@@ -505,6 +524,8 @@ int rfr_num_sms(void) { return g.nsm; }
 
 // Free everything the context holds (safe on a partially initialised one).
 static void release_ctx() {
+  for (int i = 0; i < g.npeers; i++) cudaIpcCloseMemHandle(g.peer_base[i]);
+  g.npeers = 0;
   if (g.stream) cudaStreamSynchronize(g.stream);
   DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts, &g.pkeys,
                     &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef};
@@ -713,11 +734,89 @@ int rfr_search_keys(const uint64_t* keys, int n, uint64_t lo, uint64_t width, in
 // Fused factor-mode search + verification: lists, join, secondary key window
 // and the verify kernel back to back on the device (the candidate patterns
 // never round-trip through the host); one staged H2D in, one batch of D2H out.
+namespace {
+int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
+                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
+                       int stride, int64_t cap, int early_exit, int shard, int nshards, int64_t* nout,
+                       rfr_stats* st);
+}  // namespace
+
 int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
                       int stride, int64_t cap, int early_exit, int64_t* nout, rfr_stats* st) {
   std::lock_guard<std::mutex> lk(g_mu);
+  return search_verify_impl(keys, n, lo, width, keys2, lo2, width2, prof, p_mod, d, pats, verdict, side,
+                            coeffs, stride, cap, early_exit, 0, 1, nout, st);
+}
+
+int rfr_search_verify_shard(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
+                            const uint64_t* keys2, uint64_t lo2, uint64_t width2,
+                            const rfr_profile* prof, const uint64_t* p_mod, int d, uint64_t* pats,
+                            uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride, int64_t cap,
+                            int early_exit, int shard, int nshards, int64_t* nout, rfr_stats* st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (nshards < 1 || shard < 0 || shard >= nshards) return rfr_fail(RFR_E_ARG, "bad shard");
+  return search_verify_impl(keys, n, lo, width, keys2, lo2, width2, prof, p_mod, d, pats, verdict, side,
+                            coeffs, stride, cap, early_exit, shard, nshards, nout, st);
+}
+
+// ---- cross-rank early exit: the ranks' stop flags over CUDA IPC -----------
+int rfr_peer_handle(void* handle) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if (!handle) return rfr_fail(RFR_E_ARG, "null handle");
+  cudaSetDevice(g.device);
+  cudaIpcMemHandle_t h;
+  RFR_CUDA_OK(cudaIpcGetMemHandle(&h, g.ctr.p));
+  memcpy(handle, &h, sizeof h);
+  return RFR_OK;
+}
+
+int rfr_peer_connect(const void* handles, int nranks, int self) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = ensure_ready();
+  if (rc) return rc;
+  if (!handles || nranks < 1 || self < 0 || self >= nranks || nranks - 1 > kMaxPeers)
+    return rfr_fail(RFR_E_ARG, "bad peer handles");
+  cudaSetDevice(g.device);
+  for (int i = 0; i < g.npeers; i++) cudaIpcCloseMemHandle(g.peer_base[i]);
+  g.npeers = 0;
+  for (int r = 0; r < nranks; r++) {
+    if (r == self) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)r * sizeof h, sizeof h);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int i = 0; i < g.npeers; i++) cudaIpcCloseMemHandle(g.peer_base[i]);
+      g.npeers = 0;
+      cudaGetLastError();
+      return rfr_fail_cuda(e, "cudaIpcOpenMemHandle");
+    }
+    g.peer_base[g.npeers] = p;
+    g.peer_found[g.npeers] = (unsigned long long*)((char*)p + offsetof(DevCounters, found));
+    g.npeers++;
+  }
+  return RFR_OK;
+}
+
+int rfr_peer_disconnect(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.ready) cudaSetDevice(g.device);
+  for (int i = 0; i < g.npeers; i++) cudaIpcCloseMemHandle(g.peer_base[i]);
+  g.npeers = 0;
+  return RFR_OK;
+}
+
+namespace {
+int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
+                       uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
+                       int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
+                       int stride, int64_t cap, int early_exit, int shard, int nshards, int64_t* nout,
+                       rfr_stats* st) {
   int rc = ensure_ready();
   if (rc) return rc;
   if ((rc = check_n(n))) return rc;
@@ -834,8 +933,12 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
     ee.V.side = (uint8_t*)(obase + q_side);
     ee.V.coeffs = (long long*)(obase + q_coef);
     ee.V.stride = stride;
-    rc = search_core(d_keys, n, lo, width, 0, 1, (uint64_t*)g.raw.p, raw_cap, s, &r_bits, &nwin, true,
-                     early_exit ? &ee : nullptr);
+    if (nshards > 1) {  // a sharded search also stops the other ranks' joins
+      for (int i = 0; i < g.npeers; i++) ee.V.peer_found[i] = g.peer_found[i];
+      ee.V.npeers = g.npeers;
+    }
+    rc = search_core(d_keys, n, lo, width, shard, nshards, (uint64_t*)g.raw.p, raw_cap, s, &r_bits,
+                     &nwin, true, early_exit ? &ee : nullptr);
     if (rc) return rc;
     const bool early = early_exit && nwin == 1;
     // the rest of the hits (all of them without early exit)
@@ -933,6 +1036,8 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
   }
   return RFR_OK;
 }
+
+}  // namespace
 
 int rfr_search_keys2(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                      uint64_t lo2, uint64_t width2, int shard, int nshards, uint64_t* out,

@@ -36,6 +36,8 @@ cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,
                            DevCounters* d_ctr, int nsm, cudaStream_t s);
 cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaStream_t s);
 
+constexpr int kMaxPeers = 8;  // ranks of one sharded search whose stop flags a poller raises
+
 // Batched candidate verification (rfr_verify.cu): one warp per candidate.
 struct VerifyArgs {
   int n, r, c, d;
@@ -52,6 +54,11 @@ struct VerifyArgs {
   const unsigned long long* m_dev;        // optional device count (<= m), or null
   const unsigned long long* m_begin_dev = nullptr;  // optional first candidate (chunked search)
   unsigned long long* found = nullptr;    // optional flag raised by a PASS (early exit)
+  // with found: the same flag of the other ranks' searches (their DevCounters
+  // opened through CUDA IPC, written over NVLink), so one rank's verified
+  // factor stops every rank's join at its next bucket boundary
+  unsigned long long* peer_found[kMaxPeers] = {};
+  int npeers = 0;
   const uint64_t* p_mod;  // 3 x (d+1)
   uint64_t primes[3];
   uint8_t* verdict;

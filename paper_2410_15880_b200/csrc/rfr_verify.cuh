@@ -264,7 +264,12 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
   for (int j = lane; j < e; j += 32) nz |= (B.rem[0][j] | B.rem[1][j] | B.rem[2][j]) != 0;
   const bool divides = !__any_sync(0xffffffffu, nz);
   if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
-  if (lane == 0 && divides && A.found) atomicExch(A.found, 1ull);
+  if (lane == 0 && divides && A.found) {
+    atomicExch(A.found, 1ull);
+    // cross-rank early exit: raise the peers' flags (P2P stores over NVLink)
+    for (int i = 0; i < A.npeers; i++) *(volatile unsigned long long*)A.peer_found[i] = 1ull;
+    if (A.npeers) __threadfence_system();
+  }
   if (divides)
     for (int j = lane; j <= e && j < A.stride; j += 32) A.coeffs[k * A.stride + j] = B.q[j];
 }

@@ -15,6 +15,10 @@ from __future__ import annotations
 
 import numpy as np
 
+import ctypes
+
+from . import _lib
+from .errors import RecombineDeviceError
 from .recombine import CandidateSet, RecombineStats, RhoVector, recombine_e, search_keys
 
 
@@ -26,6 +30,19 @@ def _dist():
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         return dist
     return None
+
+
+def _comm_device(dist):
+    """Where this rank's collective buffers live: its engine device for NCCL
+    (the device librfr searches on, RFR_DEVICE / LOCAL_RANK -- not whatever
+    torch.cuda.current_device() happens to be), the host for gloo."""
+    import torch
+
+    if dist.get_backend() == "nccl":
+        dev = _lib.device()
+        torch.cuda.set_device(dev)
+        return torch.device("cuda", dev)
+    return torch.device("cpu")
 
 
 def shard_ranges(nbuckets: int, nshards: int) -> list[tuple[int, int]]:
@@ -41,8 +58,7 @@ def allgather_patterns(local: np.ndarray) -> np.ndarray:
         return np.asarray(local, dtype=np.uint64)
     import torch
 
-    backend = dist.get_backend()
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    dev = _comm_device(dist)
     world = dist.get_world_size()
     cnt = torch.tensor([len(local)], dtype=torch.int64, device=dev)
     counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
@@ -98,3 +114,89 @@ def parallel_recombine_e(rho: RhoVector, eps: float, workers: int,
     for g in range(workers):
         pats |= recombine_e(rho, eps, stats, shard=g, nshards=workers).patterns
     return CandidateSet(frozenset(pats), len(rho))
+
+
+# ------------------------------------------------ sharded fused search
+_PEERS: dict = {}
+
+
+def connect_peers(dist) -> bool:
+    """Map the other ranks' stop flags (CUDA IPC handles of their search
+    counters, all-gathered once per process group): afterwards a rank whose
+    search verifies a factor stops every rank's join over NVLink.  False
+    (and no cross-rank stop, results unchanged) when a handle cannot be
+    exported or opened."""
+    key = (id(dist.group.WORLD), dist.get_world_size(), dist.get_rank())
+    if _PEERS.get("key") == key:
+        return _PEERS["ok"]
+    lib = _lib.load()
+    _lib.device()
+    world, rank = dist.get_world_size(), dist.get_rank()
+    h = ctypes.create_string_buffer(64)
+    mine = bytes(h.raw) if lib.rfr_peer_handle(h) == _lib.RFR_OK else None
+    handles = [None] * world
+    _comm_device(dist)
+    dist.all_gather_object(handles, mine)
+    ok = False
+    if all(x is not None for x in handles) and world - 1 <= 8:
+        buf = ctypes.create_string_buffer(b"".join(handles), 64 * world)
+        ok = lib.rfr_peer_connect(buf, world, rank) == _lib.RFR_OK
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    _PEERS.update(key=key, ok=ok, all=all(flags))
+    return ok
+
+
+def sharded_search_verify(prof, p, keys, half_width, keys3, half_width3, workers: int, fstats,
+                          early_exit: bool, max_rows=None):
+    """The fused search + verification (verify._search_and_verify) split into
+    `workers` key-range shards: this rank's shards on its GPU, a verified hit
+    stops every rank's join (connect_peers), then the rows (pattern, verdict,
+    side, coefficients) are all-gathered so every rank holds the same
+    candidates.  Without a process group the shards run one after another on
+    the local device and the first one that stops at a verified factor (and
+    searches its pieces) ends the loop.  Returns (pats, verdict, side, coeffs,
+    complete, stopped) like _search_and_verify: complete when every shard was
+    searched whole or a stopped shard searched its pieces (then the rows
+    cover every factor pattern)."""
+    from .verify import _search_and_verify
+
+    dist = _dist()
+    if dist is None:
+        world, rank = 1, 0
+    else:
+        world, rank = dist.get_world_size(), dist.get_rank()
+        connect_peers(dist)
+        dist.barrier()  # start together: a peer's stop flag lands in a running search
+    rows, err = [], None
+    for g in [g for g in range(workers) if g % world == rank]:
+        try:
+            res = _search_and_verify(prof, p, keys, half_width, keys3, half_width3, fstats.recombine,
+                                     early_exit, max_rows, shard=g, nshards=workers)
+        except RecombineDeviceError as e:
+            if "raw hits exceed" not in str(e):
+                raise
+            err = str(e)
+            break
+        rows.append(res)
+        if res[5]:  # stopped: this rank's or a peer's verified factor
+            if not (res[1] == _lib.V_PASS).any():
+                fstats.peer_stops += 1
+            break
+    if dist is not None:
+        parts = [None] * world
+        _comm_device(dist)
+        dist.all_gather_object(parts, (err, rows))
+        errs = [e for e, _ in parts if e]
+        rows = [r for _, rs in parts for r in rs]
+        err = errs[0] if errs else None
+    if err:
+        raise RecombineDeviceError(err)
+    stopped = any(r[5] for r in rows)
+    complete = any(r[5] and r[4] for r in rows) or (
+        all(r[4] for r in rows) and len(rows) == workers)
+    if not rows:
+        z = np.zeros(0, dtype=np.uint64)
+        return z, np.zeros(0, np.uint8), np.zeros(0, np.uint8), np.zeros((0, 65), np.int64), True, False
+    cat = [np.concatenate([r[k] for r in rows]) for k in range(4)]
+    return cat[0], cat[1], cat[2], cat[3], complete, stopped

@@ -69,6 +69,7 @@ class FactorStats:
     recombine: RecombineStats = field(default_factory=RecombineStats)
     host_verified: int = 0
     early_exits: int = 0  # searches stopped at a verified factor
+    peer_stops: int = 0  # sharded searches stopped by another rank's verified factor
 
 
 @dataclass(frozen=True)
@@ -208,7 +209,7 @@ _PIECES = True
 
 def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
                        keys3: np.ndarray, half_width3: int, stats, early_exit: bool,
-                       max_rows: int | None = None):
+                       max_rows: int | None = None, shard: int = 0, nshards: int = 1):
     """search_and_verify, optionally with early termination.  Returns (pats,
     verdict, side, coeffs, complete, stopped): stopped when the join ended at
     a verified hit; complete when the candidates nevertheless cover every
@@ -233,16 +234,17 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
         coeffs = np.empty((cap, _STRIDE), dtype=np.int64)
         nout = ctypes.c_int64(0)
         st = _lib.RfrStats()
-        _lib.check(
-            lib.rfr_search_verify(
-                _lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
+        args = (_lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
                 ctypes.byref(rp), _lib.ptr(pm, _lib.U64_P), p.degree, _lib.ptr(pats, _lib.U64_P),
                 verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
                 coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap,
-                (1 if _PIECES else 2) if early_exit else 0, ctypes.byref(nout),
-                ctypes.byref(st)),
-            "rfr_search_verify",
-        )
+                (1 if _PIECES else 2) if early_exit else 0)
+        if nshards > 1:
+            rc = lib.rfr_search_verify_shard(*args, shard, nshards, ctypes.byref(nout),
+                                             ctypes.byref(st))
+        else:
+            rc = lib.rfr_search_verify(*args, ctypes.byref(nout), ctypes.byref(st))
+        _lib.check(rc, "rfr_search_verify")
         if nout.value <= cap:
             break
         if max_rows is not None and nout.value > max_rows:
@@ -596,11 +598,20 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
     keys, T = _search_window(prof)
     keys3, T3 = _secondary_window(prof)
     complete, stopped = True, False
-    if workers == 1 and keys3 is not None:
+    if keys3 is not None:
         # one device call: search, Tr3 window and verification back to back
-        # (recombine_seconds then covers the device verification too)
-        search = lambda limit: _search_and_verify(  # noqa: E731
-            prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N, limit)
+        # (recombine_seconds then covers the device verification too); with
+        # workers > 1 every rank runs its key-range shards this way, a rank's
+        # verified factor stops the other ranks' joins, and the verified rows
+        # are all-gathered (parallel.sharded_search_verify)
+        if workers == 1:
+            search = lambda limit: _search_and_verify(  # noqa: E731
+                prof, p, keys, T, keys3, T3, stats.recombine, early_exit and n >= _EARLY_N, limit)
+        else:
+            from .parallel import sharded_search_verify
+
+            search = lambda limit: sharded_search_verify(  # noqa: E731
+                prof, p, keys, T, keys3, T3, workers, stats, early_exit and n >= _EARLY_N, limit)
         try:
             pats, verdict, side, coeffs, complete, stopped = search(1 << 16)
             flood = len(pats) > _FLOOD

@@ -1,6 +1,8 @@
-"""bench.py --impl reference (the driver's reference arm) on CPU: it times the
-reference's backend-e search port (oracle/, the one other place bench.py may
-run it) and prints one JSON line with the contract's keys."""
+"""bench.py --impl reference (the driver's reference arm) on CPU: it replays
+the reference's factor() path (oracle/ref_arm.c, the one other place bench.py
+may run oracle/) on the reference's own profiles, prints one JSON line with
+the contract's keys and the same config as the GPU arm, and never maps the
+product library (librfr.so)."""
 import json
 import os
 import subprocess
@@ -10,11 +12,11 @@ from conftest import ROOT
 
 
 def test_reference_arm_prints_the_contract_line():
-    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", BENCH_REF_SEEDS="2")
     out = subprocess.run(
         [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
          "--warmup", "1"],
-        capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -27,3 +29,16 @@ def test_reference_arm_prints_the_contract_line():
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     cb = line["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
+    # the product library is never loaded by the reference arm
+    assert line["native_so_loaded"] == ["oracle/liborc.so"], line["native_so_loaded"]
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert line["config"] == bench.workload_config([52, 54, 55, 55, 54])
+
+
+def test_bench_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                         capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
