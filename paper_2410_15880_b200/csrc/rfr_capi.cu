@@ -17,6 +17,8 @@
 
 #include "../../include/rfr.h"
 #include "rfr_common.cuh"
+#include <ctime>
+
 #include "rfr_internal.h"
 
 using namespace rfr;
@@ -25,6 +27,29 @@ using namespace rfr;
 namespace {
 
 std::mutex g_mu;
+
+// RFR_HOST_TRACE=1: host timestamps at the steps of a fused call, printed to
+// stderr when it returns (where the C host time of factor() goes).
+struct HostTrace {
+  int on = -1;
+  std::vector<std::pair<const char*, double>> marks;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+  }
+  void mark(const char* what) {
+    if (on < 0) on = getenv("RFR_HOST_TRACE") ? 1 : 0;
+    if (on) marks.emplace_back(what, now());
+  }
+  void dump() {
+    if (on != 1 || marks.empty()) return;
+    const double t0 = marks[0].second;
+    for (auto& m : marks) fprintf(stderr, "[rfr host] %8.1f us  %s\n", m.second - t0, m.first);
+    marks.clear();
+  }
+};
+HostTrace g_tr;
 thread_local std::string g_err;
 
 struct DevVec {
@@ -257,6 +282,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   }
   std::vector<std::pair<uint64_t, uint64_t>> wins = split_window(lo, width);
   *nwin = (int)wins.size();
+  g_tr.mark("search_core: plan");
   JoinPlan P0;
   int rc = make_plan(n, wins[0].first, wins[0].second, nshards, &P0);
   if (rc) return rc;
@@ -269,11 +295,14 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   char* hb[4];
   for (int i = 0; i < 4; i++) hb[i] = (char*)g.hist[i].p;
   const ListHist H = list_hist_layout(P0, hb);
+  g_tr.mark("search_core: lists launch");
   RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p, H, s));
+  g_tr.mark("search_core: lists enqueued");
   {
     int maxbits = 0;
     for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
-    g_launches += 1 + (maxbits > kBaseBits ? 2 * (maxbits - kBaseBits) : 0);
+    const int per_level = getenv("RFR_SPLIT_KERNEL") ? 2 : 1;  // split + merge, or the merge alone
+    g_launches += 1 + (maxbits > kBaseBits ? per_level * (maxbits - kBaseBits) : 0);
   }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
   DevCounters* d_ctr = (DevCounters*)g.ctr.p;
@@ -301,6 +330,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     RFR_CUDA_OK(launch_join_starts(P, final_bufs(P0), P.bucket_begin, P.bucket_end, 1, grid, d_rots,
                                    d_rots + mot, s));
     g_launches += 1;
+    g_tr.mark("search_core: join starts");
     if (early) {
       RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), s));  // kUnsetHit slots
       RFR_CUDA_OK(cudaEventRecord(g.ev_fork, s));
@@ -311,8 +341,10 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
       RFR_CUDA_OK(cudaEventRecord(g.ev_join, g.stream2));
       g_launches += 1;
     }
+    g_tr.mark("search_core: poller");
     RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, d_ctr, grid, s, d_rots, d_rots + mot, early));
     g_launches += 1;
+    g_tr.mark("search_core: join");
     if (early) RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_join, 0));
   }
   // the join emits quarter-list indices; rewrite every hit (the poller's
@@ -477,14 +509,22 @@ bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t 
     char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
     if (!ok(launch_keyfilter(dk + 64, ns, (const uint64_t*)g.raw.p, &d_ctr->out_count, raw_cap, lo2, width2,
                              d_post, post_cap, d_ctr, g.nsm, s), "piece keyfilter") ||
-        !ok(launch_deposit(d_post, &d_ctr->post_count, post_cap, M, g.nsm, s), "deposit") ||
-        !ok(launch_verify(A, s), "piece verify") ||
-        !ok(cudaMemcpyAsync(hp + 2 * 64 * 8, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "piece ctr") ||
-        !ok(cudaMemcpyAsync(rows, d_post, kPieceRows * 8, cudaMemcpyDeviceToHost, s), "piece pats") ||
-        !ok(cudaMemcpyAsync(rows + kPieceRows * 8, A.verdict, kPieceRows, cudaMemcpyDeviceToHost, s), "piece verdicts") ||
-        !ok(cudaMemcpyAsync(rows + kPieceRows * 9, A.side, kPieceRows, cudaMemcpyDeviceToHost, s), "piece sides") ||
-        !ok(cudaMemcpyAsync(rows + kPieceRows * 10, A.coeffs, kPieceRows * (size_t)stride * 8,
-                            cudaMemcpyDeviceToHost, s), "piece coeffs"))
+        !ok(launch_deposit(d_post, &d_ctr->post_count, post_cap, M, g.nsm, s), "deposit"))
+      return false;
+    CollectArgs C;
+    C.ctr = d_ctr;
+    C.pats = d_post;
+    C.verdict = A.verdict;
+    C.side = A.side;
+    C.coeffs = A.coeffs;
+    C.stride = stride;
+    C.rows = kPieceRows;
+    C.h_ctr = (DevCounters*)(hp + 2 * 64 * 8);
+    C.h_pats = (uint64_t*)rows;
+    C.h_verdict = (uint8_t*)(rows + kPieceRows * 8);
+    C.h_side = (uint8_t*)(rows + kPieceRows * 9);
+    C.h_coeffs = (long long*)(rows + kPieceRows * 10);
+    if (!ok(launch_verify(A, s), "piece verify") || !ok(launch_collect(C, s), "piece collect"))
       return false;
   }
   if ((*rc = rfr_check_cuda(cudaStreamSynchronize(s), "piece sync"))) return false;
@@ -830,7 +870,9 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     return RFR_OK;
   }
   if (!keys || !keys2) return rfr_fail(RFR_E_ARG, "null keys");
+  g_tr.mark("enter search_verify");
   cudaSetDevice(g.device);
+  g_tr.mark("cudaSetDevice");
   cudaStream_t s = g.stream;
   // ---- inputs: [keys | keys2 | profile doubles | perm | p_mod], one H2D
   const int r = prof->r, c = prof->c;
@@ -854,12 +896,15 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
   stage_profile((double*)(hs + o_prof), prof);
   memcpy(hs + o_perm, prof->perm, (size_t)n * sizeof(int32_t));
   memcpy(hs + o_pmod, p_mod, (size_t)3 * (d + 1) * sizeof(uint64_t));
+  g_tr.mark("inputs staged");
   RFR_CUDA_OK(g.vprof.ensure(in_bytes));
   char* base = (char*)g.vprof.p;
   // never overlap an early-exit poller of an earlier call (one that ended in
   // an error after its launch): it still reads the counters (no-op otherwise)
   RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_join, 0));
+  g_tr.mark("wait event");
   RFR_CUDA_OK(cudaMemcpyAsync(base, hs, in_bytes, cudaMemcpyHostToDevice, s));
+  g_tr.mark("inputs staged, H2D enqueued");
   const uint64_t* d_keys = (const uint64_t*)base;
   const uint64_t* d_keys2 = (const uint64_t*)(base + o_keys2);
   // ---- search, secondary window and verification back to back with no host
@@ -940,6 +985,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     rc = search_core(d_keys, n, lo, width, shard, nshards, (uint64_t*)g.raw.p, raw_cap, s, &r_bits,
                      &nwin, true, early_exit ? &ee : nullptr);
     if (rc) return rc;
+    g_tr.mark("search enqueued");
     const bool early = early_exit && nwin == 1;
     // the rest of the hits (all of them without early exit)
     if ((rc = filter_verify(early ? &d_ctr->raw_done : nullptr, early ? &d_ctr->post_done : nullptr,
@@ -958,9 +1004,25 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       g.h_stage_bytes = out_bytes;
     }
     hs = (char*)g.h_stage;
-    RFR_CUDA_OK(cudaMemcpyAsync(g.h_ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
-    RFR_CUDA_OK(copy_rows(0, spec));
+    {  // counters and the first rows in one launch, straight into pinned memory
+      CollectArgs C;
+      C.ctr = d_ctr;
+      C.pats = (const uint64_t*)g.post.p;
+      C.verdict = (const uint8_t*)obase;
+      C.side = (const uint8_t*)(obase + q_side);
+      C.coeffs = (const long long*)(obase + q_coef);
+      C.stride = stride;
+      C.rows = (unsigned)spec;
+      C.h_ctr = g.h_ctr;
+      C.h_pats = (uint64_t*)hs;
+      C.h_verdict = (uint8_t*)(hs + h_verd);
+      C.h_side = (uint8_t*)(hs + h_side);
+      C.h_coeffs = (long long*)(hs + h_coef);
+      RFR_CUDA_OK(launch_collect(C, s));
+    }
+    g_tr.mark("post enqueued, sync");
     RFR_CUDA_OK(cudaStreamSynchronize(s));
+    g_tr.mark("synced");
     if (g.h_ctr->out_count <= raw_cap) break;
     if (attempt == 2) return rfr_fail(RFR_E_CAP, "raw hit buffer regrow failed");
     const unsigned long long want = g.h_ctr->out_count + (g.h_ctr->out_count >> 3) + 1024;
@@ -1005,6 +1067,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       break;
     }
   }
+  g_tr.mark("pieces done");
   const unsigned long long total = cc.post_count + (unsigned long long)xp.size();
   if (m) {
     memcpy(pats, hs, m * 8);
@@ -1034,6 +1097,8 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     if (complete) st->buckets_planned = st->buckets;
     st->early_stop = stopped ? 1 : 0;
   }
+  g_tr.mark("return");
+  g_tr.dump();
   return RFR_OK;
 }
 

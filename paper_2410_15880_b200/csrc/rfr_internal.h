@@ -28,6 +28,22 @@ constexpr int kExhaustiveForceMaxN = 44;  // RFR_FORCE_EXHAUSTIVE (tests): up to
 cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
                               uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
                               cudaStream_t s);
+// Results of a fused call into pinned host memory (launch_collect).
+struct CollectArgs {
+  const DevCounters* ctr;
+  const uint64_t* pats;
+  const uint8_t* verdict;
+  const uint8_t* side;
+  const long long* coeffs;
+  int stride;
+  unsigned rows;  // at most this many rows
+  DevCounters* h_ctr;
+  uint64_t* h_pats;
+  uint8_t* h_verdict;
+  uint8_t* h_side;
+  long long* h_coeffs;
+};
+cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s);
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,

@@ -179,6 +179,34 @@ __device__ __forceinline__ uint32_t rot_of(const uint32_t* rc, int k, uint32_t n
 // all lists are searched concurrently so the merge CTAs start at their loads.
 // H.sp[li][hist_sp_off(k) + t] = # A elements before output tile t (kept:
 // it is also the rank directory of the level's provenance bits).
+// Merge-path split at output diagonal d of merge(A, B'), B'[j] = A[(r0 + j)
+// & mask] + v: the number of A elements among the first d outputs (A first on
+// ties), found by the calling warp with a 32-ary search.
+__device__ __forceinline__ uint32_t merge_split(const uint64_t* __restrict__ A, uint32_t r0,
+                                                uint32_t mask, uint64_t v, uint32_t n, uint32_t d,
+                                                int lane) {
+  auto Bk = [&](uint32_t j) { return __ldg(A + ((r0 + j) & mask)) + v; };
+  // smallest i with A[i] > B'[d - 1 - i] (A first on ties)
+  uint32_t lo = d > n ? d - n : 0, hi = d < n ? d : n;
+  while (hi > lo) {
+    const uint32_t span = hi - lo;
+    if (span <= 32) {
+      const uint32_t q = lo + lane;
+      const bool pr = (uint32_t)lane < span && __ldg(A + q) <= Bk(d - 1 - q);
+      lo += __popc(__ballot_sync(0xffffffffu, pr));
+      break;
+    }
+    const uint32_t q = lo + (uint32_t)(((uint64_t)span * lane) >> 5);
+    const bool pr = __ldg(A + q) <= Bk(d - 1 - q);
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, pr));
+    const uint32_t qc1 = __shfl_sync(0xffffffffu, q, (c > 0 ? c : 1) - 1);
+    const uint32_t qc = __shfl_sync(0xffffffffu, q, c < 32 ? c : 31);
+    if (c > 0) lo = qc1 + 1;
+    if (c < 32) hi = qc;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __restrict__ keys,
                                                           JoinPlan P, int k, ListBufs in,
                                                           const uint32_t* __restrict__ rot,
@@ -218,12 +246,14 @@ __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __rest
   if (lane == 0) pick4(H.sp, li)[hist_sp_off(k) + w] = lo;
 }
 
+template <bool kOwnSplit>
 __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64_t* __restrict__ keys,
                                                                     JoinPlan P, int k,
                                                                     ListBufs in, ListBufs out,
                                                                     uint32_t* rot, ListHist H) {
   __shared__ uint64_t sK[kMergeTile];
   __shared__ uint32_t wsum[kMergeThreads / 32];
+  __shared__ uint32_t ssplit[2];
   const int li = blockIdx.y;
   const ListSpec L = pick_list(P, li);
   if (L.bits <= k) return;
@@ -237,9 +267,28 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t r0 = rot_of(rc, k, n);
   const uint32_t mask = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t* sp = pick4(H.sp, li) + hist_sp_off(k);
-  const uint32_t a0 = __ldg(sp + blockIdx.x);
-  const uint32_t a1 = __ldg(sp + blockIdx.x + 1);
+  uint32_t* sp = pick4(H.sp, li) + hist_sp_off(k);
+  uint32_t a0, a1;
+  if (kOwnSplit) {
+    // the tile's two merge-path splits, by warps 0 and 1 (one launch per level
+    // instead of a split kernel + the merge: the search latency hides behind
+    // the other resident CTAs' merges); a0 is also kept as the rank
+    // directory of the level's provenance bits
+    if (wid < 2) {
+      const uint32_t d = min((blockIdx.x + wid) * (uint32_t)kMergeTile, 2u * n);
+      const uint32_t a = merge_split(A, r0, mask, v, n, d, lane);
+      if (lane == 0) {
+        ssplit[wid] = a;
+        if (wid == 0 || d == 2u * n) sp[blockIdx.x + wid] = a;
+      }
+    }
+    __syncthreads();
+    a0 = ssplit[0];
+    a1 = ssplit[1];
+  } else {
+    a0 = __ldg(sp + blockIdx.x);
+    a1 = __ldg(sp + blockIdx.x + 1);
+  }
   const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
   const uint32_t na = a1 - a0, nb = tile - na;
   const uint32_t b0 = d0 - a0;
@@ -620,14 +669,22 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
   lists_base_kernel<<<4, 1024, sizeof(BaseSmem), s>>>(d_keys, P, buf0, d_rot);
   int maxbits = 0;
   for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
+  // RFR_SPLIT_KERNEL=1 (A/B): the separate split kernel before every merge
+  static int split_kernel = -1;
+  if (split_kernel < 0) split_kernel = getenv("RFR_SPLIT_KERNEL") ? 1 : 0;
   for (int k = kBaseBits; k < maxbits; k++) {
     const int parity = (k - kBaseBits) & 1;
     const uint64_t outputs = 2ull << k;
     const unsigned int blocks = (unsigned int)((outputs + kMergeTile - 1) / kMergeTile);
-    lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
-                                                                 d_rot, H);
-    lists_merge_kernel<<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
-        d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+    if (split_kernel) {
+      lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
+                                                                   d_rot, H);
+      lists_merge_kernel<false><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+          d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+    } else {
+      lists_merge_kernel<true><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+          d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+    }
   }
   return cudaGetLastError();
 }
@@ -843,6 +900,29 @@ __global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long 
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s) {
   deposit_kernel<<<nsm, 256, 0, s>>>(d_pats, d_count, cap, mask);
+  return cudaGetLastError();
+}
+
+// The results of a search + verification straight into pinned host memory
+// (mapped: the host pointers are device pointers under UVA): the counters
+// and the first min(post_count, rows) rows -- one launch instead of five
+// small device-to-host copies, each with its own ~3 us of setup and gap.
+__global__ void collect_kernel(CollectArgs C) {
+  const unsigned long long cnt = C.ctr->post_count;
+  const unsigned rows = (unsigned)(cnt < C.rows ? cnt : C.rows);
+  const int t = threadIdx.x;
+  if (t < (int)(sizeof(DevCounters) / 8))
+    ((unsigned long long*)C.h_ctr)[t] = ((const unsigned long long*)C.ctr)[t];
+  for (unsigned k = t; k < rows; k += blockDim.x) {
+    C.h_pats[k] = C.pats[k];
+    C.h_verdict[k] = C.verdict[k];
+    C.h_side[k] = C.side[k];
+  }
+  const unsigned nco = rows * (unsigned)C.stride;
+  for (unsigned k = t; k < nco; k += blockDim.x) C.h_coeffs[k] = C.coeffs[k];
+}
+cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
+  collect_kernel<<<1, 256, 0, s>>>(C);
   return cudaGetLastError();
 }
 

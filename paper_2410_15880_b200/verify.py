@@ -90,14 +90,16 @@ class FactorizationResult:
 def selected_degree(s: int, profile: RootProfile) -> int:
     """Degree of the factor a pattern selects: 1 per real root, 2 per pair
     (R/verify.py:48-57)."""
-    e = 0
-    i = 0
-    while s:
-        if s & 1:
-            e += 1 if profile.perm[i] < profile.r else 2
-        s >>= 1
-        i += 1
-    return e
+    real, pair = _degree_masks(profile.perm, profile.r)
+    s = int(s)
+    return (s & real).bit_count() + 2 * (s & pair).bit_count()
+
+
+@lru_cache(maxsize=1024)
+def _degree_masks(perm: tuple, r: int) -> tuple[int, int]:
+    """Bit masks of the rho indices holding real roots and pairs."""
+    real = sum(1 << i for i, e in enumerate(perm) if e < r)
+    return real, sum(1 << i for i in range(len(perm))) & ~real
 
 
 @lru_cache(maxsize=256)
@@ -481,7 +483,8 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
 
 
 def _coeff_bits(p: IntPolynomial) -> int:
-    return max(abs(c) for c in p.coeffs).bit_length()
+    co = p.coeffs
+    return max(max(co), -min(co)).bit_length()
 
 
 def _integer_roots(p: IntPolynomial, scan: bool) -> list:
