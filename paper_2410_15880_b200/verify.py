@@ -107,8 +107,35 @@ def _profile_cached(coeffs: tuple) -> RootProfile:
     return hp_profile(IntPolynomial(coeffs))
 
 
+# Data derived from a root profile alone (packing and key sums: part of the
+# untimed preprocessing, like the roots), kept beside the cached profile.
+_DERIVED: "OrderedDict[int, tuple]" = None  # id(prof) -> (prof, {name: value})
+
+
+def _derived(prof: RootProfile, name: str, make):
+    global _DERIVED
+    if _DERIVED is None:
+        from collections import OrderedDict
+
+        _DERIVED = OrderedDict()
+    ent = _DERIVED.get(id(prof))
+    if ent is None or ent[0] is not prof:
+        ent = (prof, {})
+        _DERIVED[id(prof)] = ent
+        if len(_DERIVED) > 512:
+            _DERIVED.popitem(last=False)
+    d = ent[1]
+    if name not in d:
+        d[name] = make(prof)
+    return d[name]
+
+
 def _search_window(prof: RootProfile) -> tuple[np.ndarray, int]:
     """Combined keys (first + second power sum) and the window half-width."""
+    return _derived(prof, "window", _search_window_of)
+
+
+def _search_window_of(prof: RootProfile) -> tuple[np.ndarray, int]:
     k1 = np.asarray(prof.keys1, dtype=np.uint64)
     k2 = np.asarray(prof.keys2, dtype=np.uint64)
     keys = k1 + k2  # uint64 addition wraps: the sum mod 2^64
@@ -122,7 +149,8 @@ def _secondary_window(prof: RootProfile) -> tuple[np.ndarray | None, int]:
     or (None, 0) for a profile without them."""
     if prof.keys3 is None:
         return None, 0
-    return prof.keys3, prof.key_err3
+    return _derived(prof, "window3", lambda pr: (np.ascontiguousarray(pr.keys3, dtype=np.uint64),
+                                                 pr.key_err3))
 
 
 _PRIMES: tuple[int, ...] | None = None
@@ -148,6 +176,10 @@ def _rfr_profile(prof: RootProfile):
     """The profile as an rfr_profile struct (plus the buffer it points into,
     which the caller keeps alive for the duration of the call): the six
     double arrays packed into one buffer, perm as int32."""
+    return _derived(prof, "rfr_profile", _rfr_profile_of)
+
+
+def _rfr_profile_of(prof: RootProfile):
     r, c = prof.r, prof.c
 
     def lo(a, k):
@@ -444,14 +476,12 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
     uses the exact double-double value (hi + lo, or the multiprecision one):
     a value at or above 2^53 is not an integer in its high word alone."""
     # vectorised screen: only entities within 1e-6 of integral values are tested
+    near_r, near_p = _derived(prof, "near_integral", _near_integral)
+    if not len(near_r) and not len(near_p):
+        return []
     ru = np.asarray(prof.real_roots, dtype=np.float64)
-    near_r = np.abs(ru - np.round(ru)) <= 1e-6 * np.maximum(1.0, np.abs(ru))
     pt = np.asarray(prof.pair_sums, dtype=np.float64)
     pm = np.asarray(prof.pair_products, dtype=np.float64)
-    near_p = ((np.abs(pt - np.round(pt)) <= 1e-6 * np.maximum(1.0, np.abs(pt)))
-              & (np.abs(pm - np.round(pm)) <= 1e-6 * np.maximum(1.0, np.abs(pm))))
-    if not near_r.any() and not near_p.any():
-        return []
 
     def exact(hi, lo, j):
         v = Fraction(float(hi[j]))
@@ -461,7 +491,7 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
 
     bit_of = {ent: i for i, ent in enumerate(prof.perm)}
     out = []
-    for ent in np.flatnonzero(near_r):
+    for ent in near_r:
         e = int(ent)
         u = prof.hp_real[e] if prof.hp_real is not None else exact(ru, prof.real_lo, e)
         r = round(u)
@@ -470,7 +500,7 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
             acc = acc * r + c
         if acc == 0:
             out.append((bit_of[e], IntPolynomial([-r, 1])))
-    for j in np.flatnonzero(near_p):
+    for j in near_p:
         j = int(j)
         if prof.hp_pair is not None:
             tt, mm = prof.hp_pair[j]
@@ -480,6 +510,18 @@ def _single_entity_factors(prof: RootProfile, p: IntPolynomial) -> list:
         if divide_exact(p, q) is not None:
             out.append((bit_of[prof.r + j], q))
     return out
+
+
+def _near_integral(prof: RootProfile):
+    """Indices of the real roots, and of the pairs (sum and product), within
+    1e-6 (relative) of integers: the only one-entity factor candidates."""
+    ru = np.asarray(prof.real_roots, dtype=np.float64)
+    near_r = np.abs(ru - np.round(ru)) <= 1e-6 * np.maximum(1.0, np.abs(ru))
+    pt = np.asarray(prof.pair_sums, dtype=np.float64)
+    pm = np.asarray(prof.pair_products, dtype=np.float64)
+    near_p = ((np.abs(pt - np.round(pt)) <= 1e-6 * np.maximum(1.0, np.abs(pt)))
+              & (np.abs(pm - np.round(pm)) <= 1e-6 * np.maximum(1.0, np.abs(pm))))
+    return np.flatnonzero(near_r), np.flatnonzero(near_p)
 
 
 def _coeff_bits(p: IntPolynomial) -> int:
