@@ -277,6 +277,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_times = []
     early_exits = 0
+    hit_stop = []
     h2d = d2h = 0
     for s in range(0 if args.no_e2e else args.steps):
         seed, p, want, prof, keys, T, _ = prep[s % len(prep)]
@@ -291,6 +292,8 @@ def run_ours(args):
         e2e_times.append((time.perf_counter() - t0 - res.stats.root_seconds) * 1e3)
         assert sorted(list(g.coeffs) for g, _ in res.factors) == sorted(want) and res.certificate
         early_exits += res.stats.early_exits
+        if res.stats.recombine.hit_to_stop_us >= 0:
+            hit_stop.append(res.stats.recombine.hit_to_stop_us)
         m = res.stats.candidates
         h2d += 8 * prof.n + 8 * (2 * prof.r + 4 * prof.c) + 4 * prof.n + 8 * m + 24 * (p.degree + 1)
         d2h += 8 + 8 * m + 2 * m + 8 * 65 * m
@@ -449,7 +452,9 @@ def run_ours(args):
                 "path": "factor(): fused search + verification with early termination (the join "
                         "stops once a hit verifies; each piece is then factored over its own "
                         "roots), warm-up calls untimed",
-                "early_exits": early_exits},
+                "early_exits": early_exits,
+                "hit_to_stop_us": ({"mean": round(float(np.mean(hit_stop)), 1),
+                                    "max": round(float(np.max(hit_stop)), 1)} if hit_stop else None)},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "c4": {"workload": "C4 d=120 irreducible seed 0 (n=63), search only",

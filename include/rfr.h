@@ -72,6 +72,9 @@ typedef struct rfr_stats {
                            /* every doubling level (each level reads its input twice)  */
   int64_t bytes_join;      /* HBM bytes the join streams by design: one 8-byte inner   */
                            /* key per record of this shard's buckets                   */
+  double us_hit_to_stop;   /* rfr_search_verify with early exit: microseconds from the */
+                           /* poller's verified hit to the last join CTA leaving its   */
+                           /* bucket loop (device clock); -1 when it did not stop      */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */

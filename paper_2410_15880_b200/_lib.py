@@ -68,6 +68,7 @@ class RfrStats(ctypes.Structure):
         ("list_bits", ctypes.c_int32 * 4),
         ("bytes_lists", ctypes.c_int64),
         ("bytes_join", ctypes.c_int64),
+        ("us_hit_to_stop", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

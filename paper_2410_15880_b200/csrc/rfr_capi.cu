@@ -360,6 +360,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
 void fill_stats(rfr_stats* st, const DevCounters& c, int n, int r_bits, int nwin) {
   if (!st) return;
   memset(st, 0, sizeof *st);
+  st->us_hit_to_stop = -1.0;
   const int m = n - 1;
   const int alpha = (m + 1) / 2, beta = m - alpha;
   st->visited = n > 0 ? (int64_t)((1ull << alpha) + (1ull << beta)) : 0;
@@ -974,6 +975,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     ee.V.m = (long long)vrows;
     ee.V.m_dev = nullptr;
     ee.V.found = &d_ctr->found;
+    ee.V.t_found = &d_ctr->t_found;
     ee.V.verdict = (uint8_t*)obase;
     ee.V.side = (uint8_t*)(obase + q_side);
     ee.V.coeffs = (long long*)(obase + q_coef);
@@ -1032,6 +1034,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     RFR_CUDA_OK(g.raw.ensure(want * sizeof(uint64_t)));
   }
   const DevCounters cc = *g.h_ctr;
+  if (cc.t_found && getenv("RFR_STOP_TRACE")) dump_stop_trace(cc.t_found, g.nsm * kJoinCtasPerSm - 1);
   const int main_launches = g_launches;
   const int64_t main_planned = g_buckets_planned;
   const size_t m = cc.post_count < (unsigned long long)cap ? (size_t)cc.post_count : (size_t)cap;
@@ -1096,7 +1099,19 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     st->buckets += xbuckets;
     if (complete) st->buckets_planned = st->buckets;
     st->early_stop = stopped ? 1 : 0;
+    st->us_hit_to_stop = (stopped && cc.t_found && cc.t_stop >= cc.t_found)
+                             ? (double)(cc.t_stop - cc.t_found) * 1e-3
+                             : -1.0;
   }
+  if (g_tr.on == 1)
+    fprintf(stderr, "[rfr host] counters: out %llu post %llu raw_done %llu post_done %llu found %llu buckets %llu/%lld m %zu verdict0 %d complete %d\n",
+            cc.out_count, cc.post_count, cc.raw_done, cc.post_done, cc.found, cc.buckets,
+            (long long)main_planned, m, m ? (int)((const uint8_t*)(hs + h_verd))[0] : -1, (int)complete);
+  if (g_tr.on == 1 && cc.t_found)
+    fprintf(stderr, "[rfr host] device: hit seen->found %.1f us, found->first stop %.1f us, found->last stop %.1f us\n",
+            cc.t_hit ? (double)((long long)cc.t_found - (long long)cc.t_hit) * 1e-3 : -1.0,
+            cc.t_stop_first ? (double)((long long)cc.t_stop_first - (long long)cc.t_found) * 1e-3 : -1.0,
+            cc.t_stop ? (double)((long long)cc.t_stop - (long long)cc.t_found) * 1e-3 : -1.0);
   g_tr.mark("return");
   g_tr.dump();
   return RFR_OK;

@@ -98,13 +98,27 @@ struct DevCounters {
   unsigned long long post_count;     // survivors of the post-filter
   // early exit (rfr_search_verify with early_exit): the poller verifies hits
   // while the join runs and raises found; the join's CTAs stop at their next
-  // bucket boundary.  found is 16-byte aligned (the join copies it with one
-  // 16-byte cp.async).
+  // bucket boundary.
   unsigned long long raw_done;       // raw hits the poller turned into patterns and filtered
   unsigned long long post_done;      // survivors the poller verified
-  unsigned long long found;          // a candidate passed verification
   unsigned long long ctas_done;      // join CTAs finished (the poller's stop condition)
+  // hit-to-stop latency (globaltimer, ns): the poller's speculative stop, the
+  // moment it saw that hit, and the first / last join CTA that stopped
+  unsigned long long t_found;
+  unsigned long long t_stop;
+  unsigned long long t_hit;
+  unsigned long long t_stop_first;
+  // the stop flag on a cache line of its own: every join CTA reads it once per
+  // bucket, and the counters above take the CTAs' end-of-join atomics (on a
+  // shared line those queued the flag reads for up to ~100 us)
+  alignas(128) unsigned long long found;  // a candidate passed (or speculatively: hit) verification
+  unsigned long long found_pad[15];
 };
+__device__ __forceinline__ unsigned long long rfr_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 static_assert(offsetof(DevCounters, found) % 16 == 0, "found must be 16-byte aligned");
 
 }  // namespace rfr

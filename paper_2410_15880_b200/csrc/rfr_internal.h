@@ -12,6 +12,7 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s,
                         const uint32_t* d_rots, const uint32_t* d_starts, bool early = false);
+void dump_stop_trace(unsigned long long t_found, int grid);  // RFR_STOP_TRACE diagnostics
 cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t b0, uint64_t b1,
                                int nck, int ctas, uint32_t* d_rots, uint32_t* d_starts, cudaStream_t s);
 cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, const ListHist& hist,
@@ -75,6 +76,7 @@ struct VerifyArgs {
   // factor stops every rank's join at its next bucket boundary
   unsigned long long* peer_found[kMaxPeers] = {};
   int npeers = 0;
+  unsigned long long* t_found = nullptr;  // with found: globaltimer of the first PASS
   const uint64_t* p_mod;  // 3 x (d+1)
   uint64_t primes[3];
   uint8_t* verdict;

@@ -112,6 +112,17 @@ __device__ __forceinline__ JoinSmem& join_smem() {
   return *reinterpret_cast<JoinSmem*>(__cvta_shared_to_generic(sa));
 }
 
+// The stop flag read with gpu-scope coherence (a weak read -- the cp.async
+// copy -- may be served from a stale far-die L2 copy for tens of us).
+#ifndef RFR_STOP_COHERENT
+#define RFR_STOP_COHERENT 1
+#endif
+__device__ __forceinline__ unsigned long long ld_found_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Streaming read of a list key: read-only path without L1 allocation, so the
 // window loads do not evict the kernel's stack and small working set.
 __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
@@ -911,6 +922,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
 
   // outer keys, rotation starts and first-bucket positions: precomputed for
   // every CTA of this launch by join_starts_kernel
+  const unsigned long long t_start = a.trace_stop ? rfr_globaltimer() : 0ull;
   const uint32_t* __restrict__ st0 = a.starts + (size_t)blockIdx.x * (MoA + MoB);
   for (uint32_t i = tid; i < MoA; i += kJoinThreads) {
     S.ax[i] = __ldg(a.key[0] + i);
@@ -1005,10 +1017,18 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
         for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
       }
       RFR_MARK();
-      if (a.early && tid_now() == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
+      if (a.early && tid_now() == 0) {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        if (RFR_STOP_COHERENT) join_smem().stop_buf[0] |= ld_found_gpu(&a.ctr->found);
+      }
       __syncthreads();
       RFR_MARK();
       if (a.early && join_smem().stop_buf[0]) {
+        if (tid_now() == 0) {
+          const unsigned long long t = rfr_globaltimer();
+          atomicMax(&a.ctr->t_stop, t);
+          atomicCAS(&a.ctr->t_stop_first, 0ull, t);
+        }
         c++;
         break;
       }
@@ -1027,18 +1047,37 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       for (uint32_t i = join_smem().wlo[1][w] + l; i < join_smem().whi[1][w]; i += 32) join_smem().bpos[i] += join_smem().bmain[i];
       for (uint32_t i = join_smem().wlo[0][w] + l; i < join_smem().whi[0][w]; i += 32) join_smem().apos[i] += join_smem().amain[i];
     }
-    if (a.early && tid_now() == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (a.early && tid_now() == 0) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      if (RFR_STOP_COHERENT) join_smem().stop_buf[0] |= ld_found_gpu(&a.ctr->found);
+    }
     __syncthreads();
     if (a.early && join_smem().stop_buf[0]) {
+      if (tid_now() == 0) {
+        const unsigned long long t = rfr_globaltimer();
+        atomicMax(&a.ctr->t_stop, t);
+        atomicCAS(&a.ctr->t_stop_first, 0ull, t);
+      }
       c++;
       break;
     }
   }
-  const uint32_t n_ins = S.cnt[0][tid], n_q = S.cnt[1][tid], n_qprobe = S.cnt[2][tid];
-  atomicAdd(&a.ctr->inserts, (unsigned long long)n_ins);
-  atomicAdd(&a.ctr->queries, (unsigned long long)n_q);
-  atomicAdd(&a.ctr->query_probes, (unsigned long long)n_qprobe);
+  // the CTA's counters as one atomic each (one per thread from every CTA at
+  // once queued ~2*10^5 atomics on one line at the end of the join)
+  __syncthreads();
+  if (tid < 3) {
+    unsigned long long sum = 0;
+    for (int t = 0; t < kJoinThreads; t++) sum += S.cnt[tid][t];
+    atomicAdd(tid == 0 ? &a.ctr->inserts : tid == 1 ? &a.ctr->queries : &a.ctr->query_probes, sum);
+  }
   if (tid == 0) {
+    if (a.trace_stop) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_cta_stop[3 * blockIdx.x] = rfr_globaltimer();
+      g_cta_stop[3 * blockIdx.x + 1] = ((unsigned long long)smid << 32) | (unsigned long long)(c - c_begin);
+      g_cta_stop[3 * blockIdx.x + 2] = t_start;
+    }
     atomicAdd(&a.ctr->chunks, (unsigned long long)n_chunks);
     atomicAdd(&a.ctr->buckets, (unsigned long long)(c - c_begin));  // fewer on an early exit
     __threadfence();  // every hit of this CTA is visible before it counts as done

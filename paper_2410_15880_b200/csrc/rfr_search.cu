@@ -1,3 +1,6 @@
+#include <algorithm>
+#include <vector>
+#include <cstdio>
 #include <cmath>
 // rfr_search.cu -- the recombination search (meet in the middle) on sm_100a.
 //
@@ -246,12 +249,29 @@ __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __rest
   if (lane == 0) pick4(H.sp, li)[hist_sp_off(k) + w] = lo;
 }
 
-template <bool kOwnSplit>
+// Tile staging by the Tensor Memory Accelerator (kMode 2): the tile's A run
+// and its rotated B' run are copied as 128-byte rows (16 keys) by
+// cp.async.bulk into padded shared rows (144-byte stride: consecutive rows
+// start 4 banks apart, so the per-thread runs the merge reads do not pile
+// onto one bank pair), completing on one mbarrier; the B' rows are copied
+// without "+ v" (added on read) and wrap around the list end row by row.
+constexpr int kTmaRowKeys = 16, kTmaRowStride = 18;  // keys per row, padded stride (keys)
+constexpr int kTmaRowsSide = kMergeTile / kTmaRowKeys + 2;  // rows per side (offset + partial row)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// kMode 0: splits from lists_split_kernel, staging by loads + shared stores;
+// 1: own splits, same staging; 2: own splits, TMA bulk-copy staging.
+template <int kMode>
 __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64_t* __restrict__ keys,
                                                                     JoinPlan P, int k,
                                                                     ListBufs in, ListBufs out,
                                                                     uint32_t* rot, ListHist H) {
-  __shared__ uint64_t sK[kMergeTile];
+  constexpr bool kOwnSplit = kMode >= 1;
+  constexpr bool kTma = kMode == 2;
+  __shared__ __align__(128) uint64_t sK[kTma ? 2 * kTmaRowsSide * kTmaRowStride : kMergeTile];
+  __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t wsum[kMergeThreads / 32];
   __shared__ uint32_t ssplit[2];
   const int li = blockIdx.y;
@@ -268,6 +288,10 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t mask = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t* sp = pick4(H.sp, li) + hist_sp_off(k);
+  if (kTma && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   uint32_t a0, a1;
   if (kOwnSplit) {
     // the tile's two merge-path splits, by warps 0 and 1 (one launch per level
@@ -292,31 +316,80 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   const uint32_t tile = min((uint32_t)kMergeTile, 2u * n - d0);
   const uint32_t na = a1 - a0, nb = tile - na;
   const uint32_t b0 = d0 - a0;
-  // one pass over the tile: output slot t < na stages A[a0 + t], the rest
-  // stage B'; every thread's kMergeItems loads are independent and issued
-  // before the first shared store (the A and B halves as two loops waited
-  // on HBM twice per tile)
-  auto stage = [&](uint32_t t) {
-    const bool isA = t < na;
-    const uint64_t* src = isA ? A + a0 + t : A + ((r0 + b0 + (t - na)) & mask);
-    return __ldg(src) + (isA ? 0ull : v);
-  };
-  if (tile == (uint32_t)kMergeTile) {
-    uint64_t x[kMergeItems];
-#pragma unroll
-    for (int u = 0; u < kMergeItems; u++) x[u] = stage(tid + u * kMergeThreads);
-#pragma unroll
-    for (int u = 0; u < kMergeItems; u++) sK[kswz(tid + u * kMergeThreads)] = x[u];
+  const uint32_t sB = (r0 + b0) & mask;  // B' run = A[sB ...] + v, wrapping at n
+  const uint32_t offA = a0 & (kTmaRowKeys - 1), offB = sB & (kTmaRowKeys - 1);
+  if (kTma) {
+    const uint32_t rowsA = na ? (offA + na + kTmaRowKeys - 1) / kTmaRowKeys : 0u;
+    const uint32_t rowsB = nb ? (offB + nb + kTmaRowKeys - 1) / kTmaRowKeys : 0u;
+    if (wid == 0) {
+      const uint32_t mb = smem_u32(&mbar);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                     "r"((rowsA + rowsB) * (uint32_t)(kTmaRowKeys * 8))
+                     : "memory");
+      __syncwarp();
+      const uint32_t nrow = n / kTmaRowKeys;
+      for (uint32_t r = lane; r < rowsA + rowsB; r += 32) {
+        const bool isA = r < rowsA;
+        const uint32_t grow = isA ? (a0 >> 4) + r : ((sB >> 4) + (r - rowsA)) & (nrow - 1);
+        const uint32_t srow = isA ? r : kTmaRowsSide + (r - rowsA);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sK + srow * kTmaRowStride)),
+            "l"(A + (size_t)grow * kTmaRowKeys), "r"(kTmaRowKeys * 8), "r"(mb)
+            : "memory");
+      }
+    }
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.b32 %0, 1, 0, "
+          "p;\n\t}"
+          : "=r"(done)
+          : "r"(smem_u32(&mbar))
+          : "memory");
   } else {
-    for (uint32_t t = tid; t < tile; t += kMergeThreads) sK[kswz(t)] = stage(t);
+    // one pass over the tile: output slot t < na stages A[a0 + t], the rest
+    // stage B'; every thread's kMergeItems loads are independent and issued
+    // before the first shared store (the A and B halves as two loops waited
+    // on HBM twice per tile)
+    auto stage = [&](uint32_t t) {
+      const bool isA = t < na;
+      const uint64_t* src = isA ? A + a0 + t : A + ((r0 + b0 + (t - na)) & mask);
+      return __ldg(src) + (isA ? 0ull : v);
+    };
+    if (tile == (uint32_t)kMergeTile) {
+      uint64_t x[kMergeItems];
+#pragma unroll
+      for (int u = 0; u < kMergeItems; u++) x[u] = stage(tid + u * kMergeThreads);
+#pragma unroll
+      for (int u = 0; u < kMergeItems; u++) sK[kswz(tid + u * kMergeThreads)] = x[u];
+    } else {
+      for (uint32_t t = tid; t < tile; t += kMergeThreads) sK[kswz(t)] = stage(t);
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  // staged tile accessors: A run element i, B' run element j
+  auto LA = [&](uint32_t i) -> uint64_t {
+    if (kTma) {
+      const uint32_t x = offA + i;
+      return sK[(x >> 4) * kTmaRowStride + (x & 15u)];
+    }
+    return sK[kswz(i)];
+  };
+  auto LB = [&](uint32_t j) -> uint64_t {
+    if (kTma) {
+      const uint32_t x = offB + j;
+      return sK[(kTmaRowsSide + (x >> 4)) * kTmaRowStride + (x & 15u)] + v;
+    }
+    return sK[kswz(na + j)];
+  };
   // per-thread merge of kMergeItems outputs from the staged tile
   const uint32_t dt = min((uint32_t)(tid * kMergeItems), tile);
   uint32_t lo = dt > nb ? dt - nb : 0, hi = dt < na ? dt : na;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (sK[kswz(mid)] <= sK[kswz(na + dt - 1 - mid)]) lo = mid + 1;
+    if (LA(mid) <= LB(dt - 1 - mid)) lo = mid + 1;
     else hi = mid;
   }
   uint32_t i = lo, j = dt - lo;
@@ -324,19 +397,19 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   uint32_t from_b = 0;  // provenance bits of this thread's outputs
   // both run heads held in registers: one shared key load per output
   const uint64_t kInf = ~0ull;
-  uint64_t ka = i < na ? sK[kswz(i)] : kInf, kb = j < nb ? sK[kswz(na + j)] : kInf;
+  uint64_t ka = i < na ? LA(i) : kInf, kb = j < nb ? LB(j) : kInf;
 #pragma unroll
   for (int t = 0; t < kMergeItems; t++) {
     const bool takeA = j >= nb || (i < na && ka <= kb);
     if (takeA) {
       ok[t] = ka;
       i++;
-      ka = i < na ? sK[kswz(i)] : kInf;
+      ka = i < na ? LA(i) : kInf;
     } else {
       ok[t] = kb;
       from_b |= 1u << t;
       j++;
-      kb = j < nb ? sK[kswz(na + j)] : kInf;
+      kb = j < nb ? LB(j) : kInf;
     }
   }
   // each thread's run of outputs is contiguous and 64-byte aligned: store it
@@ -390,12 +463,16 @@ struct JoinArgs {
   const uint32_t* rots;
   const uint32_t* starts;  // [cta][MoA + MoB]
   int early;               // stop at a bucket boundary once DevCounters.found is set
+  int trace_stop;          // RFR_STOP_TRACE: each CTA records when and where it stopped
   uint64_t* out;
   unsigned long long cap;
   DevCounters* ctr;
   unsigned long long* dbg;  // optional clock64 trace of CTA 0 (RFR_TRACE)
 };
 
+// RFR_STOP_TRACE (diagnostics): per join CTA, the globaltimer when it left
+// its bucket loop and (SM id << 32 | buckets searched)
+__device__ unsigned long long g_cta_stop[3 * 1024];
 #include "rfr_join.cuh"
 
 // lower_bound of v in a sorted array by one warp: 32 probes per round narrow
@@ -669,9 +746,14 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
   lists_base_kernel<<<4, 1024, sizeof(BaseSmem), s>>>(d_keys, P, buf0, d_rot);
   int maxbits = 0;
   for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
-  // RFR_SPLIT_KERNEL=1 (A/B): the separate split kernel before every merge
-  static int split_kernel = -1;
+  // RFR_SPLIT_KERNEL=1 (A/B): the separate split kernel before every merge;
+  // RFR_MERGE_TMA=0/1: staging by loads + shared stores, or by TMA bulk copies
+  static int split_kernel = -1, tma = -1;
   if (split_kernel < 0) split_kernel = getenv("RFR_SPLIT_KERNEL") ? 1 : 0;
+  if (tma < 0) {
+    const char* e = getenv("RFR_MERGE_TMA");
+    tma = e ? atoi(e) : 0;  // measured slower: off by default
+  }
   for (int k = kBaseBits; k < maxbits; k++) {
     const int parity = (k - kBaseBits) & 1;
     const uint64_t outputs = 2ull << k;
@@ -679,10 +761,13 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
     if (split_kernel) {
       lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
                                                                    d_rot, H);
-      lists_merge_kernel<false><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+      lists_merge_kernel<0><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+          d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+    } else if (tma) {
+      lists_merge_kernel<2><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
           d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
     } else {
-      lists_merge_kernel<true><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
+      lists_merge_kernel<1><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
           d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
     }
   }
@@ -713,6 +798,12 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
   a.rots = d_rots;
   a.starts = d_starts;
   a.early = early ? 1 : 0;
+  a.trace_stop = getenv("RFR_STOP_TRACE") != nullptr && grid <= 1024;
+  if (a.trace_stop) {
+    void* sym = nullptr;
+    cudaGetSymbolAddress(&sym, g_cta_stop);
+    cudaMemsetAsync(sym, 0, sizeof(g_cta_stop), s);
+  }
   static unsigned long long* dbg = nullptr;
   a.dbg = nullptr;
   if (getenv("RFR_TRACE")) {
@@ -969,6 +1060,7 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
   __syncwarp();
   const long long t0 = clock64();
   unsigned long long done = 0;
+  bool spec = false;  // a speculative stop was raised
   while (true) {
     // once the join is over the batch kernels take the rest (a flood of hits
     // would keep one warp busy for seconds)
@@ -982,6 +1074,7 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
              clock64() - t0 < a.max_cycles) {
       }
       if (v == kUnsetHit) break;  // time limit: the batch kernels take over
+      const unsigned long long t_seen = rfr_globaltimer();
       // pattern: lanes 0-3 walk the four quarter lists (index_to_pattern_kernel)
       uint64_t part = 0;
       if (lane < 4) {
@@ -1002,6 +1095,25 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
         unsigned long long k = 0;
         if (lane == 0) k = atomicAdd(&a.ctr->post_count, 1ull);
         k = __shfl_sync(0xffffffffu, k, 0);
+        // Speculative stop: a hit inside both key windows is a factor but for
+        // ~2^(n-1) (2T+1)(2T3+1) / 2^128 false hits of random keys (~1e-17
+        // at d = 100), so the join is stopped now and the hit verified after:
+        // verifying first left the join running ~0.6 ms past the hit (one
+        // warp verifying a degree-50 candidate beside 16 busy join warps).
+        // Only while hits are rare (the first non-empty survivor among the
+        // first 16 raw hits):
+        // structured inputs (Swinnerton-Dyer) flood the windows with
+        // non-factors and keep verify-then-stop.  A stop whose hit then
+        // fails verification leaves the search incomplete without a PASS,
+        // and the caller searches the whole space (verify.py).
+        if (!spec && t != 0 && done < 16 && lane == 0 && a.V.found) {  // t = 0: the empty pattern
+          if (a.V.t_found) atomicCAS(a.V.t_found, 0ull, rfr_globaltimer());
+          a.ctr->t_hit = t_seen;
+          atomicExch(a.V.found, 1ull);
+          for (int i = 0; i < a.V.npeers; i++) *(volatile unsigned long long*)a.V.peer_found[i] = 1ull;
+          if (a.V.npeers) __threadfence_system();
+        }
+        spec |= t != 0;
         if (k < a.post_cap && lane == 0) a.post[k] = t;
         __syncwarp();
         if (k < a.post_cap && (long long)k < a.V.m) verify_one(a.V, PS, B, (long long)k, lane);
@@ -1050,4 +1162,28 @@ cudaError_t launch_rho_keys(const double* d_rho, int n, uint64_t* d_keys, cudaSt
   return cudaGetLastError();
 }
 
+}  // namespace rfr
+
+namespace rfr {
+// RFR_STOP_TRACE: the join CTAs that left their bucket loop last after a stop
+void dump_stop_trace(unsigned long long t_found, int grid) {
+  static unsigned long long h[3 * 1024];
+  if (grid > 1024) return;
+  cudaMemcpyFromSymbol(h, g_cta_stop, sizeof(unsigned long long) * 3 * grid);
+  std::vector<std::pair<long long, int>> v;
+  unsigned long long t0 = ~0ull;
+  for (int i = 0; i < grid; i++) {
+    if (h[3 * i]) v.push_back({(long long)h[3 * i] - (long long)t_found, i});
+    if (h[3 * i + 2] && h[3 * i + 2] < t0) t0 = h[3 * i + 2];
+  }
+  std::sort(v.begin(), v.end());
+  fprintf(stderr, "[rfr stop] %zu CTAs stopped; found at +%.1f us after the first CTA start; median %.1f us after found\n",
+          v.size(), ((long long)t_found - (long long)t0) * 1e-3, v.empty() ? 0.0 : v[v.size() / 2].first * 1e-3);
+  for (size_t k = 0; k < v.size(); k += (v.size() > 8 ? v.size() / 8 : 1)) {
+    const int i = v[k].second;
+    fprintf(stderr, "[rfr stop]   cta %4d sm %3llu buckets %6llu start +%.1f us stop +%.1f us after found\n", i,
+            h[3 * i + 1] >> 32, h[3 * i + 1] & 0xffffffffull, ((long long)h[3 * i + 2] - (long long)t0) * 1e-3,
+            v[k].first * 1e-3);
+  }
+}
 }  // namespace rfr

@@ -265,6 +265,7 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
   const bool divides = !__any_sync(0xffffffffu, nz);
   if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
   if (lane == 0 && divides && A.found) {
+    if (A.t_found) atomicCAS(A.t_found, 0ull, rfr_globaltimer());
     atomicExch(A.found, 1ull);
     // cross-rank early exit: raise the peers' flags (P2P stores over NVLink)
     for (int i = 0; i < A.npeers; i++) *(volatile unsigned long long*)A.peer_found[i] = 1ull;

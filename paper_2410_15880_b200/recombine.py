@@ -93,6 +93,9 @@ class RecombineStats:
     find_steps: int = 0
     raw_hits: int = 0
     device_ms: float = 0.0
+    # early exit: microseconds from the verified hit to the join's stop (the
+    # last search that stopped; -1 when none did)
+    hit_to_stop_us: float = -1.0
 
     @property
     def probes_mean(self) -> float:
@@ -138,6 +141,8 @@ def _fill_stats(stats: RecombineStats | None, st: "_lib.RfrStats") -> None:
     stats.query_probes += int(st.query_probes)
     stats.raw_hits += int(st.raw_hits)
     stats.device_ms += float(st.ms_total)
+    if st.us_hit_to_stop >= 0:
+        stats.hit_to_stop_us = float(st.us_hit_to_stop)
 
 
 def recombine_e(rho: RhoVector, eps: float, stats: RecombineStats | None = None,
