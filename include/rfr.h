@@ -164,7 +164,7 @@ enum {
  * trace_test -> round_and_divide (R/verify.py:60-155) for every candidate of
  * one search.  For candidate k the smaller-degree side of {pat, complement}
  * is rebuilt in double-double, screened by power-sum integrality, rounded,
- * and trial-divided into p modulo three primes (2^61-1, 2^62-57, 2^63-25).
+ * and trial-divided into p modulo three primes (2^31-1, 2^31-19, 2^31-61).
  *   pats[m]          candidate patterns (bit i = rho index i)
  *   p_mod[3*(d+1)]   coefficients of the monic input p (low->high) mod the
  *                    primes returned by rfr_verify_primes

@@ -976,6 +976,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     ee.V.m_dev = nullptr;
     ee.V.found = &d_ctr->found;
     ee.V.t_found = &d_ctr->t_found;
+    if (g_tr.on == 1) ee.V.t_probe = &d_ctr->t_probe[0];
     ee.V.verdict = (uint8_t*)obase;
     ee.V.side = (uint8_t*)(obase + q_side);
     ee.V.coeffs = (long long*)(obase + q_coef);
@@ -1112,6 +1113,15 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
             cc.t_hit ? (double)((long long)cc.t_found - (long long)cc.t_hit) * 1e-3 : -1.0,
             cc.t_stop_first ? (double)((long long)cc.t_stop_first - (long long)cc.t_found) * 1e-3 : -1.0,
             cc.t_stop ? (double)((long long)cc.t_stop - (long long)cc.t_found) * 1e-3 : -1.0);
+  if (g_tr.on == 1 && cc.t_probe[3])
+    fprintf(stderr, "[rfr host] poller verify: expand %.1f us, integrality %.1f us, division %.1f us\n",
+            ((long long)cc.t_probe[0] - (long long)cc.t_probe[3]) * 1e-3,
+            ((long long)cc.t_probe[1] - (long long)cc.t_probe[0]) * 1e-3,
+            ((long long)cc.t_probe[2] - (long long)cc.t_probe[1]) * 1e-3);
+  if (g_tr.on == 1 && cc.t_found)
+    fprintf(stderr, "[rfr host] device: found->verified %.1f us, found->poller exit %.1f us\n",
+            cc.t_verified ? (double)((long long)cc.t_verified - (long long)cc.t_found) * 1e-3 : -1.0,
+            cc.t_poller_exit ? (double)((long long)cc.t_poller_exit - (long long)cc.t_found) * 1e-3 : -1.0);
   g_tr.mark("return");
   g_tr.dump();
   return RFR_OK;

@@ -108,6 +108,9 @@ struct DevCounters {
   unsigned long long t_stop;
   unsigned long long t_hit;
   unsigned long long t_stop_first;
+  unsigned long long t_verified;    // the poller finished verifying the stopping hit
+  unsigned long long t_poller_exit;
+  unsigned long long t_probe[4];    // RFR_HOST_TRACE: phases of the poller's verification
   // the stop flag on a cache line of its own: every join CTA reads it once per
   // bucket, and the counters above take the CTAs' end-of-join atomics (on a
   // shared line those queued the flag reads for up to ~100 us)

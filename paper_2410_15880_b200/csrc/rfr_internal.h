@@ -77,6 +77,7 @@ struct VerifyArgs {
   unsigned long long* peer_found[kMaxPeers] = {};
   int npeers = 0;
   unsigned long long* t_found = nullptr;  // with found: globaltimer of the first PASS
+  unsigned long long* t_probe = nullptr;  // diagnostics: phase timestamps of one verification
   const uint64_t* p_mod;  // 3 x (d+1)
   uint64_t primes[3];
   uint8_t* verdict;
@@ -90,8 +91,9 @@ cudaError_t launch_early_exit_poller(const JoinPlan& P, const ListBufs& base, co
                                      const uint64_t* d_keys2, int n, uint64_t lo2, uint64_t width2,
                                      uint64_t* d_post, unsigned long long post_cap, const VerifyArgs& V,
                                      DevCounters* d_ctr, int join_ctas, cudaStream_t s);
-// Primes of the modular division test, P = 2^k - c with small c (fast
-// reduction in the verify kernel): 2^61 - 1, 2^62 - 57, 2^63 - 25.
-constexpr uint64_t kVerifyPrimes[3] = {2305843009213693951ull, 4611686018427387847ull,
-                                       9223372036854775783ull};
+// Primes of the modular division test, P = 2^31 - c with small c (products
+// fit 64-bit registers, two folds reduce them): 2^31 - 1, 2^31 - 19,
+// 2^31 - 61.  The test is a filter: every factor the host keeps is confirmed
+// by exact division.
+constexpr uint64_t kVerifyPrimes[3] = {2147483647ull, 2147483629ull, 2147483587ull};
 }  // namespace rfr

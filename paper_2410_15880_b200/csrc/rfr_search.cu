@@ -1118,6 +1118,7 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
         __syncwarp();
         if (k < a.post_cap && (long long)k < a.V.m) verify_one(a.V, PS, B, (long long)k, lane);
         __syncwarp();
+        if (lane == 0 && t != 0 && a.ctr->t_verified == 0 && a.ctr->t_found) a.ctr->t_verified = rfr_globaltimer();
       }
       done++;
       if (lane == 0) {
@@ -1129,6 +1130,7 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
     if (clock64() - t0 > a.max_cycles) break;
     __nanosleep(1000);
   }
+  if (lane == 0) a.ctr->t_poller_exit = rfr_globaltimer();
 }
 
 cudaError_t launch_early_exit_poller(const JoinPlan& P, const ListBufs& base, const ListHist& hist,

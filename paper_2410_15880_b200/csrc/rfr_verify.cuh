@@ -54,23 +54,20 @@ struct WarpBuf {
   ddv c[2][kMaxE + 2];
   double mag[2][kMaxE + 2];
   double magp[2][kMaxE + 2];
-  uint64_t rem[3][kMaxD + 1];  // p mod each prime, reduced in lockstep
+  uint32_t rem[3][kMaxD + 1];  // p mod each prime, reduced in lockstep
   long long q[kMaxE + 1];
 };
 
-// a * b mod P for P = 2^k - c (c small, a, b < P): the 2k-bit product
-// x = xh 2^k + xl is folded twice with 2^k = c (mod P), leaving z < 2P.
-__device__ __forceinline__ uint64_t mulmod_k(uint64_t a, uint64_t b, uint64_t P, int k, uint64_t c) {
-  const uint64_t mask = (1ull << k) - 1ull;
-  const uint64_t lo = a * b, hi = __umul64hi(a, b);
-  const uint64_t xh = (hi << (64 - k)) | (lo >> k), xl = lo & mask;  // xh < 2^k
-  const uint64_t tl = xh * c, th = __umul64hi(xh, c);
-  const uint64_t yl = xl + tl, yh = th + (yl < xl ? 1ull : 0ull);     // y = xl + xh c
-  const uint64_t zh = (yh << (64 - k)) | (yl >> k);                   // y >> k <= c
-  uint64_t z = (yl & mask) + zh * c;                                   // < P + c + c^2
-  if (z >= P) z -= P;
-  if (z >= P) z -= P;
-  return z;
+// a * b mod P for P = 2^31 - c (c < 2^10, a, b < P): the 62-bit product
+// x = xh 2^31 + xl folds twice with 2^31 = c (mod P) inside 64-bit
+// registers (one wide multiply-add each), leaving z < 2P: ~10 instructions,
+// against ~45 for the 61-63-bit primes of round 1, whose 128-bit products
+// made the division the slowest part of a verification.
+__device__ __forceinline__ uint32_t mulmod31(uint32_t a, uint32_t b, uint32_t P, uint32_t c) {
+  const uint64_t x = (uint64_t)a * b;
+  const uint64_t y = (x >> 31) * c + (x & 0x7fffffffull);   // < 2^41
+  uint32_t z = (uint32_t)((y >> 31) * c + (y & 0x7fffffffull));  // < 2^31 + 2^20
+  return z >= P ? z - P : z;
 }
 
 // The profile, staged once per CTA in shared memory: the product loop below
@@ -101,6 +98,7 @@ __device__ __forceinline__ void stage_profile_smem(ProfSmem& PS, const VerifyArg
 // A.verdict[k] and, on PASS, A.coeffs row k (and raises *A.found if set).
 __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& PS, WarpBuf& B,
                                         long long k, int lane) {
+  if (A.t_probe && lane == 0 && A.t_probe[3] == 0) A.t_probe[3] = rfr_globaltimer();
   const uint64_t full = A.n >= 64 ? ~0ull : ((1ull << A.n) - 1ull);
   const uint64_t s = A.pats[k] & full;
   int deg_s = 0;
@@ -169,6 +167,7 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
     __syncwarp();
   }
   // len == e + 1
+  if (A.t_probe && lane == 0 && A.t_probe[0] == 0) A.t_probe[0] = rfr_globaltimer();
 
   // ---- integrality with a derived error bound
   const double arith = (double)(4 * e + 8) * 7.9e-31;  // ~ (4e+8) * 2^-100
@@ -216,31 +215,30 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
     return;
   }
 
-  // ---- trial division of p by q modulo three primes, the three divisions
-  // interleaved step by step (independent mulmod chains per lane)
-  uint64_t* qm0 = reinterpret_cast<uint64_t*>(&B.mag[0][0]);   // q mod P_i: the magnitude
-  uint64_t* qm1 = reinterpret_cast<uint64_t*>(&B.mag[1][0]);   // arrays are dead here
-  uint64_t* qm2 = reinterpret_cast<uint64_t*>(&B.magp[0][0]);
-  uint64_t* qmv[3] = {qm0, qm1, qm2};
-  uint64_t P[3], pc[3];
-  int pk[3];
+  if (A.t_probe && lane == 0 && A.t_probe[1] == 0) A.t_probe[1] = rfr_globaltimer();
+  // ---- trial division of p by q modulo three 31-bit primes, the three
+  // divisions interleaved step by step (independent mulmod chains per lane)
+  uint32_t* qm0 = reinterpret_cast<uint32_t*>(&B.mag[0][0]);   // q mod P_i: the magnitude
+  uint32_t* qm1 = reinterpret_cast<uint32_t*>(&B.mag[1][0]);   // arrays are dead here
+  uint32_t* qm2 = reinterpret_cast<uint32_t*>(&B.magp[0][0]);
+  uint32_t* qmv[3] = {qm0, qm1, qm2};
+  uint32_t P[3], pc[3];
 #pragma unroll
   for (int pi = 0; pi < 3; pi++) {
-    P[pi] = A.primes[pi];
-    pk[pi] = 64 - __clzll((long long)P[pi]);  // P = 2^pk - pc
-    pc[pi] = (1ull << pk[pi]) - P[pi];
+    P[pi] = (uint32_t)A.primes[pi];
+    pc[pi] = 0x80000000u - P[pi];  // P = 2^31 - c
     const uint64_t* pm = A.p_mod + (size_t)pi * (A.d + 1);
-    for (int j = lane; j <= A.d; j += 32) B.rem[pi][j] = pm[j];
-    for (int j = lane; j < e; j += 32) {  // |q_j| < 2^62, so one reduction each
+    for (int j = lane; j <= A.d; j += 32) B.rem[pi][j] = (uint32_t)pm[j];
+    for (int j = lane; j < e; j += 32) {  // |q_j| < 2^62: one 64-bit remainder each
       const long long qj = B.q[j];
       const uint64_t aq = qj >= 0 ? (uint64_t)qj : (uint64_t)(-qj);
-      const uint64_t r = aq % P[pi];
+      const uint32_t r = (uint32_t)(aq % P[pi]);
       qmv[pi][j] = (qj >= 0 || r == 0) ? r : P[pi] - r;
     }
   }
   __syncwarp();
   for (int kk = A.d - e; kk >= 0; kk--) {
-    uint64_t lead[3];
+    uint32_t lead[3];
 #pragma unroll
     for (int pi = 0; pi < 3; pi++) lead[pi] = B.rem[pi][kk + e];  // q monic
     __syncwarp();
@@ -252,14 +250,15 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
       if (j < e) {
 #pragma unroll
         for (int pi = 0; pi < 3; pi++) {
-          const uint64_t sub = mulmod_k(lead[pi], qmv[pi][j], P[pi], pk[pi], pc[pi]);
-          const uint64_t r0 = B.rem[pi][kk + j];
+          const uint32_t sub = mulmod31(lead[pi], qmv[pi][j], P[pi], pc[pi]);
+          const uint32_t r0 = B.rem[pi][kk + j];
           B.rem[pi][kk + j] = r0 >= sub ? r0 - sub : r0 + P[pi] - sub;
         }
       }
     }
     __syncwarp();
   }
+  if (A.t_probe && lane == 0 && A.t_probe[2] == 0) A.t_probe[2] = rfr_globaltimer();
   bool nz = false;
   for (int j = lane; j < e; j += 32) nz |= (B.rem[0][j] | B.rem[1][j] | B.rem[2][j]) != 0;
   const bool divides = !__any_sync(0xffffffffu, nz);

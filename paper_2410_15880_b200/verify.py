@@ -398,6 +398,7 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
     pieces' patterns only imply some factors (t minus a pattern inside t),
     which a greedy cover by minimal patterns would leave merged."""
     cells = [(full, p)]
+    bad = []  # device PASSes the exact division refutes (the device test is a filter)
     for t in sorted(found, key=lambda x: (bin(x).count("1"), x)):
         q = found[t]
         refined = []
@@ -408,6 +409,8 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
                 continue
             if inter == t:  # the pattern lies inside the cell: pc = q * (pc / q)
                 g, r = q, divide_exact(pc, q)
+                if r is None:
+                    bad.append(t)
             else:  # partial overlap: the common factor
                 g = poly_gcd(pc, q)
                 r = divide_exact(pc, g) if g.degree >= 1 else None
@@ -416,6 +419,7 @@ def _factor_cells(found: dict, p: IntPolynomial, full: int) -> list:
                 continue
             refined += [(inter, g), (c & ~t, r)]
         cells = refined
+    _factor_cells.bad = bad
     return cells
 
 
@@ -734,6 +738,16 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
         stats.verify_seconds += time.perf_counter() - t0
         return [p]
     cells = _factor_cells(found, p, full)
+    if _factor_cells.bad:
+        # a device PASS that exact division refutes: after a stop its pieces
+        # were searched around a non-factor, so search the whole space; after
+        # a whole search, drop it
+        stats.verify_seconds += time.perf_counter() - t0
+        if stopped:
+            return _factor_monic_squarefree(p, cfg, workers, stats, prof, early_exit=False)
+        for t in _factor_cells.bad:
+            found.pop(t, None)
+        cells = _factor_cells(found, p, full)
     if stopped and any(pc.degree != selected_degree(c, prof) for c, pc in cells):
         # inconsistent cells after a stopped search (not seen): search the whole space
         stats.verify_seconds += time.perf_counter() - t0
