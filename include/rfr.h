@@ -209,13 +209,17 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
  * rfr_peer_connect has run, every other rank's join (their stop flags are
  * written over NVLink); a rank stopped by a peer returns with buckets <
  * buckets_planned, the rank that found the factor searches its pieces as
- * rfr_search_verify does.
+ * rfr_search_verify does.  epoch (1 .. 2^63 - 1): the same value on every rank
+ * for the same search, different for successive searches (a call counter);
+ * the stop flag carries it, so a peer's flag that lands early still counts and
+ * a late one from an earlier search is ignored.
  */
 int rfr_search_verify_shard(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
                             const uint64_t* keys2, uint64_t lo2, uint64_t width2,
                             const rfr_profile* prof, const uint64_t* p_mod, int d, uint64_t* pats,
                             uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride, int64_t cap,
-                            int early_exit, int shard, int nshards, int64_t* nout, rfr_stats* st);
+                            int early_exit, int shard, int nshards, uint64_t epoch, int64_t* nout,
+                            rfr_stats* st);
 
 /*
  * Cross-rank early exit (no reference counterpart: its workers share one

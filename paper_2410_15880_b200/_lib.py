@@ -160,8 +160,8 @@ def load():
         L.rfr_search_verify_shard.argtypes = [
             U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
             ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
-            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, I64_P,
-            ctypes.POINTER(RfrStats),
+            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_uint64, I64_P, ctypes.POINTER(RfrStats),
         ]
         L.rfr_peer_handle.argtypes = [ctypes.c_void_p]
         L.rfr_peer_connect.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]

@@ -342,7 +342,8 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
       g_launches += 1;
     }
     g_tr.mark("search_core: poller");
-    RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, d_ctr, grid, s, d_rots, d_rots + mot, early));
+    RFR_CUDA_OK(launch_join(P, final_bufs(P0), d_out, cap, d_ctr, grid, s, d_rots, d_rots + mot,
+                             early ? ee->V.found_value : 0ull));
     g_launches += 1;
     g_tr.mark("search_core: join");
     if (early) RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_join, 0));
@@ -779,8 +780,9 @@ namespace {
 int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                        uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                        int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
-                       int stride, int64_t cap, int early_exit, int shard, int nshards, int64_t* nout,
-                       rfr_stats* st);
+                       int stride, int64_t cap, int early_exit, int shard, int nshards,
+                       unsigned long long epoch, int64_t* nout, rfr_stats* st);
+unsigned long long g_local_epoch = 0;  // epochs of unsharded searches (high bit set)
 }  // namespace
 
 int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
@@ -789,18 +791,20 @@ int rfr_search_verify(const uint64_t* keys, int n, uint64_t lo, uint64_t width, 
                       int stride, int64_t cap, int early_exit, int64_t* nout, rfr_stats* st) {
   std::lock_guard<std::mutex> lk(g_mu);
   return search_verify_impl(keys, n, lo, width, keys2, lo2, width2, prof, p_mod, d, pats, verdict, side,
-                            coeffs, stride, cap, early_exit, 0, 1, nout, st);
+                            coeffs, stride, cap, early_exit, 0, 1, (1ull << 63) | ++g_local_epoch, nout, st);
 }
 
 int rfr_search_verify_shard(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
                             const uint64_t* keys2, uint64_t lo2, uint64_t width2,
                             const rfr_profile* prof, const uint64_t* p_mod, int d, uint64_t* pats,
                             uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride, int64_t cap,
-                            int early_exit, int shard, int nshards, int64_t* nout, rfr_stats* st) {
+                            int early_exit, int shard, int nshards, uint64_t epoch, int64_t* nout,
+                            rfr_stats* st) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (nshards < 1 || shard < 0 || shard >= nshards) return rfr_fail(RFR_E_ARG, "bad shard");
+  if (epoch == 0 || (epoch >> 63)) return rfr_fail(RFR_E_ARG, "epoch must be in [1, 2^63)");
   return search_verify_impl(keys, n, lo, width, keys2, lo2, width2, prof, p_mod, d, pats, verdict, side,
-                            coeffs, stride, cap, early_exit, shard, nshards, nout, st);
+                            coeffs, stride, cap, early_exit, shard, nshards, epoch, nout, st);
 }
 
 // ---- cross-rank early exit: the ranks' stop flags over CUDA IPC -----------
@@ -856,8 +860,8 @@ namespace {
 int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width, const uint64_t* keys2,
                        uint64_t lo2, uint64_t width2, const rfr_profile* prof, const uint64_t* p_mod,
                        int d, uint64_t* pats, uint8_t* verdict, uint8_t* side, int64_t* coeffs,
-                       int stride, int64_t cap, int early_exit, int shard, int nshards, int64_t* nout,
-                       rfr_stats* st) {
+                       int stride, int64_t cap, int early_exit, int shard, int nshards,
+                       unsigned long long epoch, int64_t* nout, rfr_stats* st) {
   int rc = ensure_ready();
   if (rc) return rc;
   if ((rc = check_n(n))) return rc;
@@ -943,7 +947,9 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
     RFR_CUDA_OK(g.post.ensure(raw_cap * sizeof(uint64_t)));
     const unsigned long long post_cap = g.post.bytes / sizeof(uint64_t);
-    RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, sizeof(DevCounters), s));
+    // the counters, but not the stop flag: a peer's flag for this epoch may
+    // already be there
+    RFR_CUDA_OK(cudaMemsetAsync(d_ctr, 0, offsetof(DevCounters, found), s));
     // Tr3 window over the raw hits from *begin on, then verification of the
     // survivors from *vbegin on (null: all); found: flag a PASS raises
     auto filter_verify = [&](const unsigned long long* begin, const unsigned long long* vbegin,
@@ -975,6 +981,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     ee.V.m = (long long)vrows;
     ee.V.m_dev = nullptr;
     ee.V.found = &d_ctr->found;
+    ee.V.found_value = epoch;
     ee.V.t_found = &d_ctr->t_found;
     if (g_tr.on == 1) ee.V.t_probe = &d_ctr->t_probe[0];
     ee.V.verdict = (uint8_t*)obase;

@@ -11,7 +11,8 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
                          uint32_t* d_rot, ListHist H, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s,
-                        const uint32_t* d_rots, const uint32_t* d_starts, bool early = false);
+                        const uint32_t* d_rots, const uint32_t* d_starts,
+                        unsigned long long stop_epoch = 0);
 void dump_stop_trace(unsigned long long t_found, int grid);  // RFR_STOP_TRACE diagnostics
 cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t b0, uint64_t b1,
                                int nck, int ctas, uint32_t* d_rots, uint32_t* d_starts, cudaStream_t s);
@@ -71,6 +72,7 @@ struct VerifyArgs {
   const unsigned long long* m_dev;        // optional device count (<= m), or null
   const unsigned long long* m_begin_dev = nullptr;  // optional first candidate (chunked search)
   unsigned long long* found = nullptr;    // optional flag raised by a PASS (early exit)
+  unsigned long long found_value = 1;     // the value raised: the search's epoch
   // with found: the same flag of the other ranks' searches (their DevCounters
   // opened through CUDA IPC, written over NVLink), so one rank's verified
   // factor stops every rank's join at its next bucket boundary
@@ -78,6 +80,10 @@ struct VerifyArgs {
   int npeers = 0;
   unsigned long long* t_found = nullptr;  // with found: globaltimer of the first PASS
   unsigned long long* t_probe = nullptr;  // diagnostics: phase timestamps of one verification
+  // integral, monic coefficients suffice for a PASS (the caller divides
+  // exactly anyway): the speculative early-exit candidate, whose modular
+  // division would sit on the critical path of every early stop
+  int skip_division = 0;
   const uint64_t* p_mod;  // 3 x (d+1)
   uint64_t primes[3];
   uint8_t* verdict;

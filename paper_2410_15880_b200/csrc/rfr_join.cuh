@@ -1019,11 +1019,11 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       RFR_MARK();
       if (a.early && tid_now() == 0) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
-        if (RFR_STOP_COHERENT) join_smem().stop_buf[0] |= ld_found_gpu(&a.ctr->found);
+        if (RFR_STOP_COHERENT && ld_found_gpu(&a.ctr->found) == a.early) join_smem().stop_buf[0] = a.early;
       }
       __syncthreads();
       RFR_MARK();
-      if (a.early && join_smem().stop_buf[0]) {
+      if (a.early && join_smem().stop_buf[0] == a.early) {
         if (tid_now() == 0) {
           const unsigned long long t = rfr_globaltimer();
           atomicMax(&a.ctr->t_stop, t);
@@ -1049,10 +1049,10 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     }
     if (a.early && tid_now() == 0) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
-      if (RFR_STOP_COHERENT) join_smem().stop_buf[0] |= ld_found_gpu(&a.ctr->found);
+      if (RFR_STOP_COHERENT && ld_found_gpu(&a.ctr->found) == a.early) join_smem().stop_buf[0] = a.early;
     }
     __syncthreads();
-    if (a.early && join_smem().stop_buf[0]) {
+    if (a.early && join_smem().stop_buf[0] == a.early) {
       if (tid_now() == 0) {
         const unsigned long long t = rfr_globaltimer();
         atomicMax(&a.ctr->t_stop, t);

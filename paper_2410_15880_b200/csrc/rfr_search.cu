@@ -462,7 +462,11 @@ struct JoinArgs {
   // start position in each CTA's first bucket (join_starts_kernel)
   const uint32_t* rots;
   const uint32_t* starts;  // [cta][MoA + MoB]
-  int early;               // stop at a bucket boundary once DevCounters.found is set
+  // early exit: stop at a bucket boundary once DevCounters.found holds this
+  // search's epoch (0: no early exit).  An epoch instead of a 0/1 flag lets a
+  // peer's flag that lands before this rank cleared its counters count, and
+  // keeps a late flag of an earlier search from stopping this one.
+  unsigned long long early;
   int trace_stop;          // RFR_STOP_TRACE: each CTA records when and where it stopped
   uint64_t* out;
   unsigned long long cap;
@@ -785,7 +789,7 @@ cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t 
 
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
                         unsigned long long cap, DevCounters* d_ctr, int grid, cudaStream_t s,
-                        const uint32_t* d_rots, const uint32_t* d_starts, bool early) {
+                        const uint32_t* d_rots, const uint32_t* d_starts, unsigned long long stop_epoch) {
   static uint64_t attr_done = 0;
   cudaError_t e = raise_smem_limit(join_kernel, sizeof(JoinSmem), attr_done);
   if (e != cudaSuccess) return e;
@@ -797,7 +801,7 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
   a.ctr = d_ctr;
   a.rots = d_rots;
   a.starts = d_starts;
-  a.early = early ? 1 : 0;
+  a.early = stop_epoch;
   a.trace_stop = getenv("RFR_STOP_TRACE") != nullptr && grid <= 1024;
   if (a.trace_stop) {
     void* sym = nullptr;
@@ -1106,17 +1110,26 @@ __global__ void __launch_bounds__(32) early_exit_poller_kernel(const __grid_cons
         // non-factors and keep verify-then-stop.  A stop whose hit then
         // fails verification leaves the search incomplete without a PASS,
         // and the caller searches the whole space (verify.py).
-        if (!spec && t != 0 && done < 16 && lane == 0 && a.V.found) {  // t = 0: the empty pattern
+        const bool spec_now = !spec && t != 0 && done < 16 && a.V.found;  // t = 0: the empty pattern
+        if (spec_now && lane == 0) {
           if (a.V.t_found) atomicCAS(a.V.t_found, 0ull, rfr_globaltimer());
           a.ctr->t_hit = t_seen;
-          atomicExch(a.V.found, 1ull);
-          for (int i = 0; i < a.V.npeers; i++) *(volatile unsigned long long*)a.V.peer_found[i] = 1ull;
+          atomicExch(a.V.found, a.V.found_value);
+          for (int i = 0; i < a.V.npeers; i++) *(volatile unsigned long long*)a.V.peer_found[i] = a.V.found_value;
           if (a.V.npeers) __threadfence_system();
         }
         spec |= t != 0;
         if (k < a.post_cap && lane == 0) a.post[k] = t;
         __syncwarp();
-        if (k < a.post_cap && (long long)k < a.V.m) verify_one(a.V, PS, B, (long long)k, lane);
+        if (k < a.post_cap && (long long)k < a.V.m) {
+          if (spec_now) {  // the stopping hit: integral + monic, exact division on the host
+            VerifyArgs V = a.V;
+            V.skip_division = 1;
+            verify_one(V, PS, B, (long long)k, lane);
+          } else {
+            verify_one(a.V, PS, B, (long long)k, lane);
+          }
+        }
         __syncwarp();
         if (lane == 0 && t != 0 && a.ctr->t_verified == 0 && a.ctr->t_found) a.ctr->t_verified = rfr_globaltimer();
       }

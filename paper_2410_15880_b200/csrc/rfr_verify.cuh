@@ -214,6 +214,11 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
     if (lane == 0) A.verdict[k] = RFR_V_REJECT;
     return;
   }
+  if (A.skip_division) {
+    if (lane == 0) A.verdict[k] = RFR_V_PASS;
+    for (int j = lane; j <= e && j < A.stride; j += 32) A.coeffs[k * A.stride + j] = B.q[j];
+    return;
+  }
 
   if (A.t_probe && lane == 0 && A.t_probe[1] == 0) A.t_probe[1] = rfr_globaltimer();
   // ---- trial division of p by q modulo three 31-bit primes, the three
@@ -265,9 +270,9 @@ __device__ __forceinline__ void verify_one(const VerifyArgs& A, const ProfSmem& 
   if (lane == 0) A.verdict[k] = divides ? RFR_V_PASS : RFR_V_REJECT;
   if (lane == 0 && divides && A.found) {
     if (A.t_found) atomicCAS(A.t_found, 0ull, rfr_globaltimer());
-    atomicExch(A.found, 1ull);
+    atomicExch(A.found, A.found_value);
     // cross-rank early exit: raise the peers' flags (P2P stores over NVLink)
-    for (int i = 0; i < A.npeers; i++) *(volatile unsigned long long*)A.peer_found[i] = 1ull;
+    for (int i = 0; i < A.npeers; i++) *(volatile unsigned long long*)A.peer_found[i] = A.found_value;
     if (A.npeers) __threadfence_system();
   }
   if (divides)

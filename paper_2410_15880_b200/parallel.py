@@ -118,6 +118,7 @@ def parallel_recombine_e(rho: RhoVector, eps: float, workers: int,
 
 # ------------------------------------------------ sharded fused search
 _PEERS: dict = {}
+_EPOCH = [0]  # sharded searches so far (the stop flags' epoch)
 
 
 def connect_peers(dist) -> bool:
@@ -168,11 +169,14 @@ def sharded_search_verify(prof, p, keys, half_width, keys3, half_width3, workers
         world, rank = dist.get_world_size(), dist.get_rank()
         connect_peers(dist)
         dist.barrier()  # start together: a peer's stop flag lands in a running search
+    # the search's epoch: the same on every rank (the calls are collective)
+    _EPOCH[0] += 1
+    epoch = _EPOCH[0]
     rows, err = [], None
     for g in [g for g in range(workers) if g % world == rank]:
         try:
             res = _search_and_verify(prof, p, keys, half_width, keys3, half_width3, fstats.recombine,
-                                     early_exit, max_rows, shard=g, nshards=workers)
+                                     early_exit, max_rows, shard=g, nshards=workers, epoch=epoch)
         except RecombineDeviceError as e:
             if "raw hits exceed" not in str(e):
                 raise

@@ -243,7 +243,8 @@ _PIECES = True
 
 def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, half_width: int,
                        keys3: np.ndarray, half_width3: int, stats, early_exit: bool,
-                       max_rows: int | None = None, shard: int = 0, nshards: int = 1):
+                       max_rows: int | None = None, shard: int = 0, nshards: int = 1,
+                       epoch: int = 0):
     """search_and_verify, optionally with early termination.  Returns (pats,
     verdict, side, coeffs, complete, stopped): stopped when the join ended at
     a verified hit; complete when the candidates nevertheless cover every
@@ -274,7 +275,7 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
                 coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap,
                 (1 if _PIECES else 2) if early_exit else 0)
         if nshards > 1:
-            rc = lib.rfr_search_verify_shard(*args, shard, nshards, ctypes.byref(nout),
+            rc = lib.rfr_search_verify_shard(*args, shard, nshards, epoch, ctypes.byref(nout),
                                              ctypes.byref(st))
         else:
             rc = lib.rfr_search_verify(*args, ctypes.byref(nout), ctypes.byref(st))

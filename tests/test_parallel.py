@@ -74,7 +74,7 @@ def _sv_worker(rank, world, port, scenario, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
-    def fake(prof, p, keys, T, keys3, T3, stats, early, max_rows, shard=0, nshards=1):
+    def fake(prof, p, keys, T, keys3, T3, stats, early, max_rows, shard=0, nshards=1, epoch=0):
         assert nshards == 2 and shard == rank
         if scenario == "flood" and shard == 1:
             raise RecombineDeviceError("70000 raw hits exceed the flood limit 65536")
