@@ -275,7 +275,12 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     *r_bits = 0;
     if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[0], s));
     if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
-    RFR_CUDA_OK(launch_exhaustive(d_keys, n, lo, width, d_out, cap, (DevCounters*)g.ctr.p, s));
+    // RFR_FORCE_EXHAUSTIVE: the Gray-code brute force (the checker); else the
+    // in-CTA meet in the middle (RFR_SMALL_EXHAUSTIVE=1: brute force, A/B)
+    if (forced || getenv("RFR_SMALL_EXHAUSTIVE"))
+      RFR_CUDA_OK(launch_exhaustive(d_keys, n, lo, width, d_out, cap, (DevCounters*)g.ctr.p, s));
+    else
+      RFR_CUDA_OK(launch_table_search(d_keys, n, lo, width, d_out, cap, (DevCounters*)g.ctr.p, s));
     g_launches = 1;
     if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[2], s));
     return RFR_OK;

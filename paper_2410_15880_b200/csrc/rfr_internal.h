@@ -25,8 +25,13 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
                              unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
                              const unsigned long long* d_begin = nullptr);
-constexpr int kExhaustiveMaxN = 27;  // search_core: exhaustive kernel at or below this width (break-even with the join ~28)
+// search_core: at or below this width one small-search kernel (table_search_kernel,
+// an in-CTA meet in the middle) replaces the lists and the join
+constexpr int kExhaustiveMaxN = 31;  // table vs join crossover (profiles/r2f_small_search.txt)
 constexpr int kExhaustiveForceMaxN = 44;  // RFR_FORCE_EXHAUSTIVE (tests): up to 2^43 patterns, ~1 s
+cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
+                                uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
+                                cudaStream_t s);
 cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
                               uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
                               cudaStream_t s);

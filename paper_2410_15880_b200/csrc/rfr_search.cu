@@ -978,6 +978,112 @@ cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------- table search
+// Small searches (n <= kTableMaxN, one shard; every piece search after an
+// early stop): a one-sided meet in the middle inside each CTA.  The 2^b subset
+// sums of the low b keys are built and bitonic-sorted in shared memory; each
+// thread walks a range of high-bit patterns in Gray-code order (one key added
+// or removed per step) and finds the low sums that complete its partial sum
+// into the window by one binary search of the table: b steps per 2^b
+// patterns instead of one add and one compare per pattern (the Gray-code
+// exhaustive_kernel, kept as the independent checker of RFR_FORCE_EXHAUSTIVE).
+constexpr int kTableMaxBits = 12;
+__global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __restrict__ keys, int n,
+                                                           uint64_t lo, uint64_t width, int b, int g,
+                                                           uint64_t* __restrict__ out,
+                                                           unsigned long long cap, DevCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  uint64_t* tk = reinterpret_cast<uint64_t*>(tsm);                     // sorted low sums
+  uint16_t* ti = reinterpret_cast<uint16_t*>(tsm + (8u << b));         // their low patterns
+  __shared__ uint64_t sk[64];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += blockDim.x) sk[i] = keys[i];
+  __syncthreads();
+  const uint32_t nt = 1u << b;
+  for (uint32_t i = tid; i < nt; i += blockDim.x) {
+    uint64_t s = 0;
+    for (uint32_t u = i; u; u &= u - 1) s += sk[__ffs(u) - 1];
+    tk[i] = s;
+    ti[i] = (uint16_t)i;
+  }
+  __syncthreads();
+  // bitonic sort of (tk, ti) by tk
+  for (uint32_t kk = 2; kk <= nt; kk <<= 1) {
+    for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = tid; i < nt; i += blockDim.x) {
+        const uint32_t p = i ^ jj;
+        if (p > i) {
+          const bool up = (i & kk) == 0;
+          const uint64_t a = tk[i], c = tk[p];
+          if ((a > c) == up) {
+            tk[i] = c;
+            tk[p] = a;
+            const uint16_t t = ti[i];
+            ti[i] = ti[p];
+            ti[p] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int m = n - 1, h = m - b;
+  const uint64_t T = (uint64_t)blockIdx.x * blockDim.x + tid;
+  if (T == 0) atomicAdd(&ctr->queries, 1ull << m);  // patterns tested (stats)
+  if (h < 0 || (T << g) >> h) return;  // past 2^h high patterns
+  const uint64_t i0 = T << g;
+  uint64_t gh = i0 ^ (i0 >> 1), S = 0;  // Gray high pattern and its key sum
+  for (uint64_t u = gh; u; u &= u - 1) S += sk[b + __ffsll((long long)u) - 1];
+  const uint64_t steps = 1ull << g;
+  for (uint64_t st = 0;; st++) {
+    // low sums D with (S + D - lo) mod 2^64 <= width: D in [a, a + width] (mod 2^64)
+    const uint64_t a = lo - S;
+    uint32_t l = 0, r = nt;  // first D >= a
+    while (l < r) {
+      const uint32_t mid = (l + r) >> 1;
+      if (tk[mid] < a) l = mid + 1;
+      else r = mid;
+    }
+    auto emit = [&](uint32_t i) {
+      const unsigned long long k = atomicAdd(&ctr->out_count, 1ull);
+      if (k < cap) out[k] = (gh << b) | ti[i];
+    };
+    for (uint32_t i = l; i < nt && tk[i] - a <= width; i++) emit(i);
+    if (a + width < a)  // the window wraps past 2^64: its head is at the table's start
+      for (uint32_t i = 0; i < l && tk[i] <= a + width; i++) emit(i);
+    if (st + 1 == steps) break;
+    const int j = __ffsll((long long)(i0 + st + 1)) - 1;  // Gray step: toggle bit j
+    gh ^= 1ull << j;
+    S += ((gh >> j) & 1ull) ? sk[b + j] : 0ull - sk[b + j];
+  }
+}
+
+cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
+                                uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
+                                cudaStream_t s) {
+  const int m = n - 1;
+  // table bits: the per-CTA bitonic sort (latency-bound, ~b^2/2 barrier
+  // stages) against 2^(m-b) binary searches of b steps; RFR_TABLE_BITS (A/B)
+  static int forced_b = -1;
+  if (forced_b < 0) {
+    const char* e = getenv("RFR_TABLE_BITS");
+    forced_b = e ? atoi(e) : 0;
+  }
+  int b = forced_b > 0 ? forced_b : (m <= 30 ? 8 : (m <= 33 ? 10 : kTableMaxBits));
+  if (b > m) b = m;
+  if (b > kTableMaxBits) b = kTableMaxBits;
+  const int h = m - b;
+  const int g = h > 16 ? h - 16 : 0;  // <= 2^16 threads, 2^g high patterns each
+  const uint64_t threads = 1ull << (h - g);
+  const size_t smem = (size_t)10 << b;
+  static uint64_t attr_done = 0;
+  cudaError_t e = raise_smem_limit(table_search_kernel, (size_t)10 << kTableMaxBits, attr_done);
+  if (e != cudaSuccess) return e;
+  table_search_kernel<<<(unsigned)((threads + 255) / 256), 256, smem, s>>>(d_keys, n, lo, width, b, g,
+                                                                          d_out, cap, d_ctr);
+  return cudaGetLastError();
+}
+
 // Patterns of a piece's search (bit j = the j-th set bit of mask) rewritten
 // as patterns of the parent's search (rfr_search_verify after an early stop).
 __global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long long* __restrict__ count,

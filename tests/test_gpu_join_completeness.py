@@ -133,3 +133,53 @@ def _window_sets(keys, centre, T, monkeypatch):
         got4 = np.sort(np.concatenate([run(g, 4) for g in range(4)]))
     assert len(np.unique(ex)) == len(ex)
     return ex, got1, got4
+
+
+@pytest.mark.parametrize("n,kind", [(12, "random"), (20, "random"), (27, "random"), (30, "random"),
+                                    (31, "few"), (28, "few"), (30, "equal")])
+def test_small_search_table_kernel_equals_exhaustive(n, kind, monkeypatch):
+    """Searches of n <= 31 run table_search_kernel (a sorted table of low-key
+    sums per CTA, one binary search per high pattern); the Gray-code brute
+    force is its independent checker."""
+    rng = np.random.default_rng(4000 + n)
+    if kind == "random":
+        keys = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+        centre, T = 0, int(2000 * 2.0 ** (64 - n))
+    elif kind == "few":
+        vals = rng.integers(0, 2**64 - 1, size=6, dtype=np.uint64, endpoint=True)
+        keys = vals[rng.integers(0, 6, size=n)]
+        centre, T = int(sum(int(v) for v in keys[:5])) % TWO64, 1 << 20
+    else:
+        v = int(rng.integers(1, 2**63)) | 1
+        keys = np.full(n, v, dtype=np.uint64)
+        centre, T = (3 * v) % TWO64, 1 << 16
+    import ctypes
+
+    from paper_2410_15880_b200 import _lib
+
+    lib = _lib.load()
+    _lib.device()
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    lo, width = (centre - T) % TWO64, 2 * T
+
+    def run():
+        cap = 1 << 16
+        while True:
+            out = np.empty(cap, dtype=np.uint64)
+            nout = ctypes.c_int64(0)
+            st = _lib.RfrStats()
+            _lib.check(lib.rfr_search_keys(_lib.ptr(keys, _lib.U64_P), n, lo, width, 0, 1,
+                                           _lib.ptr(out, _lib.U64_P), cap, ctypes.byref(nout),
+                                           ctypes.byref(st)), "rfr_search_keys")
+            if nout.value <= cap:
+                return np.sort(out[: nout.value])
+            cap = int(nout.value)
+
+    with monkeypatch.context() as m:
+        m.delenv("RFR_FORCE_JOIN", raising=False)
+        m.delenv("RFR_FORCE_EXHAUSTIVE", raising=False)
+        got = run()
+    with monkeypatch.context() as m:
+        m.setenv("RFR_FORCE_EXHAUSTIVE", "1")
+        ex = run()
+    assert len(ex) > 0 and np.array_equal(got, ex), (len(got), len(ex))

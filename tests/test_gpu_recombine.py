@@ -25,7 +25,7 @@ TWO64 = 1 << 64
 
 @pytest.fixture(params=["exhaustive", "join"])
 def search_path(request, monkeypatch):
-    """Searches of n <= 27 run the exhaustive kernel; the parity tests run
+    """Searches of n <= 31 run the table kernel; the parity tests run
     each case on the quarter-list join as well (RFR_FORCE_JOIN)."""
     if request.param == "join":
         monkeypatch.setenv("RFR_FORCE_JOIN", "1")
