@@ -9,7 +9,8 @@ reference's own ``BenchRecord.from_csv`` and sit beside its rows in one CSV.
 (degree, trial), ``wall_s`` = the recombination stage unless
 ``include_roots``.  The backend column reads ``"e-b200"``; the GPU-side
 fields (GPUs, device time, pairs/s, HBM GB/s against the SURVEY s8(d)
-algorithmic bytes, roofline fraction) go in ``BenchRecord.extra`` and in
+algorithmic bytes and the roofline fraction, all over the whole device call:
+``*_call``) go in ``BenchRecord.extra`` and in
 ``to_json()``, not in the CSV.  The reference's argparse CLI itself is out of
 scope.
 """
@@ -108,9 +109,12 @@ def bench_rows(degrees, trials: int = 1, seed: int = 0, workers: int = 1,
             if dev_ms:
                 alg = algorithmic_bytes(st.n)
                 gbs = alg / (dev_ms * 1e-3) / 1e9
+                # over the whole fused call (lists, join -- stopped early when a
+                # factor verifies -- and verification): not bench.py's
+                # join-only roofline, hence the _call suffix
                 extra.update({"device_ms": dev_ms,
-                              "pairs_per_s": 2.0 ** (st.n - 1) / (dev_ms * 1e-3),
-                              "hbm_gbs_algorithmic": gbs, "roofline_frac": gbs / peak,
+                              "pairs_per_s_call": 2.0 ** (st.n - 1) / (dev_ms * 1e-3),
+                              "hbm_gbs_algorithmic_call": gbs, "roofline_frac_call": gbs / peak,
                               "peak_gbs": peak, "peak_source": peak_kind})
             yield BenchRecord(
                 d=d, n=st.n, backend=BACKEND_NAME, workers=workers, wall_s=wall,

@@ -35,4 +35,4 @@ def test_bench_rows_on_the_gpu():
         assert r.factors == 2 and r.backend == "e-b200" and r.n >= 10
         assert BenchRecord.from_csv(r.to_csv()).n == r.n
         extra = json.loads(r.to_json())
-        assert extra["device_ms"] > 0 and 0 < extra["roofline_frac"] < 10
+        assert extra["device_ms"] > 0 and 0 < extra["roofline_frac_call"] < 10
