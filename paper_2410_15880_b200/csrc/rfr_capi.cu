@@ -79,10 +79,11 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // early-exit poller, beside the join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fill = nullptr;
   DevVec keys, keys2, rho, raw, post, ctr, rotc, jstarts, pkeys;
   DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
+  DevVec pctr, praw, ppost;  // the two pieces' counters / raw hits / survivors (concurrent)
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
   void* h_stage = nullptr;       // pinned staging of rfr_verify (in, then out)
@@ -300,6 +301,14 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   char* hb[4];
   for (int i = 0; i < 4; i++) hb[i] = (char*)g.hist[i].p;
   const ListHist H = list_hist_layout(P0, hb);
+  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
+  const bool early = ee != nullptr && wins.size() == 1;
+  if (early) {
+    // the raw-hit slots start as kUnsetHit (the poller's "not yet written"):
+    // filled on the second stream while the lists are built
+    RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), g.stream2));
+    RFR_CUDA_OK(cudaEventRecord(g.ev_fill, g.stream2));
+  }
   g_tr.mark("search_core: lists launch");
   RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p, H, s));
   g_tr.mark("search_core: lists enqueued");
@@ -310,8 +319,6 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     g_launches += 1 + (maxbits > kBaseBits ? per_level * (maxbits - kBaseBits) : 0);
   }
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
-  DevCounters* d_ctr = (DevCounters*)g.ctr.p;
-  const bool early = ee != nullptr && wins.size() == 1;
   for (auto& w : wins) {
     // every piece reuses the geometry planned for the widest (first) piece
     JoinPlan P = P0;
@@ -337,7 +344,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     g_launches += 1;
     g_tr.mark("search_core: join starts");
     if (early) {
-      RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), s));  // kUnsetHit slots
+      RFR_CUDA_OK(cudaStreamWaitEvent(s, g.ev_fill, 0));  // kUnsetHit slots
       RFR_CUDA_OK(cudaEventRecord(g.ev_fork, s));
       RFR_CUDA_OK(cudaStreamWaitEvent(g.stream2, g.ev_fork, 0));
       RFR_CUDA_OK(launch_early_exit_poller(P0, bufs(0), H, (const uint32_t*)g.rotc.p, d_out, cap,
@@ -463,6 +470,115 @@ int check_profile(const rfr_profile* prof, int d) {
 // survivors) -- the caller reports the stop and the host factors the pieces.
 constexpr int kPieceMaxN = 48;   // whole-space searches above this size stop early themselves
 constexpr int kPieceRows = 64;
+constexpr unsigned long long kPieceRaw = 1ull << 16;  // raw hits per small piece (concurrent path)
+
+// search_pieces for two small pieces: the table kernel, the Tr3 window, the
+// deposit into parent patterns, the verification and the collection of each
+// piece on its own stream (g.stream and g.stream2), with its own counters,
+// raw and survivor buffers and verification rows.  Returns false when a
+// piece overflows (the caller's incomplete-search path takes over).
+bool search_small_pieces(const uint64_t* keys, const uint64_t* keys2, uint64_t lo, uint64_t width,
+                         uint64_t lo2, uint64_t width2, const uint64_t masks[2], const VerifyArgs& V0,
+                         int stride, cudaStream_t s, size_t per, std::vector<uint64_t>& xp,
+                         std::vector<uint8_t>& xv, std::vector<uint8_t>& xs, std::vector<int64_t>& xc,
+                         int64_t* buckets, int* rc) {
+  auto ok = [&](cudaError_t e, const char* what) { return (*rc = rfr_check_cuda(e, what)) == RFR_OK; };
+  if (!ok(g.pctr.ensure(2 * sizeof(DevCounters)), "piece counters") ||
+      !ok(g.praw.ensure(2 * kPieceRaw * sizeof(uint64_t)), "piece raw") ||
+      !ok(g.ppost.ensure(2 * kPieceRaw * sizeof(uint64_t)), "piece post"))
+    return false;
+  // both pieces' keys in one copy, staged after the two pieces' row areas:
+  // [piece][keys | keys2][64]
+  int ns[2] = {0, 0};
+  uint64_t* stage = (uint64_t*)((char*)g.h_piece + 2 * per);
+  const size_t stage_b = 2 * 128 * sizeof(uint64_t);
+  for (int pi = 0; pi < 2; pi++) {
+    int j = 0;
+    for (uint64_t mm = masks[pi]; mm; mm &= mm - 1, j++) {
+      const int i = __builtin_ctzll(mm);
+      stage[pi * 128 + j] = keys[i];
+      stage[pi * 128 + 64 + j] = keys2[i];
+    }
+    ns[pi] = j;
+  }
+  if (!ok(cudaMemcpyAsync(g.pkeys.p, stage, stage_b, cudaMemcpyHostToDevice, s), "piece keys") ||
+      !ok(cudaMemsetAsync(g.pctr.p, 0, 2 * sizeof(DevCounters), s), "piece counters") ||
+      !ok(cudaEventRecord(g.ev_fork, s), "fork") || !ok(cudaStreamWaitEvent(g.stream2, g.ev_fork, 0), "fork wait"))
+    return false;
+  // per piece: table search, Tr3 window, deposit, verification, collection;
+  // the launches of the two pieces alternate so neither stream waits on the
+  // host while the other's are enqueued
+  VerifyArgs A[2];
+  CollectArgs C[2];
+  for (int pi = 0; pi < 2; pi++) {
+    DevCounters* ctr = (DevCounters*)g.pctr.p + pi;
+    uint64_t* post = (uint64_t*)g.ppost.p + pi * kPieceRaw;
+    A[pi] = V0;
+    A[pi].pats = post;
+    A[pi].m = kPieceRows;
+    A[pi].m_dev = &ctr->post_count;
+    A[pi].m_begin_dev = nullptr;
+    A[pi].found = nullptr;
+    A[pi].verdict = V0.verdict + pi * kPieceRows;
+    A[pi].side = V0.side + pi * kPieceRows;
+    A[pi].coeffs = V0.coeffs + (size_t)pi * kPieceRows * stride;
+    char* hp = (char*)g.h_piece + pi * per;
+    char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+    C[pi].ctr = ctr;
+    C[pi].pats = post;
+    C[pi].verdict = A[pi].verdict;
+    C[pi].side = A[pi].side;
+    C[pi].coeffs = A[pi].coeffs;
+    C[pi].stride = stride;
+    C[pi].rows = kPieceRows;
+    C[pi].h_ctr = (DevCounters*)(hp + 2 * 64 * 8);
+    C[pi].h_pats = (uint64_t*)rows;
+    C[pi].h_verdict = (uint8_t*)(rows + kPieceRows * 8);
+    C[pi].h_side = (uint8_t*)(rows + kPieceRows * 9);
+    C[pi].h_coeffs = (long long*)(rows + kPieceRows * 10);
+  }
+  for (int stage = 0; stage < 5; stage++) {
+    for (int pi = 0; pi < 2; pi++) {
+      if (ns[pi] < 2) continue;  // one linear or quadratic entity: irreducible
+      cudaStream_t sp = pi ? g.stream2 : s;
+      DevCounters* ctr = (DevCounters*)g.pctr.p + pi;
+      uint64_t* dk = (uint64_t*)g.pkeys.p + pi * 128;
+      uint64_t* raw = (uint64_t*)g.praw.p + pi * kPieceRaw;
+      uint64_t* post = (uint64_t*)g.ppost.p + pi * kPieceRaw;
+      cudaError_t e = cudaSuccess;
+      switch (stage) {
+        case 0: e = launch_table_search(dk, ns[pi], lo, width, raw, kPieceRaw, ctr, sp); break;
+        case 1:
+          e = launch_keyfilter(dk + 64, ns[pi], raw, &ctr->out_count, kPieceRaw, lo2, width2, post, kPieceRaw,
+                               ctr, g.nsm, sp);
+          break;
+        case 2: e = launch_deposit(post, &ctr->post_count, kPieceRaw, masks[pi], g.nsm, sp); break;
+        case 3: e = launch_verify(A[pi], sp); break;
+        default: e = launch_collect(C[pi], sp); break;
+      }
+      if (!ok(e, "piece search")) return false;
+    }
+  }
+  if (!ok(cudaEventRecord(g.ev_join, g.stream2), "join") || !ok(cudaStreamWaitEvent(s, g.ev_join, 0), "join wait") ||
+      !ok(cudaStreamSynchronize(s), "piece sync"))
+    return false;
+  for (int pi = 0; pi < 2; pi++) {
+    if (ns[pi] < 2) continue;
+    const char* hp = (const char*)g.h_piece + pi * per;
+    const DevCounters c = *(const DevCounters*)(hp + 2 * 64 * 8);
+    if (c.out_count > kPieceRaw || c.post_count > (unsigned long long)kPieceRows) return false;
+    const char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+    for (unsigned long long k = 0; k < c.post_count; k++) {
+      xp.push_back(((const uint64_t*)rows)[k]);
+      xv.push_back(((const uint8_t*)(rows + kPieceRows * 8))[k]);
+      xs.push_back(((const uint8_t*)(rows + kPieceRows * 9))[k]);
+      const int64_t* cr = (const int64_t*)(rows + kPieceRows * 10) + k * stride;
+      xc.insert(xc.end(), cr, cr + stride);
+    }
+    *buckets += (int64_t)c.buckets;
+  }
+  return true;
+}
 bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t lo, uint64_t width,
                    uint64_t lo2, uint64_t width2, uint64_t t, const VerifyArgs& V0, int stride,
                    cudaStream_t s, std::vector<uint64_t>& xp, std::vector<uint8_t>& xv,
@@ -474,14 +590,21 @@ bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t 
     if (__builtin_popcountll(M) >= kPieceMaxN) return false;
   const size_t row_b = 8 + 1 + 1 + (size_t)stride * 8;
   const size_t per = 2 * 64 * 8 + sizeof(DevCounters) + kPieceRows * row_b;
-  if (g.h_piece_bytes < 2 * per) {
+  const size_t hbytes = 2 * per + 2 * 2 * 64 * sizeof(uint64_t);  // + both pieces' keys in one block
+  if (g.h_piece_bytes < hbytes) {
     if (g.h_piece) cudaFreeHost(g.h_piece);
     g.h_piece = nullptr;
     g.h_piece_bytes = 0;
-    if ((*rc = rfr_check_cuda(cudaMallocHost(&g.h_piece, 2 * per), "cudaMallocHost"))) return false;
-    g.h_piece_bytes = 2 * per;
+    if ((*rc = rfr_check_cuda(cudaMallocHost(&g.h_piece, hbytes), "cudaMallocHost"))) return false;
+    g.h_piece_bytes = hbytes;
   }
   if ((*rc = rfr_check_cuda(g.pkeys.ensure(2 * 2 * 64 * sizeof(uint64_t)), "pkeys"))) return false;
+  // both pieces small (the table kernel): searched concurrently, one on each
+  // stream, each with its own counters and buffers, one synchronisation
+  if (__builtin_popcountll(masks[0]) <= kExhaustiveMaxN && __builtin_popcountll(masks[1]) <= kExhaustiveMaxN &&
+      !getenv("RFR_FORCE_JOIN") && !getenv("RFR_SMALL_EXHAUSTIVE"))
+    return search_small_pieces(keys, keys2, lo, width, lo2, width2, masks, V0, stride, s, per, xp, xv, xs,
+                               xc, buckets, rc);
   DevCounters* d_ctr = (DevCounters*)g.ctr.p;
   const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
   const unsigned long long post_cap = g.post.bytes / sizeof(uint64_t);
@@ -575,7 +698,8 @@ static void release_ctx() {
   g.npeers = 0;
   if (g.stream) cudaStreamSynchronize(g.stream);
   DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts, &g.pkeys,
-                    &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef};
+                    &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef, &g.pctr, &g.praw,
+                    &g.ppost};
   for (DevVec* v : vecs) v->release();
   for (auto& h : g.hist) h.release();
   for (auto& a : g.lk)
@@ -586,6 +710,7 @@ static void release_ctx() {
     if (e) cudaEventDestroy(e);
   if (g.ev_fork) cudaEventDestroy(g.ev_fork);
   if (g.ev_join) cudaEventDestroy(g.ev_join);
+  if (g.ev_fill) cudaEventDestroy(g.ev_fill);
   if (g.stream2) cudaStreamDestroy(g.stream2);
   if (g.h_ctr) cudaFreeHost(g.h_ctr);
   if (g.h_stage) cudaFreeHost(g.h_stage);
@@ -608,6 +733,7 @@ static int init_ctx(int device) {
   for (auto& e : g.ev) RFR_CUDA_OK(cudaEventCreate(&e));
   RFR_CUDA_OK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
   RFR_CUDA_OK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+  RFR_CUDA_OK(cudaEventCreateWithFlags(&g.ev_fill, cudaEventDisableTiming));
   RFR_CUDA_OK(g.ctr.ensure(sizeof(DevCounters)));
   RFR_CUDA_OK(cudaMallocHost(&g.h_ctr, sizeof(DevCounters)));
   RFR_CUDA_OK(g.keys.ensure(64 * sizeof(uint64_t)));

@@ -124,6 +124,15 @@ __device__ __forceinline__ unsigned long long rfr_globaltimer() {
 }
 static_assert(offsetof(DevCounters, found) % 16 == 0, "found must be 16-byte aligned");
 
+// Programmatic dependent launch (the list levels and the join's start
+// positions, launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// a kernel waits for its predecessor's completion (and memory) before its
+// first global access, then lets its own successor launch, so the next
+// level's CTAs are resident and waiting when this one drains instead of
+// being launched after it (no-ops in a plain launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace rfr
 
 #define RFR_CUDA_OK(expr)                                   \

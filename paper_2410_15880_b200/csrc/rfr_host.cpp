@@ -301,17 +301,13 @@ static int squarefree_euclid(const uint64_t* cm, int d, uint64_t q, const Red R)
   return da == 0 ? 1 : 0;
 }
 
-// The same Euclid for q < 2^25 in doubles: residues are exact integers in
-// [0, q), the pseudo-division update A lb - la B stays below 2^51 in
-// magnitude (exact), and one floor-based reduction per entry brings it back
-// -- branch-free and vectorisable, several times faster than the 128-bit
-// products above.
-static inline double red_fp(double x, double q, double qinv) {
-  double r = x - std::floor(x * qinv) * q;
-  r += r < 0.0 ? q : 0.0;
-  r -= r >= q ? q : 0.0;
-  return r;
-}
+// The same Euclid for q < 2^25 in doubles: residues are exact integers kept
+// in the symmetric range |r| <= q/2 (+1 when x / q rounds the other way), so
+// the pseudo-division update A lb - la B stays below 2q^2 < 2^51 in magnitude
+// (exact), and one round-to-nearest reduction per entry, with no compare,
+// brings it back: branch-free, so the update loops vectorise (AVX2: 34 -> ~8
+// us at d = 100).  A residue is zero iff its representative is 0.0.
+static inline double red_fp(double x, double q, double qinv) { return x - std::rint(x * qinv) * q; }
 __attribute__((target_clones("avx2", "default")))
 static int squarefree_euclid_fp(const uint64_t* cm, int d, uint64_t q64) {
   const double q = (double)q64, qinv = 1.0 / q;

@@ -1,3 +1,4 @@
+#include <utility>
 #include <algorithm>
 #include <vector>
 #include <cstdio>
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __rest
                                                           JoinPlan P, ListBufs out, uint32_t* rot) {
   extern __shared__ __align__(16) unsigned char base_raw[];
   BaseSmem& S = *reinterpret_cast<BaseSmem*>(base_raw);
+  pdl_trigger();  // the first merge level may launch (it waits for this grid)
   const ListSpec L = pick_list(P, blockIdx.x);
   const int b = L.bits < kBaseBits ? L.bits : kBaseBits;
   const int len = 1 << b;
@@ -274,6 +276,8 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t wsum[kMergeThreads / 32];
   __shared__ uint32_t ssplit[2];
+  pdl_wait();  // the previous level (and its rotation counts) is complete
+  pdl_trigger();
   const int li = blockIdx.y;
   const ListSpec L = pick_list(P, li);
   if (L.bits <= k) return;
@@ -510,6 +514,7 @@ __global__ void __launch_bounds__(256) join_starts_kernel(JoinPlan P, const uint
                                                           uint64_t b0, uint64_t b1, int nck, int ctas,
                                                           uint32_t* __restrict__ rots,
                                                           uint32_t* __restrict__ starts) {
+  pdl_wait();  // the top list level is complete
   const int lane = threadIdx.x & 31;
   const uint32_t MoA = 1u << P.list[0].bits, MoB = 1u << P.list[2].bits, MoT = MoA + MoB;
   const uint64_t task = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -742,6 +747,32 @@ ListHist list_hist_layout(const JoinPlan& P, char* const base[4]) {
   return H;
 }
 
+// RFR_PDL=0 (A/B): plain launches for the list levels and the start positions
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RFR_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
                          uint32_t* d_rot, ListHist H, cudaStream_t s) {
   static uint64_t attr_done = 0;
@@ -771,8 +802,9 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
       lists_merge_kernel<2><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
           d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
     } else {
-      lists_merge_kernel<1><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
-          d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+      const cudaError_t le = launch_pdl(lists_merge_kernel<1>, dim3(blocks, 4), dim3(kMergeThreads), 0, s,
+                                        d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+      if (le != cudaSuccess) return le;
     }
   }
   return cudaGetLastError();
@@ -782,8 +814,11 @@ cudaError_t launch_join_starts(const JoinPlan& P, const ListBufs& fin, uint64_t 
                                int nck, int ctas, uint32_t* d_rots, uint32_t* d_starts, cudaStream_t s) {
   const uint64_t mot = (1ull << P.list[0].bits) + (1ull << P.list[2].bits);
   const uint64_t warps = mot * (1ull + (uint64_t)nck * (uint64_t)ctas);
-  join_starts_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(P, fin.k[0], fin.k[1], fin.k[2], fin.k[3],
-                                                                b0, b1, nck, ctas, d_rots, d_starts);
+  const cudaError_t e = launch_pdl(join_starts_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, P,
+                                   (const uint64_t*)fin.k[0], (const uint64_t*)fin.k[1],
+                                   (const uint64_t*)fin.k[2], (const uint64_t*)fin.k[3], b0, b1, nck, ctas,
+                                   d_rots, d_starts);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

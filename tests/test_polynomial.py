@@ -213,6 +213,39 @@ def test_squarefree_screen_never_accepts_a_square(q):
     assert accepted > 30
 
 
+def test_squarefree_screen_fp_path_is_exact_mod_q():
+    """The double-precision path (q < 2^25, symmetric residues reduced by
+    round-to-nearest) decides gcd(p, p') = 1 over F_q exactly as sympy's
+    GF(q) gcd does, up to degree 140 (where the residues are largest)."""
+    import ctypes
+
+    import numpy as np
+    import sympy
+
+    from paper_2410_15880_b200 import _lib
+
+    lib = _lib.load()
+    x = sympy.symbols("x")
+    q = 33554393
+    rng = random.Random(11)
+    yes = no = 0
+    for _ in range(40):
+        d = rng.randint(2, 140)
+        co = [rng.randrange(q) for _ in range(d)] + [1]
+        if rng.random() < 0.5:  # a square factor mod q
+            f = [rng.randrange(q) for _ in range(rng.randint(1, 4))] + [1]
+            pp = sympy.Poly(list(reversed(co)), x, modulus=q) * sympy.Poly(list(reversed(f)), x, modulus=q) ** 2
+            co = [int(c) % q for c in reversed(pp.all_coeffs())]
+        cm = np.array(co, dtype=np.uint64)
+        got = lib.rfr_squarefree_mod(cm.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(co) - 1, q)
+        poly = sympy.Poly(list(reversed(co)), x, modulus=q)
+        want = int(sympy.gcd(poly, poly.diff(x)).degree() == 0)
+        assert got == want
+        yes += want
+        no += 1 - want
+    assert yes > 5 and no > 5
+
+
 def test_factor_cells_split_implied_factors():
     """The factor partition (verify._factor_cells): after an early stop the
     candidates may hold t = f3*f4, f3 inside t, f1 inside ~t and nothing for
