@@ -75,6 +75,9 @@ typedef struct rfr_stats {
   double us_hit_to_stop;   /* rfr_search_verify with early exit: microseconds from the */
                            /* poller's verified hit to the last join CTA leaving its   */
                            /* bucket loop (device clock); -1 when it did not stop      */
+  int64_t pieces;          /* after an early stop: 0 the pieces were not searched in   */
+                           /* the call, 1 searched by host-driven launches, 2 searched */
+                           /* by kernels chained behind the main search on the device  */
 } rfr_stats;
 
 /* ---- lifecycle -------------------------------------------------------- */

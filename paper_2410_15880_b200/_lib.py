@@ -69,6 +69,7 @@ class RfrStats(ctypes.Structure):
         ("bytes_lists", ctypes.c_int64),
         ("bytes_join", ctypes.c_int64),
         ("us_hit_to_stop", ctypes.c_double),
+        ("pieces", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

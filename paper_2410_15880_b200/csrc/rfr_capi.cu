@@ -84,6 +84,7 @@ struct Ctx {
   DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec pctr, praw, ppost;  // the two pieces' counters / raw hits / survivors (concurrent)
+  DevVec pdesc, pver;        // device piece plan; the pieces' verification rows
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
   void* h_stage = nullptr;       // pinned staging of rfr_verify (in, then out)
@@ -472,6 +473,54 @@ constexpr int kPieceMaxN = 48;   // whole-space searches above this size stop ea
 constexpr int kPieceRows = 64;
 constexpr unsigned long long kPieceRaw = 1ull << 16;  // raw hits per small piece (concurrent path)
 
+// Pinned piece area: per piece [keys | keys2][64], its counters and
+// kPieceRows result rows; then both pieces' keys (one H2D) and the device
+// plan's PieceDesc.
+size_t piece_per(int stride) {
+  return 2 * 64 * 8 + sizeof(DevCounters) + kPieceRows * (10 + (size_t)stride * 8);
+}
+int ensure_piece_host(int stride) {
+  const size_t hbytes = 2 * piece_per(stride) + 2 * 2 * 64 * sizeof(uint64_t) + sizeof(PieceDesc);
+  if (g.h_piece_bytes >= hbytes) return RFR_OK;
+  if (g.h_piece) cudaFreeHost(g.h_piece);
+  g.h_piece = nullptr;
+  g.h_piece_bytes = 0;
+  int rc = rfr_check_cuda(cudaMallocHost(&g.h_piece, hbytes), "cudaMallocHost");
+  if (rc == RFR_OK) g.h_piece_bytes = hbytes;
+  return rc;
+}
+PieceDesc* piece_h_desc(int stride) {
+  return (PieceDesc*)((char*)g.h_piece + 2 * piece_per(stride) + 2 * 2 * 64 * sizeof(uint64_t));
+}
+// The collected rows of the pieces with >= 2 entities; false on an overflow
+// (more raw hits than raw_cap or more survivors than kPieceRows).
+bool read_piece_rows(int stride, const int ns[2], unsigned long long raw_cap, std::vector<uint64_t>& xp,
+                     std::vector<uint8_t>& xv, std::vector<uint8_t>& xs, std::vector<int64_t>& xc,
+                     int64_t* buckets) {
+  const size_t per = piece_per(stride);
+  for (int pi = 0; pi < 2; pi++) {
+    if (ns[pi] < 2) continue;
+    const char* hp = (const char*)g.h_piece + pi * per;
+    const DevCounters c = *(const DevCounters*)(hp + 2 * 64 * 8);
+    if (c.out_count > raw_cap || c.post_count > (unsigned long long)kPieceRows) return false;
+  }
+  for (int pi = 0; pi < 2; pi++) {
+    if (ns[pi] < 2) continue;
+    const char* hp = (const char*)g.h_piece + pi * per;
+    const DevCounters c = *(const DevCounters*)(hp + 2 * 64 * 8);
+    const char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+    for (unsigned long long k = 0; k < c.post_count; k++) {
+      xp.push_back(((const uint64_t*)rows)[k]);
+      xv.push_back(((const uint8_t*)(rows + kPieceRows * 8))[k]);
+      xs.push_back(((const uint8_t*)(rows + kPieceRows * 9))[k]);
+      const int64_t* cr = (const int64_t*)(rows + kPieceRows * 10) + k * stride;
+      xc.insert(xc.end(), cr, cr + stride);
+    }
+    *buckets += (int64_t)c.buckets;
+  }
+  return true;
+}
+
 // search_pieces for two small pieces: the table kernel, the Tr3 window, the
 // deposit into parent patterns, the verification and the collection of each
 // piece on its own stream (g.stream and g.stream2), with its own counters,
@@ -562,22 +611,7 @@ bool search_small_pieces(const uint64_t* keys, const uint64_t* keys2, uint64_t l
   if (!ok(cudaEventRecord(g.ev_join, g.stream2), "join") || !ok(cudaStreamWaitEvent(s, g.ev_join, 0), "join wait") ||
       !ok(cudaStreamSynchronize(s), "piece sync"))
     return false;
-  for (int pi = 0; pi < 2; pi++) {
-    if (ns[pi] < 2) continue;
-    const char* hp = (const char*)g.h_piece + pi * per;
-    const DevCounters c = *(const DevCounters*)(hp + 2 * 64 * 8);
-    if (c.out_count > kPieceRaw || c.post_count > (unsigned long long)kPieceRows) return false;
-    const char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
-    for (unsigned long long k = 0; k < c.post_count; k++) {
-      xp.push_back(((const uint64_t*)rows)[k]);
-      xv.push_back(((const uint8_t*)(rows + kPieceRows * 8))[k]);
-      xs.push_back(((const uint8_t*)(rows + kPieceRows * 9))[k]);
-      const int64_t* cr = (const int64_t*)(rows + kPieceRows * 10) + k * stride;
-      xc.insert(xc.end(), cr, cr + stride);
-    }
-    *buckets += (int64_t)c.buckets;
-  }
-  return true;
+  return read_piece_rows(stride, ns, kPieceRaw, xp, xv, xs, xc, buckets);
 }
 bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t lo, uint64_t width,
                    uint64_t lo2, uint64_t width2, uint64_t t, const VerifyArgs& V0, int stride,
@@ -588,16 +622,8 @@ bool search_pieces(const uint64_t* keys, const uint64_t* keys2, int n, uint64_t 
   const uint64_t masks[2] = {t & full, ~t & full};
   for (uint64_t M : masks)
     if (__builtin_popcountll(M) >= kPieceMaxN) return false;
-  const size_t row_b = 8 + 1 + 1 + (size_t)stride * 8;
-  const size_t per = 2 * 64 * 8 + sizeof(DevCounters) + kPieceRows * row_b;
-  const size_t hbytes = 2 * per + 2 * 2 * 64 * sizeof(uint64_t);  // + both pieces' keys in one block
-  if (g.h_piece_bytes < hbytes) {
-    if (g.h_piece) cudaFreeHost(g.h_piece);
-    g.h_piece = nullptr;
-    g.h_piece_bytes = 0;
-    if ((*rc = rfr_check_cuda(cudaMallocHost(&g.h_piece, hbytes), "cudaMallocHost"))) return false;
-    g.h_piece_bytes = hbytes;
-  }
+  const size_t per = piece_per(stride);
+  if ((*rc = ensure_piece_host(stride))) return false;
   if ((*rc = rfr_check_cuda(g.pkeys.ensure(2 * 2 * 64 * sizeof(uint64_t)), "pkeys"))) return false;
   // both pieces small (the table kernel): searched concurrently, one on each
   // stream, each with its own counters and buffers, one synchronisation
@@ -699,7 +725,7 @@ static void release_ctx() {
   if (g.stream) cudaStreamSynchronize(g.stream);
   DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts, &g.pkeys,
                     &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef, &g.pctr, &g.praw,
-                    &g.ppost};
+                    &g.ppost, &g.pdesc, &g.pver};
   for (DevVec* v : vecs) v->release();
   for (auto& h : g.hist) h.release();
   for (auto& a : g.lk)
@@ -1074,6 +1100,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
                           k * (size_t)stride * 8, cudaMemcpyDeviceToHost, s);
     return e;
   };
+  bool dev_pieces = false;
   for (int attempt = 0;; attempt++) {
     const unsigned long long raw_cap = g.raw.bytes / sizeof(uint64_t);
     RFR_CUDA_OK(g.post.ensure(raw_cap * sizeof(uint64_t)));
@@ -1161,6 +1188,69 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       C.h_coeffs = (long long*)(hs + h_coef);
       RFR_CUDA_OK(launch_collect(C, s));
     }
+    // an early stop's two pieces, searched on the device right behind (every
+    // piece kernel is a no-op unless the search stopped at a PASS whose
+    // pieces are small); RFR_HOST_PIECES=1 (A/B): the host-driven path only
+    dev_pieces = false;
+    if (early_exit == 1 && early && !getenv("RFR_HOST_PIECES")) {
+      const size_t pv_side = al(2 * kPieceRows), pv_coef = 2 * pv_side;
+      RFR_CUDA_OK(g.pctr.ensure(2 * sizeof(DevCounters)));
+      RFR_CUDA_OK(g.praw.ensure(2 * kPieceRaw * sizeof(uint64_t)));
+      RFR_CUDA_OK(g.ppost.ensure(2 * kPieceRaw * sizeof(uint64_t)));
+      RFR_CUDA_OK(g.pkeys.ensure(2 * 2 * 64 * sizeof(uint64_t)));
+      RFR_CUDA_OK(g.pdesc.ensure(sizeof(PieceDesc)));
+      RFR_CUDA_OK(g.pver.ensure(pv_coef + 2 * kPieceRows * (size_t)stride * sizeof(int64_t)));
+      if ((rc = ensure_piece_host(stride))) return rc;
+      PiecePlanArgs pa;
+      pa.ctr = d_ctr;
+      pa.planned = (unsigned long long)g_buckets_planned;
+      pa.raw_cap = raw_cap;
+      pa.rows_cap = (unsigned long long)cap;
+      pa.pats = (const uint64_t*)g.post.p;
+      pa.verdict = (const uint8_t*)obase;
+      pa.side = (const uint8_t*)(obase + q_side);
+      pa.n = n;
+      pa.keys = d_keys;
+      pa.keys2 = d_keys2;
+      pa.desc = (PieceDesc*)g.pdesc.p;
+      pa.h_desc = piece_h_desc(stride);
+      pa.pkeys = (uint64_t*)g.pkeys.p;
+      pa.pctr = (DevCounters*)g.pctr.p;
+      VerifyArgs PV[2];
+      CollectArgs PC[2];
+      const size_t per = piece_per(stride);
+      char* pvb = (char*)g.pver.p;
+      for (int pi = 0; pi < 2; pi++) {
+        DevCounters* ctr = (DevCounters*)g.pctr.p + pi;
+        uint64_t* post = (uint64_t*)g.ppost.p + pi * kPieceRaw;
+        PV[pi] = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
+        PV[pi].pats = post;
+        PV[pi].m = kPieceRows;
+        PV[pi].m_dev = &ctr->post_count;
+        PV[pi].found = nullptr;
+        PV[pi].verdict = (uint8_t*)pvb + pi * kPieceRows;
+        PV[pi].side = (uint8_t*)(pvb + pv_side) + pi * kPieceRows;
+        PV[pi].coeffs = (long long*)(pvb + pv_coef) + (size_t)pi * kPieceRows * stride;
+        PV[pi].stride = stride;
+        char* hp = (char*)g.h_piece + pi * per;
+        char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
+        PC[pi].ctr = ctr;
+        PC[pi].pats = post;
+        PC[pi].verdict = PV[pi].verdict;
+        PC[pi].side = PV[pi].side;
+        PC[pi].coeffs = PV[pi].coeffs;
+        PC[pi].stride = stride;
+        PC[pi].rows = kPieceRows;
+        PC[pi].h_ctr = (DevCounters*)(hp + 2 * 64 * 8);
+        PC[pi].h_pats = (uint64_t*)rows;
+        PC[pi].h_verdict = (uint8_t*)(rows + kPieceRows * 8);
+        PC[pi].h_side = (uint8_t*)(rows + kPieceRows * 9);
+        PC[pi].h_coeffs = (long long*)(rows + kPieceRows * 10);
+      }
+      RFR_CUDA_OK(launch_pieces(pa, lo, width, lo2, width2, (uint64_t*)g.praw.p, kPieceRaw,
+                                (uint64_t*)g.ppost.p, kPieceRaw, PV, PC, g.nsm, s));
+      dev_pieces = true;
+    }
     g_tr.mark("post enqueued, sync");
     RFR_CUDA_OK(cudaStreamSynchronize(s));
     g_tr.mark("synced");
@@ -1188,6 +1278,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
   int64_t xbuckets = 0;
   bool complete = cc.buckets >= (unsigned long long)main_planned;
   const bool stopped = !complete;
+  int pieces_how = 0;
   if (early_exit == 1 && !complete && m == cc.post_count) {
     const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
     for (size_t k = 0; k < m; k++) {
@@ -1200,12 +1291,23 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       V0.side = (uint8_t*)(obase + q_side);
       V0.coeffs = (long long*)(obase + q_coef);
       V0.stride = stride;
+      const PieceDesc* D = dev_pieces ? piece_h_desc(stride) : nullptr;
+      if (D && D->active && D->t == t) {  // searched on the device behind the main search
+        const int ns[2] = {D->ns[0], D->ns[1]};
+        if (read_piece_rows(stride, ns, kPieceRaw, xp, xv, xs, xc, &xbuckets)) {
+          complete = true;
+          pieces_how = 2;
+        }
+        break;
+      }
       int prc = RFR_OK;
       if (search_pieces(keys, keys2, n, lo, width, lo2, width2, t, V0, stride, s, xp, xv, xs, xc,
-                        &xbuckets, &prc))
+                        &xbuckets, &prc)) {
         complete = true;
-      else if (prc)
+        pieces_how = 1;
+      } else if (prc) {
         return prc;
+      }
       break;
     }
   }
@@ -1238,6 +1340,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
     st->buckets += xbuckets;
     if (complete) st->buckets_planned = st->buckets;
     st->early_stop = stopped ? 1 : 0;
+    st->pieces = pieces_how;
     st->us_hit_to_stop = (stopped && cc.t_found && cc.t_stop >= cc.t_found)
                              ? (double)(cc.t_stop - cc.t_found) * 1e-3
                              : -1.0;

@@ -51,6 +51,35 @@ struct CollectArgs {
   long long* h_coeffs;
 };
 cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s);
+// The pieces of an early stop searched on the device behind the main search
+// (launch_pieces, rfr_search.cu).
+struct PieceDesc {
+  unsigned long long t;        // the factor's pattern (parent bits)
+  unsigned long long mask[2];  // piece 0 = t, piece 1 = its complement
+  int ns[2];                   // entities per piece
+  int active;                  // 0: no piece search (every piece kernel returns)
+  int pad;
+};
+struct PiecePlanArgs {
+  const DevCounters* ctr;       // the main search's counters
+  unsigned long long planned;   // its planned buckets (fewer searched = stopped)
+  unsigned long long raw_cap;   // its raw-hit capacity (an overflow is no stop)
+  unsigned long long rows_cap;  // rows the caller takes (more: the host decides)
+  const uint64_t* pats;         // its verified rows
+  const uint8_t* verdict;
+  const uint8_t* side;
+  int n;
+  const uint64_t* keys;  // the search's keys and Tr3 keys (n each)
+  const uint64_t* keys2;
+  PieceDesc* desc;    // device copy (read by the piece kernels)
+  PieceDesc* h_desc;  // pinned host copy (checked by the host)
+  uint64_t* pkeys;    // [piece][keys | keys2][64]
+  DevCounters* pctr;  // [2], cleared by the plan
+};
+cudaError_t launch_pieces(const PiecePlanArgs& a, uint64_t lo, uint64_t width, uint64_t lo2, uint64_t width2,
+                          uint64_t* praw, unsigned long long raw_cap, uint64_t* ppost,
+                          unsigned long long post_cap, const struct VerifyArgs* V, const CollectArgs* C,
+                          int nsm, cudaStream_t s);
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,

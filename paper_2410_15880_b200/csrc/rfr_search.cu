@@ -62,6 +62,8 @@ __device__ __forceinline__ ListSpec pick_list(const JoinPlan& P, int i) {
 struct BaseSmem {
   uint64_t k[2][1 << kBaseBits];
   uint32_t p[2][1 << kBaseBits];
+  uint64_t v[kBaseBits + 1];  // the level keys, loaded once (not one global load per level)
+  uint32_t cnt[3];            // # entries of level i below -v_i, accumulated by level i - 1
 };
 
 // # of entries of the ascending rotated sequence s[(r + j) mod n] + v, j < n,
@@ -91,35 +93,35 @@ __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __rest
     S.k[0][0] = 0;
     S.p[0][0] = 0;
   }
+  if (tid <= b && tid < L.bits) S.v[tid] = elem_key(keys, L, tid);
+  if (tid < 3) S.cnt[tid] = 0;
+  __syncthreads();
+  if (tid == 0) S.cnt[0] = S.v[0] != 0 ? 1u : 0u;  // level 0 = {0}: 0 < -v_0 iff v_0 != 0
   __syncthreads();
   int cur = 0;
   for (int i = 0; i < b; i++) {
     const uint32_t n = 1u << i;
-    const uint64_t v = elem_key(keys, L, i);
+    const uint64_t v = S.v[i];
     const uint64_t* A = S.k[cur];
-    // rotation start: # of A < -v (0 when v == 0 or when every A is < -v)
-    uint32_t r = 0;
-    if (v != 0) {
-      uint32_t lo = 0, hi = n;
-      const uint64_t t = 0ull - v;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (A[mid] < t) lo = mid + 1;
-        else hi = mid;
-      }
-      r = lo == n ? 0 : lo;
-    }
+    // rotation start: # of A < -v (0 when v == 0 or when every A is < -v),
+    // counted by the previous level as it placed its outputs
+    uint32_t r = S.cnt[i % 3];
+    if (r >= n) r = 0;
+    if (tid == 0) S.cnt[(i + 2) % 3] = 0;  // read at level i - 1, summed at level i + 1
+    const uint64_t thr = i + 1 < b ? 0ull - S.v[i + 1] : 0ull;  // next level's threshold
+    uint32_t below = 0;
     uint64_t* Ok = S.k[cur ^ 1];
     uint32_t* Op = S.p[cur ^ 1];
     for (uint32_t e = tid; e < 2 * n; e += blockDim.x) {
+      uint64_t x;
       if (e < n) {  // A[e]: after e A's and the B's strictly below it
-        const uint64_t x = A[e];
+        x = A[e];
         const uint32_t d = e + rank_rot(A, n, r, v, x, true);
         Ok[d] = x;
         Op[d] = S.p[cur][e];
       } else {  // B'[j] = A[(r + j) mod n] + v: after j B's and the A's <= it
         const uint32_t j = e - n, src = (r + j) & (n - 1);
-        const uint64_t x = A[src] + v;
+        x = A[src] + v;
         uint32_t lo = 0, hi = n;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
@@ -129,7 +131,10 @@ __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __rest
         Ok[j + lo] = x;
         Op[j + lo] = S.p[cur][src] | (1u << i);
       }
+      below += x < thr ? 1u : 0u;
     }
+    below = __reduce_add_sync(0xffffffffu, below);
+    if ((tid & 31) == 0 && below) atomicAdd(&S.cnt[(i + 1) % 3], below);
     __syncthreads();
     cur ^= 1;
   }
@@ -145,7 +150,7 @@ __global__ void __launch_bounds__(1024) lists_base_kernel(const uint64_t* __rest
   for (int k = tid; k < kRotSlots; k += blockDim.x) rc[k] = 0;
   __syncthreads();
   if (L.bits > b) {
-    const uint64_t thr = 0ull - elem_key(keys, L, b);
+    const uint64_t thr = 0ull - S.v[b];
     uint32_t c = 0;
     for (int p = tid; p < len; p += blockDim.x) c += S.k[cur][p] < thr ? 1u : 0u;
     c = __reduce_add_sync(0xffffffffu, c);
@@ -502,6 +507,42 @@ __device__ __forceinline__ uint32_t warp_lower_bound(const uint64_t* __restrict_
   return lo + __popc(__ballot_sync(FULL, q < hi && __ldg(a + q) < v));
 }
 
+// Two lower bounds in the same sorted array, advanced in lockstep so their
+// dependent loads overlap (the starts kernel's searches miss L2: ~1 us each).
+__device__ __forceinline__ void warp_lower_bound2(const uint64_t* __restrict__ a, uint32_t n, uint64_t v0,
+                                                  uint64_t v1, int lane, uint32_t* r0, uint32_t* r1) {
+  const unsigned FULL = 0xffffffffu;
+  uint32_t lo[2] = {0, 0}, hi[2] = {n, n};
+  const uint64_t v[2] = {v0, v1};
+  while (hi[0] - lo[0] > 32 || hi[1] - lo[1] > 32) {
+    uint32_t q[2];
+    bool pr[2];
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      const uint32_t span = hi[s] - lo[s];
+      q[s] = span > 32 ? lo[s] + (uint32_t)(((uint64_t)span * (uint32_t)(lane + 1)) >> 5) - 1u : lo[s];
+      pr[s] = span > 32 && __ldg(a + q[s]) < v[s];
+    }
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      if (hi[s] - lo[s] <= 32) continue;  // warp-uniform
+      const uint32_t c = __popc(__ballot_sync(FULL, pr[s]));
+      const uint32_t qlo = __shfl_sync(FULL, q[s], (c ? c : 1u) - 1u);
+      const uint32_t qhi = __shfl_sync(FULL, q[s], c < 32u ? c : 31u);
+      if (c) lo[s] = qlo + 1u;
+      if (c < 32u) hi[s] = qhi;
+    }
+  }
+  bool pr[2];
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const uint32_t q = lo[s] + (uint32_t)lane;
+    pr[s] = q < hi[s] && __ldg(a + q) < v[s];
+  }
+  *r0 = lo[0] + __popc(__ballot_sync(FULL, pr[0]));
+  *r1 = lo[1] + __popc(__ballot_sync(FULL, pr[1]));
+}
+
 // Start state of every join launch of one key window, computed up front with
 // one warp per search (the join's CTAs would otherwise each run ~140
 // dependent binary-search loads before their first bucket, per launch).
@@ -546,8 +587,8 @@ __global__ void __launch_bounds__(256) join_starts_kernel(JoinPlan P, const uint
     const uint64_t bound = c_begin << (64 - P.r);
     if (bound != 0) {
       const uint64_t hi = l0 + bound;  // exclusive end, mod 2^64
-      const uint32_t l = warp_lower_bound(inner, n, l0, lane);
-      const uint32_t h = warp_lower_bound(inner, n, hi, lane);
+      uint32_t l, h;
+      warp_lower_bound2(inner, n, l0, hi, lane, &l, &h);
       pos = hi > l0 ? h - l : (n - l) + h;  // wraps through 2^64 when hi <= l0
     }
   }
@@ -1023,18 +1064,58 @@ cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64
 // patterns instead of one add and one compare per pattern (the Gray-code
 // exhaustive_kernel, kept as the independent checker of RFR_FORCE_EXHAUSTIVE).
 constexpr int kTableMaxBits = 12;
-__global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __restrict__ keys, int n,
-                                                           uint64_t lo, uint64_t width, int b, int g,
-                                                           uint64_t* __restrict__ out,
-                                                           unsigned long long cap, DevCounters* ctr) {
+__device__ __forceinline__ void table_search_body(const uint64_t* __restrict__ keys, int n, uint64_t lo,
+                                                  uint64_t width, int b, int g, uint64_t* __restrict__ out,
+                                                  unsigned long long cap, DevCounters* ctr, unsigned blk) {
   extern __shared__ __align__(16) unsigned char tsm[];
   uint64_t* tk = reinterpret_cast<uint64_t*>(tsm);                     // sorted low sums
   uint16_t* ti = reinterpret_cast<uint16_t*>(tsm + (8u << b));         // their low patterns
   __shared__ uint64_t sk[64];
   const int tid = threadIdx.x;
+  {  // a CTA past the 2^h high patterns has nothing to do (fixed-size grids)
+    const int h0 = n - 1 - b;
+    if (h0 >= 0 && blk != 0 && (((uint64_t)blk * blockDim.x) << g) >> h0) return;
+  }
   for (int i = tid; i < n; i += blockDim.x) sk[i] = keys[i];
   __syncthreads();
   const uint32_t nt = 1u << b;
+  if (nt == blockDim.x) {
+    // one entry per thread: bitonic sort in registers, the partner of the
+    // stages with j < 32 read by a warp shuffle, only the j >= 32 stages
+    // through shared memory (6 barriers for b = 8 instead of 36)
+    const uint32_t i = tid;
+    uint64_t x = 0;
+    for (uint32_t u = i; u; u &= u - 1) x += sk[__ffs(u) - 1];
+    uint32_t xi = i;
+    for (uint32_t kk = 2; kk <= nt; kk <<= 1) {
+      for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+        uint64_t y;
+        uint32_t yi;
+        if (jj >= 32) {
+          __syncthreads();
+          tk[i] = x;
+          ti[i] = (uint16_t)xi;
+          __syncthreads();
+          y = tk[i ^ jj];
+          yi = ti[i ^ jj];
+        } else {
+          y = __shfl_xor_sync(0xffffffffu, x, jj);
+          yi = __shfl_xor_sync(0xffffffffu, xi, jj);
+        }
+        // the lower index of an ascending pair keeps the minimum
+        const bool lower = (i & jj) == 0, up = (i & kk) == 0;
+        const bool take = lower == up ? (y < x) : (y > x);
+        if (take) {
+          x = y;
+          xi = yi;
+        }
+      }
+    }
+    __syncthreads();
+    tk[i] = x;
+    ti[i] = (uint16_t)xi;
+    __syncthreads();
+  } else {
   for (uint32_t i = tid; i < nt; i += blockDim.x) {
     uint64_t s = 0;
     for (uint32_t u = i; u; u &= u - 1) s += sk[__ffs(u) - 1];
@@ -1062,8 +1143,9 @@ __global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __res
       __syncthreads();
     }
   }
+  }
   const int m = n - 1, h = m - b;
-  const uint64_t T = (uint64_t)blockIdx.x * blockDim.x + tid;
+  const uint64_t T = (uint64_t)blk * blockDim.x + tid;
   if (T == 0) atomicAdd(&ctr->queries, 1ull << m);  // patterns tested (stats)
   if (h < 0 || (T << g) >> h) return;  // past 2^h high patterns
   const uint64_t i0 = T << g;
@@ -1093,6 +1175,17 @@ __global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __res
   }
 }
 
+__global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __restrict__ keys, int n,
+                                                           uint64_t lo, uint64_t width, int b, int g,
+                                                           uint64_t* __restrict__ out,
+                                                           unsigned long long cap, DevCounters* ctr) {
+  table_search_body(keys, n, lo, width, b, g, out, cap, ctr, blockIdx.x);
+}
+
+// table bits and threads of a small search of n entities (<= 2^16 threads,
+// 2^g high patterns each)
+__host__ __device__ inline int table_bits(int m) { return m <= 30 ? 8 : (m <= 33 ? 10 : kTableMaxBits); }
+
 cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width,
                                 uint64_t* d_out, unsigned long long cap, DevCounters* d_ctr,
                                 cudaStream_t s) {
@@ -1104,7 +1197,7 @@ cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint
     const char* e = getenv("RFR_TABLE_BITS");
     forced_b = e ? atoi(e) : 0;
   }
-  int b = forced_b > 0 ? forced_b : (m <= 30 ? 8 : (m <= 33 ? 10 : kTableMaxBits));
+  int b = forced_b > 0 ? forced_b : table_bits(m);
   if (b > m) b = m;
   if (b > kTableMaxBits) b = kTableMaxBits;
   const int h = m - b;
@@ -1159,6 +1252,152 @@ __global__ void collect_kernel(CollectArgs C) {
 }
 cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
   collect_kernel<<<1, 256, 0, s>>>(C);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------- pieces after an early stop
+// The two pieces of the verified factor searched right behind the main
+// search on the same stream, with no host round trip: piece_plan_kernel
+// takes the first PASS row (the pattern the host would pick), splits the
+// entities into t and its complement, compacts each piece's keys and clears
+// its counters; the table search, the Tr3 window + deposit, the verification
+// and the collection follow, each piece on its own grid row (blockIdx.y) or
+// launch.  Inactive (no stop, no PASS, a piece above kExhaustiveMaxN, more
+// rows than the caller takes) makes every later kernel a no-op; the host
+// compares the plan's t with its own before using the rows.
+__global__ void piece_plan_kernel(PiecePlanArgs a) {
+  __shared__ unsigned long long s_t;
+  __shared__ int s_act;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (int)(2 * sizeof(DevCounters) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(a.pctr)[i] = 0ull;
+  if (tid == 0) {
+    const DevCounters& c = *a.ctr;
+    const uint64_t full = a.n >= 64 ? ~0ull : ((1ull << a.n) - 1ull);
+    int act = 0;
+    unsigned long long t = 0;
+    if (c.buckets < a.planned && c.out_count <= a.raw_cap && c.post_count <= a.rows_cap) {
+      for (unsigned long long k = 0; k < c.post_count; k++) {
+        if (a.verdict[k] != RFR_V_PASS) continue;
+        const uint64_t sp = a.pats[k] & full;
+        t = a.side[k] ? (~sp & full) : sp;
+        act = __popcll(t) <= kExhaustiveMaxN && __popcll(~t & full) <= kExhaustiveMaxN;
+        break;
+      }
+    }
+    s_t = t;
+    s_act = act;
+    PieceDesc d;
+    d.t = t;
+    d.mask[0] = t;
+    d.mask[1] = ~t & full;
+    d.ns[0] = __popcll(d.mask[0]);
+    d.ns[1] = __popcll(d.mask[1]);
+    d.active = act;
+    d.pad = 0;
+    *a.desc = d;
+    *a.h_desc = d;
+  }
+  __syncthreads();
+  if (!s_act) return;
+  const uint64_t full = a.n >= 64 ? ~0ull : ((1ull << a.n) - 1ull);
+  const uint64_t t = s_t;
+  for (int i = tid; i < a.n; i += blockDim.x) {  // compact: [piece][keys | keys2][64]
+    const int pi = (t >> i) & 1ull ? 0 : 1;
+    const uint64_t mk = pi ? (~t & full) : t;
+    const int j = __popcll(mk & ((1ull << i) - 1ull));
+    a.pkeys[pi * 128 + j] = a.keys[i];
+    a.pkeys[pi * 128 + 64 + j] = a.keys2[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) piece_search_kernel(const PieceDesc* __restrict__ desc,
+                                                           const uint64_t* __restrict__ pkeys, uint64_t lo,
+                                                           uint64_t width, uint64_t* __restrict__ praw,
+                                                           unsigned long long cap, DevCounters* pctr) {
+  const int pi = blockIdx.y;
+  if (!desc->active) return;
+  const int n = desc->ns[pi];
+  if (n < 2) return;  // one linear or quadratic entity: irreducible
+  const int m = n - 1;
+  int b = table_bits(m);
+  if (b > m) b = m;
+  const int h = m - b;
+  const int g = h > 16 ? h - 16 : 0;
+  table_search_body(pkeys + pi * 128, n, lo, width, b, g, praw + (size_t)pi * cap, cap, pctr + pi,
+                    blockIdx.x);
+}
+
+// Tr3 window over a piece's raw hits, then each survivor deposited into the
+// parent's pattern bits (keyfilter_kernel + deposit_kernel for both pieces)
+__global__ void piece_filter_kernel(const PieceDesc* __restrict__ desc, const uint64_t* __restrict__ pkeys,
+                                    const uint64_t* __restrict__ praw, unsigned long long raw_cap,
+                                    uint64_t lo2, uint64_t width2, uint64_t* __restrict__ ppost,
+                                    unsigned long long post_cap, DevCounters* pctr) {
+  const int pi = blockIdx.y;
+  if (!desc->active || desc->ns[pi] < 2) return;
+  __shared__ uint64_t sk[64];
+  const int n = desc->ns[pi];
+  const uint64_t mask = desc->mask[pi];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = pkeys[pi * 128 + 64 + i];
+  __syncthreads();
+  DevCounters* ctr = pctr + pi;
+  unsigned long long m = ctr->out_count;
+  if (m > raw_cap) m = raw_cap;
+  const uint64_t* in = praw + (size_t)pi * raw_cap;
+  uint64_t* out = ppost + (size_t)pi * post_cap;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t t = in[i];
+    uint64_t sum = 0, v = 0, u = t, mm = mask;
+    for (int j = 0; u; j++, u >>= 1, mm &= mm - 1)
+      if (u & 1ull) {
+        sum += sk[j];
+        v |= mm & (0ull - mm);
+      }
+    if (sum - lo2 <= width2) {
+      const unsigned long long k = atomicAdd(&ctr->post_count, 1ull);
+      if (k < post_cap) out[k] = v;
+    }
+  }
+}
+
+__global__ void collect2_kernel(CollectArgs C0, CollectArgs C1) {
+  const CollectArgs& C = blockIdx.x ? C1 : C0;
+  const unsigned long long cnt = C.ctr->post_count;
+  const unsigned rows = (unsigned)(cnt < C.rows ? cnt : C.rows);
+  const int t = threadIdx.x;
+  if (t < (int)(sizeof(DevCounters) / 8))
+    ((unsigned long long*)C.h_ctr)[t] = ((const unsigned long long*)C.ctr)[t];
+  for (unsigned k = t; k < rows; k += blockDim.x) {
+    C.h_pats[k] = C.pats[k];
+    C.h_verdict[k] = C.verdict[k];
+    C.h_side[k] = C.side[k];
+  }
+  const unsigned nco = rows * (unsigned)C.stride;
+  for (unsigned k = t; k < nco; k += blockDim.x) C.h_coeffs[k] = C.coeffs[k];
+}
+
+cudaError_t launch_pieces(const PiecePlanArgs& a, uint64_t lo, uint64_t width, uint64_t lo2, uint64_t width2,
+                          uint64_t* praw, unsigned long long raw_cap, uint64_t* ppost,
+                          unsigned long long post_cap, const struct VerifyArgs* V, const CollectArgs* C,
+                          int nsm, cudaStream_t s) {
+  piece_plan_kernel<<<1, 64, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  static uint64_t attr_done = 0;
+  e = raise_smem_limit(piece_search_kernel, (size_t)10 << kTableMaxBits, attr_done);
+  if (e != cudaSuccess) return e;
+  // <= 2^16 threads per piece (n <= kExhaustiveMaxN: b = 8, h <= 22, g = h - 16)
+  piece_search_kernel<<<dim3(256, 2), 256, (size_t)10 << 8, s>>>(a.desc, a.pkeys, lo, width, praw, raw_cap,
+                                                                  a.pctr);
+  piece_filter_kernel<<<dim3(nsm, 2), 256, 0, s>>>(a.desc, a.pkeys, praw, raw_cap, lo2, width2, ppost,
+                                                     post_cap, a.pctr);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  for (int pi = 0; pi < 2; pi++)
+    if ((e = launch_verify(V[pi], s)) != cudaSuccess) return e;
+  collect2_kernel<<<2, 256, 0, s>>>(C[0], C[1]);
   return cudaGetLastError();
 }
 

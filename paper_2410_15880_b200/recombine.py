@@ -96,6 +96,9 @@ class RecombineStats:
     # early exit: microseconds from the verified hit to the join's stop (the
     # last search that stopped; -1 when none did)
     hit_to_stop_us: float = -1.0
+    # early stops whose two pieces were searched by kernels chained on the
+    # device behind the main search (rfr_stats.pieces == 2)
+    device_pieces: int = 0
 
     @property
     def probes_mean(self) -> float:
@@ -143,6 +146,7 @@ def _fill_stats(stats: RecombineStats | None, st: "_lib.RfrStats") -> None:
     stats.device_ms += float(st.ms_total)
     if st.us_hit_to_stop >= 0:
         stats.hit_to_stop_us = float(st.us_hit_to_stop)
+    stats.device_pieces += int(st.pieces == 2)
 
 
 def recombine_e(rho: RhoVector, eps: float, stats: RecombineStats | None = None,

@@ -234,6 +234,42 @@ def test_factor_with_early_exit_matches_the_reference(big_inputs):
     assert res.irreducible and res.stats.early_exits == 0
 
 
+def test_device_chained_pieces_match_host_driven_pieces(big_inputs, monkeypatch):
+    """After an early stop the two pieces are searched by kernels chained on
+    the device behind the main search (rfr_stats.pieces == 2); the host-driven
+    piece searches (RFR_HOST_PIECES=1) give the same rows: same factors and
+    the same candidate counts on the d = 100 inputs and on products of
+    several factors (where the stop may land on a union of factors)."""
+    import sympy
+
+    x = sympy.symbols("x")
+    polys = [poly_of(c["p"]) for c in big_inputs["c3"]]
+    rng = random.Random(41)
+    for k, deg in ((3, 32), (4, 24)):
+        fs = []
+        while len(fs) < k:
+            co = [rng.randint(-20, 20) for _ in range(deg)] + [1]
+            f = sympy.Poly(list(reversed(co)), x)
+            if f.is_irreducible:
+                fs.append(f)
+        prod = fs[0]
+        for f in fs[1:]:
+            prod = prod * f
+        polys.append(P([int(c) for c in reversed(prod.all_coeffs())]))
+    device = 0
+    for p in polys:
+        monkeypatch.delenv("RFR_HOST_PIECES", raising=False)
+        a = factor(p)
+        monkeypatch.setenv("RFR_HOST_PIECES", "1")
+        b = factor(p)
+        assert _got(a) == _got(b) and a.certificate and b.certificate
+        assert a.stats.candidates == b.stats.candidates
+        assert b.stats.recombine.device_pieces == 0
+        device += a.stats.recombine.device_pieces
+    monkeypatch.delenv("RFR_HOST_PIECES", raising=False)
+    assert device >= 4
+
+
 def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
     """If the exact check rejects every verified factor of a stopped search
     (a false device PASS), factor() searches the whole pattern space and
