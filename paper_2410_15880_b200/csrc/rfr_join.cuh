@@ -553,6 +553,10 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // outer whose last chunk is still full is flagged for continue_pass
 // (off = 32 * nch).  Same record semantics as window_pass.
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
+// chunk counts of the default plan's runs (lambda = 256 A records and 128 B
+// records per outer per bucket: ceil((lambda + 3 sqrt(lambda) + 8) / 32)),
+// compiled as their own run_pass instances
+constexpr int kNchA = 10, kNchB = 6;
 // SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
 // so "in bucket" and "in halo" are 32-bit tests on the high / low words.
 // 32-bit bucket/halo classification in the run pass (SMALLH): the halo fits
@@ -563,9 +567,16 @@ __device__ __forceinline__ bool use_smallh(const JoinPlan& P) {
          (32u * kMaxCh >> P.list[3].bits) == 0u;
 }
 
-template <bool SIDE_A, bool SMALLH>
+// NCH > 0: the chunk count fixed at compile time (the production plans' run
+// lengths), so the chunk loads need no per-chunk predicate and the chunks
+// past the run cost no code; 0: nch at run time (any plan), <= kMaxCh.
+// NOOVF (side A): the caller checked that the warp's runs cannot overflow its
+// partition (wfill + outers * 32 * NCH <= kPart), so no per-chunk check.
+template <bool SIDE_A, bool SMALLH, int NCH = 0, bool NOOVF = false>
 __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t lo, uint32_t hi,
                                       int nch, PassSt st) {
+  constexpr int KM = NCH ? NCH : kMaxCh;
+  if (NCH) nch = NCH;
   JoinSmem& S = join_smem();
   uint32_t wfill = st.wfill, n_stat = st.n_stat, n_qprobe = st.n_qprobe;
   bool overflow = st.overflow, cont = false;
@@ -588,11 +599,12 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     const uint32_t rot = (SIDE_A ? S.arot : S.brot)[i];
     const uint64_t x = (SIDE_A ? S.ax : S.bx)[i];
     if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64();
-    uint64_t kv[kMaxCh];
+    uint64_t kv[KM];
 #pragma unroll
-    for (int k = 0; k < kMaxCh; k++) {
+    for (int k = 0; k < KM; k++) {
       const uint32_t q = (uint32_t)(k * 32 + lane);
-      kv[k] = (k < nch && q < Mi) ? ld_stream(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
+      // SMALLH: every chunk lane is a list entry (Mi >= 32 kMaxCh)
+      kv[k] = ((NCH || k < nch) && (SMALLH || q < Mi)) ? ld_stream(kin + ((rot + pos + q) & (Mi - 1))) : 0ull;
     }
     if (RFR_JOIN_TRACE && tr && trn < 60) tr[trn++] = clock64() | (1ull << 63);
     // along a run the offset rel = x + key - cW grows with q (one pass over the
@@ -604,8 +616,8 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     const uint32_t lim = Mi - pos;  // o < Mi  <=>  q < lim  (pos <= Mi)
     uint32_t mcl = 0, nq = 0, em = 0;
 #pragma unroll
-    for (int k = 0; k < kMaxCh; k++) {
-      if (k < nch) {
+    for (int k = 0; k < KM; k++) {
+      if (NCH || k < nch) {
         const uint32_t q = (uint32_t)(k * 32 + lane);
         const uint32_t j = (rot + pos + q) & (Mi - 1);
         const uint64_t sv = x + kv[k];
@@ -629,8 +641,8 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
           // chunk entirely past the run (warp-uniform): nothing to store or probe
         } else if (SIDE_A) {
           const uint32_t ne = __popc(em);
-          if (wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
-          if (!overflow && e) {
+          if (!NOOVF && wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
+          if ((NOOVF || !overflow) && e) {
             const uint32_t r = wid * kPart + wfill + lane;  // em is a prefix
             S.recK[r] = sv;
             S.recI[r] = (i << aib) | j;
@@ -638,7 +650,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
             S.t1[h1] = (uint16_t)r;
             S.rh[r] = (uint16_t)h1;
           }
-          if (!overflow) wfill += ne;
+          if (NOOVF || !overflow) wfill += ne;
         } else {
           const int deep = probe_b_l1_fast(S, a, K, e, sv, !m, i, j, n_qprobe);
           const uint32_t dm = __ballot_sync(FULL, deep != 0);
@@ -974,8 +986,15 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
     {
       const int t = tid_now(), w = t >> 5;
       PassSt sa{0u, join_smem().cnt[0][t], join_smem().cnt[2][t], false, false};
-      sa = gsA > 32 ? (smallh ? run_pass<true, true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa) : run_pass<true, false>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA >> 5, sa))
-                    : window_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
+      const uint32_t wlo = join_smem().wlo[0][w], whi = join_smem().whi[0][w];
+      if (gsA > 32 && smallh && (gsA >> 5) == kNchA) {
+        sa = (whi - wlo) * 32u * kNchA <= (uint32_t)kPart
+                 ? run_pass<true, true, kNchA, true>(a, cW, wlo, whi, gsA >> 5, sa)
+                 : run_pass<true, true, kNchA>(a, cW, wlo, whi, gsA >> 5, sa);
+      } else {
+        sa = gsA > 32 ? (smallh ? run_pass<true, true>(a, cW, wlo, whi, gsA >> 5, sa) : run_pass<true, false>(a, cW, wlo, whi, gsA >> 5, sa))
+                        : window_pass<true>(a, cW, wlo, whi, gsA, sa);
+      }
       if (sa.cont) {
         __syncwarp();
         sa = continue_pass<true>(a, cW, join_smem().wlo[0][w], join_smem().whi[0][w], gsA, sa);
@@ -999,7 +1018,7 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       {
         const int t = tid_now(), w = t >> 5;
         PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
-        sb = gsB > 32 ? (smallh ? run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
+        sb = gsB > 32 ? (smallh ? ((gsB >> 5) == kNchB ? run_pass<false, true, kNchB>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb)) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
                       : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
