@@ -553,9 +553,10 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // outer whose last chunk is still full is flagged for continue_pass
 // (off = 32 * nch).  Same record semantics as window_pass.
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
-// chunk counts of the default plan's runs (lambda = 256 A records and 128 B
-// records per outer per bucket: ceil((lambda + 3 sqrt(lambda) + 8) / 32)),
-// compiled as their own run_pass instances
+// chunk counts of the default plan's runs (lambda = 256 records per outer
+// per bucket on side A, 128 or 256 on side B for even or odd n:
+// ceil((lambda + 3 sqrt(lambda) + 8) / 32)), compiled as their own run_pass
+// instances
 constexpr int kNchA = 10, kNchB = 6;
 // SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
 // so "in bucket" and "in halo" are 32-bit tests on the high / low words.
@@ -991,6 +992,10 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
         sa = (whi - wlo) * 32u * kNchA <= (uint32_t)kPart
                  ? run_pass<true, true, kNchA, true>(a, cW, wlo, whi, gsA >> 5, sa)
                  : run_pass<true, true, kNchA>(a, cW, wlo, whi, gsA >> 5, sa);
+      } else if (gsA > 32 && smallh && (gsA >> 5) == kNchB) {  // lambda = 128 (sharded plans)
+        sa = (whi - wlo) * 32u * kNchB <= (uint32_t)kPart
+                 ? run_pass<true, true, kNchB, true>(a, cW, wlo, whi, gsA >> 5, sa)
+                 : run_pass<true, true, kNchB>(a, cW, wlo, whi, gsA >> 5, sa);
       } else {
         sa = gsA > 32 ? (smallh ? run_pass<true, true>(a, cW, wlo, whi, gsA >> 5, sa) : run_pass<true, false>(a, cW, wlo, whi, gsA >> 5, sa))
                         : window_pass<true>(a, cW, wlo, whi, gsA, sa);
@@ -1018,7 +1023,11 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       {
         const int t = tid_now(), w = t >> 5;
         PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
-        sb = gsB > 32 ? (smallh ? ((gsB >> 5) == kNchB ? run_pass<false, true, kNchB>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb) : run_pass<false, true>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb)) : run_pass<false, false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB >> 5, sb))
+        const uint32_t blo = join_smem().wlo[1][w], bhi = join_smem().whi[1][w];
+        sb = gsB > 32 ? (smallh ? ((gsB >> 5) == kNchB   ? run_pass<false, true, kNchB>(a, cW, blo, bhi, gsB >> 5, sb)
+                                   : (gsB >> 5) == kNchA ? run_pass<false, true, kNchA>(a, cW, blo, bhi, gsB >> 5, sb)
+                                                         : run_pass<false, true>(a, cW, blo, bhi, gsB >> 5, sb))
+                                : run_pass<false, false>(a, cW, blo, bhi, gsB >> 5, sb))
                       : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
