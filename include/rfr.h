@@ -261,6 +261,21 @@ int rfr_polish_roots(const double* coef_hi, const double* coef_lo, int d, double
  * coeffs_mod: p's coefficients reduced mod q (d+1), lead_mod != 0.
  */
 int rfr_squarefree_mod(const uint64_t* coeffs_mod, int d, uint64_t q);
+/*
+ * The same screen from signed 64-bit coefficients, reduced mod q inside
+ * (Python's sign rule): the factor() prologue calls this once per input, so
+ * the reduction is not a separate host pass.  -1 when some |c| >= 2^62.
+ */
+int rfr_squarefree_i64(const int64_t* coeffs, int d, uint64_t q);
+/*
+ * Exact division by a monic divisor (R/polynomial.py:155-183 for monic q,
+ * the only divisors factor() produces): r = p / q by long division in
+ * 128-bit integers; r must hold dp - dq + 1 entries.  1: q divides p (r
+ * filled), 0: it does not, -1: outside the native range (some |p_i| >=
+ * 2^62, |q_i| >= 2^31 or quotient coefficient >= 2^62: the caller takes its
+ * big-integer path).
+ */
+int rfr_divide_monic_i64(const int64_t* p, int dp, const int64_t* q, int dq, int64_t* r);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,8 @@ EXPORTS = (
     "rfr_verify_primes",
     "rfr_polish_roots",
     "rfr_squarefree_mod",
+    "rfr_squarefree_i64",
+    "rfr_divide_monic_i64",
 )
 
 
@@ -170,6 +172,10 @@ def load():
         L.rfr_verify_primes.argtypes = [U64_P]
         L.rfr_polish_roots.argtypes = [D_P, D_P, ctypes.c_int, D_P, D_P, D_P, D_P, D_P, ctypes.c_int]
         L.rfr_squarefree_mod.argtypes = [U64_P, ctypes.c_int, ctypes.c_uint64]
+        # raw address (int): the per-call pointer wrapping costs more than the screen
+        L.rfr_squarefree_i64.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64]
+        L.rfr_divide_monic_i64.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.c_void_p]
         _lib = L
         return L
 

@@ -339,6 +339,47 @@ static int squarefree_euclid_fp(const uint64_t* cm, int d, uint64_t q64) {
 }
 }  // extern "C++"
 
+int rfr_divide_monic_i64(const int64_t* p, int dp, const int64_t* q, int dq, int64_t* r) {
+  if (dq < 0 || dp < dq || q[dq] != 1) return -1;
+  const int64_t p_lim = (int64_t)1 << 62, q_lim = (int64_t)1 << 31;
+  for (int i = 0; i <= dp; i++)
+    if (p[i] >= p_lim || p[i] <= -p_lim) return -1;
+  for (int i = 0; i <= dq; i++)
+    if (q[i] >= q_lim || q[i] <= -q_lim) return -1;
+  // |rem| <= |p| + sum |t| |q| < 2^62 + (dq + 1) 2^62 2^31 < 2^127 for dq < 2^32
+  std::vector<__int128> rem(p, p + dp + 1);
+  const __int128 lim = (__int128)1 << 62;
+  for (int k = dp - dq; k >= 0; k--) {
+    const __int128 t = rem[k + dq];
+    if (t >= lim || t <= -lim) return -1;
+    r[k] = (int64_t)t;
+    if (t != 0)
+      for (int i = 0; i < dq; i++) rem[k + i] -= t * (__int128)q[i];
+  }
+  for (int i = 0; i < dq; i++)
+    if (rem[i] != 0) return 0;
+  return 1;
+}
+
+int rfr_squarefree_i64(const int64_t* c, int d, uint64_t q) {
+  if (d < 1 || q < 3 || q >= (1ull << 62)) return 0;
+  for (int k = 0; k <= d; k++)
+    if (c[k] >= ((int64_t)1 << 62) || c[k] <= -((int64_t)1 << 62)) return -1;
+  uint64_t buf[256];
+  std::vector<uint64_t> big;
+  uint64_t* cm = buf;
+  if (d + 1 > 256) {
+    big.resize((size_t)d + 1);
+    cm = big.data();
+  }
+  const int64_t qs = (int64_t)q;
+  for (int k = 0; k <= d; k++) {
+    int64_t r = c[k] % qs;
+    cm[k] = (uint64_t)(r < 0 ? r + qs : r);
+  }
+  return rfr_squarefree_mod(cm, d, q);
+}
+
 int rfr_squarefree_mod(const uint64_t* cm, int d, uint64_t q) {
   if (d < 1 || q < 3) return 0;
   if (cm[d] % q == 0) return 0;

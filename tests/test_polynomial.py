@@ -246,6 +246,31 @@ def test_squarefree_screen_fp_path_is_exact_mod_q():
     assert yes > 5 and no > 5
 
 
+def test_squarefree_screen_i64_entry_matches_the_residue_entry():
+    """rfr_squarefree_i64 (signed coefficients reduced inside) answers as
+    rfr_squarefree_mod on the residues, for both prime paths."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2410_15880_b200 import _lib
+
+    lib = _lib.load()
+    rng = random.Random(17)
+    for q in (33554393, 2305843009213693951):
+        for _ in range(60):
+            d = rng.randint(1, 120)
+            co = [rng.randint(-(1 << 61), 1 << 61) for _ in range(d)] + [rng.choice([1, -3, 7])]
+            if rng.random() < 0.3:  # a square factor over Z
+                co = list(multiply(P(co[: d // 2 + 1]), multiply(P([rng.randint(-9, 9), 1]), P([rng.randint(-9, 9), 1]))).coeffs)
+                if max(abs(c) for c in co) >= 1 << 62:
+                    continue
+            a = np.array(co, dtype=np.int64)
+            cm = np.array([c % q for c in co], dtype=np.uint64)
+            want = lib.rfr_squarefree_mod(cm.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(co) - 1, q)
+            assert lib.rfr_squarefree_i64(a.ctypes.data, len(co) - 1, q) == want
+
+
 def test_factor_cells_split_implied_factors():
     """The factor partition (verify._factor_cells): after an early stop the
     candidates may hold t = f3*f4, f3 inside t, f1 inside ~t and nothing for
