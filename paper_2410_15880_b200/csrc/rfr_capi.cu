@@ -304,15 +304,15 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
   const ListHist H = list_hist_layout(P0, hb);
   DevCounters* d_ctr = (DevCounters*)g.ctr.p;
   const bool early = ee != nullptr && wins.size() == 1;
+  g_tr.mark("search_core: lists launch");
+  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p, H, s));
+  g_tr.mark("search_core: lists enqueued");
   if (early) {
     // the raw-hit slots start as kUnsetHit (the poller's "not yet written"):
     // filled on the second stream while the lists are built
     RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), g.stream2));
     RFR_CUDA_OK(cudaEventRecord(g.ev_fill, g.stream2));
   }
-  g_tr.mark("search_core: lists launch");
-  RFR_CUDA_OK(launch_lists(d_keys, P0, bufs(0), bufs(1), (uint32_t*)g.rotc.p, H, s));
-  g_tr.mark("search_core: lists enqueued");
   {
     int maxbits = 0;
     for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
