@@ -139,20 +139,23 @@ int make_plan(int n, uint64_t lo, uint64_t width, int nshards, JoinPlan* P) {
   if (r > 61 - hb) r = 61 - hb;  // keep the window radius <= W / 8
   if (r < 2) return rfr_fail(RFR_E_ARG, "window too wide for one plan (internal)");
   auto clampi = [](int v, int lo_, int hi_) { return v < lo_ ? lo_ : (v > hi_ ? hi_ : v); };
-  // outer lists: one outer per join warp per side (each warp walks one long
-  // run per bucket), unless the runs would exceed 2^lam records
-  // per bucket (default 256: the run pass keeps <= 12 chunks of a run in
-  // flight); inner lists capped at 2^kMaxInnerBits entries (streamed)
+  // outer lists: at least one outer per join warp per side, and runs of at
+  // most 2^lam records per outer per bucket.  Default 128:
+  // since the run passes are compiled for fixed chunk counts (join v17) the
+  // join pays only ~6 % for 128 against 256, while the inner lists and their
+  // build halve (C3: lists 0.41 -> 0.26 ms; RFR_LAMBDA_LOG=8: 256); inner
+  // lists capped at 2^kMaxInnerBits entries (streamed)
   static int lam = -1;
   if (lam < 0) {
     const char* e = getenv("RFR_LAMBDA_LOG");
-    lam = e ? atoi(e) : 8;
+    lam = e ? atoi(e) : 7;
   }
   int warps_log = 0;
   while ((1 << (warps_log + 1)) <= kJoinThreadsPerCta / 32) warps_log++;
   // every shard rebuilds the whole quarter lists while the join is split
   // nshards ways, so shorter runs (smaller inner lists) pay off on many GPUs
-  // (measured at n = 55: 256 is best up to 2 shards, 128 at 4, 64-128 at 8)
+  // (round 1, measured at n = 55 with the join then: 256 was best up to 2
+  // shards, 128 at 4, 64-128 at 8)
   const int lam_s = lam - (nshards >= 4 ? 1 : 0) - (nshards >= 16 ? 1 : 0);
   auto outer_bits = [&](int side) {
     const int want = side - r - lam_s > warps_log ? side - r - lam_s : warps_log;

@@ -553,11 +553,11 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // outer whose last chunk is still full is flagged for continue_pass
 // (off = 32 * nch).  Same record semantics as window_pass.
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
-// chunk counts of the default plan's runs (lambda = 256 records per outer
-// per bucket on side A, 128 or 256 on side B for even or odd n:
-// ceil((lambda + 3 sqrt(lambda) + 8) / 32)), compiled as their own run_pass
-// instances
-constexpr int kNchA = 10, kNchB = 6;
+// chunk counts of runs of lambda = 256, 128 and 64 records per outer per
+// bucket (ceil((lambda + 3 sqrt(lambda) + 8) / 32)), compiled as their own
+// run_pass instances: the default plan runs 128 on both sides, sharded plans
+// 64, RFR_LAMBDA_LOG=8 256
+constexpr int kNch256 = 10, kNch128 = 6, kNch64 = 3;
 // SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
 // so "in bucket" and "in halo" are 32-bit tests on the high / low words.
 // 32-bit bucket/halo classification in the run pass (SMALLH): the halo fits
@@ -988,14 +988,18 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
       const int t = tid_now(), w = t >> 5;
       PassSt sa{0u, join_smem().cnt[0][t], join_smem().cnt[2][t], false, false};
       const uint32_t wlo = join_smem().wlo[0][w], whi = join_smem().whi[0][w];
-      if (gsA > 32 && smallh && (gsA >> 5) == kNchA) {
-        sa = (whi - wlo) * 32u * kNchA <= (uint32_t)kPart
-                 ? run_pass<true, true, kNchA, true>(a, cW, wlo, whi, gsA >> 5, sa)
-                 : run_pass<true, true, kNchA>(a, cW, wlo, whi, gsA >> 5, sa);
-      } else if (gsA > 32 && smallh && (gsA >> 5) == kNchB) {  // lambda = 128 (sharded plans)
-        sa = (whi - wlo) * 32u * kNchB <= (uint32_t)kPart
-                 ? run_pass<true, true, kNchB, true>(a, cW, wlo, whi, gsA >> 5, sa)
-                 : run_pass<true, true, kNchB>(a, cW, wlo, whi, gsA >> 5, sa);
+      const int nA = gsA >> 5;
+      if (gsA > 32 && smallh && (nA == kNch256 || nA == kNch128 || nA == kNch64)) {
+        const bool noovf = (whi - wlo) * 32u * (uint32_t)nA <= (uint32_t)kPart;
+        if (nA == kNch128)
+          sa = noovf ? run_pass<true, true, kNch128, true>(a, cW, wlo, whi, nA, sa)
+                     : run_pass<true, true, kNch128>(a, cW, wlo, whi, nA, sa);
+        else if (nA == kNch256)
+          sa = noovf ? run_pass<true, true, kNch256, true>(a, cW, wlo, whi, nA, sa)
+                     : run_pass<true, true, kNch256>(a, cW, wlo, whi, nA, sa);
+        else
+          sa = noovf ? run_pass<true, true, kNch64, true>(a, cW, wlo, whi, nA, sa)
+                     : run_pass<true, true, kNch64>(a, cW, wlo, whi, nA, sa);
       } else {
         sa = gsA > 32 ? (smallh ? run_pass<true, true>(a, cW, wlo, whi, gsA >> 5, sa) : run_pass<true, false>(a, cW, wlo, whi, gsA >> 5, sa))
                         : window_pass<true>(a, cW, wlo, whi, gsA, sa);
@@ -1024,10 +1028,12 @@ __global__ void __launch_bounds__(kJoinThreads, kJoinCtasPerSm)
         const int t = tid_now(), w = t >> 5;
         PassSt sb{0u, join_smem().cnt[1][t], join_smem().cnt[2][t], false, false};
         const uint32_t blo = join_smem().wlo[1][w], bhi = join_smem().whi[1][w];
-        sb = gsB > 32 ? (smallh ? ((gsB >> 5) == kNchB   ? run_pass<false, true, kNchB>(a, cW, blo, bhi, gsB >> 5, sb)
-                                   : (gsB >> 5) == kNchA ? run_pass<false, true, kNchA>(a, cW, blo, bhi, gsB >> 5, sb)
-                                                         : run_pass<false, true>(a, cW, blo, bhi, gsB >> 5, sb))
-                                : run_pass<false, false>(a, cW, blo, bhi, gsB >> 5, sb))
+        const int nB = gsB >> 5;
+        sb = gsB > 32 ? (smallh ? (nB == kNch128   ? run_pass<false, true, kNch128>(a, cW, blo, bhi, nB, sb)
+                                   : nB == kNch256 ? run_pass<false, true, kNch256>(a, cW, blo, bhi, nB, sb)
+                                   : nB == kNch64  ? run_pass<false, true, kNch64>(a, cW, blo, bhi, nB, sb)
+                                                   : run_pass<false, true>(a, cW, blo, bhi, nB, sb))
+                                : run_pass<false, false>(a, cW, blo, bhi, nB, sb))
                       : window_pass<false>(a, cW, join_smem().wlo[1][w], join_smem().whi[1][w], gsB, sb);
         RFR_MARK();
         if (sb.cont) {
