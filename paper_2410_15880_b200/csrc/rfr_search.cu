@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(256) lists_split_kernel(const uint64_t* __rest
                                                           JoinPlan P, int k, ListBufs in,
                                                           const uint32_t* __restrict__ rot,
                                                           ListHist H) {
+  pdl_wait();  // the previous level is complete
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const uint32_t w = blockIdx.x * 8u + (threadIdx.x >> 5);
   const int li = blockIdx.y;
@@ -835,10 +837,12 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
     const uint64_t outputs = 2ull << k;
     const unsigned int blocks = (unsigned int)((outputs + kMergeTile - 1) / kMergeTile);
     if (split_kernel) {
-      lists_split_kernel<<<dim3((blocks + 1 + 7) / 8, 4), 256, 0, s>>>(d_keys, P, k, parity ? buf1 : buf0,
-                                                                   d_rot, H);
-      lists_merge_kernel<0><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
-          d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+      cudaError_t le = launch_pdl(lists_split_kernel, dim3((blocks + 1 + 7) / 8, 4), dim3(256), 0, s, d_keys, P,
+                                  k, parity ? buf1 : buf0, (const uint32_t*)d_rot, H);
+      if (le == cudaSuccess)
+        le = launch_pdl(lists_merge_kernel<0>, dim3(blocks, 4), dim3(kMergeThreads), 0, s, d_keys, P, k,
+                        parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
+      if (le != cudaSuccess) return le;
     } else if (tma) {
       lists_merge_kernel<2><<<dim3(blocks, 4), kMergeThreads, 0, s>>>(
           d_keys, P, k, parity ? buf1 : buf0, parity ? buf0 : buf1, d_rot, H);
