@@ -4,6 +4,8 @@
 // of its per-entity keys (fixed-point fractional parts scaled by 2^64), so an
 // integer sum of fractional parts is a key near 0.  See DESIGN.md section 2.
 #pragma once
+#include <cstdlib>
+#include <utility>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -132,6 +134,32 @@ static_assert(offsetof(DevCounters, found) % 16 == 0, "found must be 16-byte ali
 // being launched after it (no-ops in a plain launch).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// RFR_PDL=0 (A/B): plain launches everywhere launch_pdl is used
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RFR_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace rfr
 

@@ -643,6 +643,8 @@ __global__ void __launch_bounds__(256) index_to_pattern_kernel(const PatArgs a, 
                                                                const unsigned long long* count,
                                                                unsigned long long cap,
                                                                const unsigned long long* begin) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   unsigned long long m = *count;
   if (m > cap) m = cap;
   const unsigned long long m0 = begin ? min(*begin, m) : 0ull;  // hits [m0, m) are new
@@ -676,7 +678,8 @@ cudaError_t launch_index_to_pattern(const JoinPlan& P, const ListBufs& base, con
   for (int i = 0; i < 4; i++) a.pat[i] = base.p[i];
   a.hist = hist;
   a.rot = d_rot;
-  index_to_pattern_kernel<<<nsm * 4, 256, 0, s>>>(a, d_out, d_count, cap, d_begin);
+  cudaError_t e = launch_pdl(index_to_pattern_kernel, dim3(nsm * 4), dim3(256), 0, s, a, d_out, d_count, cap, d_begin);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -716,6 +719,8 @@ __global__ void keyfilter_kernel(const uint64_t* __restrict__ keys2, int n,
                                  unsigned long long cap_in, uint64_t lo2, uint64_t width2,
                                  uint64_t* __restrict__ out, unsigned long long cap_out,
                                  DevCounters* ctr, const unsigned long long* __restrict__ begin) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   __shared__ uint64_t sk[64];
   for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = keys2[i];
   __syncthreads();
@@ -788,32 +793,6 @@ ListHist list_hist_layout(const JoinPlan& P, char* const base[4]) {
     H.sp[i] = (uint32_t*)(b + ((bm + 15) & ~(size_t)15) + ((dir + 15) & ~(size_t)15));
   }
   return H;
-}
-
-// RFR_PDL=0 (A/B): plain launches for the list levels and the start positions
-static bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("RFR_PDL");
-    on = e ? atoi(e) != 0 : 1;
-  }
-  return on != 0;
-}
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
@@ -952,8 +931,9 @@ cudaError_t launch_keyfilter(const uint64_t* d_keys2, int n, const uint64_t* d_i
                              uint64_t lo2, uint64_t width2, uint64_t* d_out,
                              unsigned long long cap_out, DevCounters* d_ctr, int nsm, cudaStream_t s,
                              const unsigned long long* d_begin) {
-  keyfilter_kernel<<<nsm * 4, 256, 0, s>>>(d_keys2, n, d_in, d_in_count, cap_in, lo2, width2, d_out,
-                                          cap_out, d_ctr, d_begin);
+  cudaError_t e = launch_pdl(keyfilter_kernel, dim3(nsm * 4), dim3(256), 0, s, d_keys2, n, d_in, d_in_count,
+                             cap_in, lo2, width2, d_out, cap_out, d_ctr, d_begin);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1183,6 +1163,8 @@ __global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __res
                                                            uint64_t lo, uint64_t width, int b, int g,
                                                            uint64_t* __restrict__ out,
                                                            unsigned long long cap, DevCounters* ctr) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   table_search_body(keys, n, lo, width, b, g, out, cap, ctr, blockIdx.x);
 }
 
@@ -1211,8 +1193,9 @@ cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint
   static uint64_t attr_done = 0;
   cudaError_t e = raise_smem_limit(table_search_kernel, (size_t)10 << kTableMaxBits, attr_done);
   if (e != cudaSuccess) return e;
-  table_search_kernel<<<(unsigned)((threads + 255) / 256), 256, smem, s>>>(d_keys, n, lo, width, b, g,
-                                                                          d_out, cap, d_ctr);
+  e = launch_pdl(table_search_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), smem, s, d_keys, n, lo,
+                 width, b, g, d_out, cap, d_ctr);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1220,6 +1203,8 @@ cudaError_t launch_table_search(const uint64_t* d_keys, int n, uint64_t lo, uint
 // as patterns of the parent's search (rfr_search_verify after an early stop).
 __global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long long* __restrict__ count,
                                unsigned long long cap, uint64_t mask) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   unsigned long long m = *count;
   if (m > cap) m = cap;
   for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
@@ -1232,7 +1217,8 @@ __global__ void deposit_kernel(uint64_t* __restrict__ pats, const unsigned long 
 }
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s) {
-  deposit_kernel<<<nsm, 256, 0, s>>>(d_pats, d_count, cap, mask);
+  cudaError_t e = launch_pdl(deposit_kernel, dim3(nsm), dim3(256), 0, s, d_pats, d_count, cap, mask);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1241,6 +1227,8 @@ cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, 
 // and the first min(post_count, rows) rows -- one launch instead of five
 // small device-to-host copies, each with its own ~3 us of setup and gap.
 __global__ void collect_kernel(CollectArgs C) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   const unsigned long long cnt = C.ctr->post_count;
   const unsigned rows = (unsigned)(cnt < C.rows ? cnt : C.rows);
   const int t = threadIdx.x;
@@ -1255,7 +1243,8 @@ __global__ void collect_kernel(CollectArgs C) {
   for (unsigned k = t; k < nco; k += blockDim.x) C.h_coeffs[k] = C.coeffs[k];
 }
 cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
-  collect_kernel<<<1, 256, 0, s>>>(C);
+  cudaError_t e = launch_pdl(collect_kernel, dim3(1), dim3(256), 0, s, C);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1270,6 +1259,8 @@ cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
 // rows than the caller takes) makes every later kernel a no-op; the host
 // compares the plan's t with its own before using the rows.
 __global__ void piece_plan_kernel(PiecePlanArgs a) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   __shared__ unsigned long long s_t;
   __shared__ int s_act;
   const int tid = threadIdx.x;
@@ -1319,6 +1310,8 @@ __global__ void __launch_bounds__(256) piece_search_kernel(const PieceDesc* __re
                                                            const uint64_t* __restrict__ pkeys, uint64_t lo,
                                                            uint64_t width, uint64_t* __restrict__ praw,
                                                            unsigned long long cap, DevCounters* pctr) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   const int pi = blockIdx.y;
   if (!desc->active) return;
   const int n = desc->ns[pi];
@@ -1338,6 +1331,8 @@ __global__ void piece_filter_kernel(const PieceDesc* __restrict__ desc, const ui
                                     const uint64_t* __restrict__ praw, unsigned long long raw_cap,
                                     uint64_t lo2, uint64_t width2, uint64_t* __restrict__ ppost,
                                     unsigned long long post_cap, DevCounters* pctr) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   const int pi = blockIdx.y;
   if (!desc->active || desc->ns[pi] < 2) return;
   __shared__ uint64_t sk[64];
@@ -1367,6 +1362,8 @@ __global__ void piece_filter_kernel(const PieceDesc* __restrict__ desc, const ui
 }
 
 __global__ void collect2_kernel(CollectArgs C0, CollectArgs C1) {
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   const CollectArgs& C = blockIdx.x ? C1 : C0;
   const unsigned long long cnt = C.ctr->post_count;
   const unsigned rows = (unsigned)(cnt < C.rows ? cnt : C.rows);
@@ -1386,22 +1383,22 @@ cudaError_t launch_pieces(const PiecePlanArgs& a, uint64_t lo, uint64_t width, u
                           uint64_t* praw, unsigned long long raw_cap, uint64_t* ppost,
                           unsigned long long post_cap, const struct VerifyArgs* V, const CollectArgs* C,
                           int nsm, cudaStream_t s) {
-  piece_plan_kernel<<<1, 64, 0, s>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(piece_plan_kernel, dim3(1), dim3(64), 0, s, a);
   if (e != cudaSuccess) return e;
   static uint64_t attr_done = 0;
   e = raise_smem_limit(piece_search_kernel, (size_t)10 << kTableMaxBits, attr_done);
   if (e != cudaSuccess) return e;
   // <= 2^16 threads per piece (n <= kExhaustiveMaxN: b = 8, h <= 22, g = h - 16)
-  piece_search_kernel<<<dim3(256, 2), 256, (size_t)10 << 8, s>>>(a.desc, a.pkeys, lo, width, praw, raw_cap,
-                                                                  a.pctr);
-  piece_filter_kernel<<<dim3(nsm, 2), 256, 0, s>>>(a.desc, a.pkeys, praw, raw_cap, lo2, width2, ppost,
-                                                     post_cap, a.pctr);
-  e = cudaGetLastError();
+  e = launch_pdl(piece_search_kernel, dim3(256, 2), dim3(256), (size_t)10 << 8, s, (const PieceDesc*)a.desc,
+                 (const uint64_t*)a.pkeys, lo, width, praw, raw_cap, a.pctr);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(piece_filter_kernel, dim3(nsm, 2), dim3(256), 0, s, (const PieceDesc*)a.desc,
+                 (const uint64_t*)a.pkeys, (const uint64_t*)praw, raw_cap, lo2, width2, ppost, post_cap, a.pctr);
   if (e != cudaSuccess) return e;
   for (int pi = 0; pi < 2; pi++)
     if ((e = launch_verify(V[pi], s)) != cudaSuccess) return e;
-  collect2_kernel<<<2, 256, 0, s>>>(C[0], C[1]);
+  e = launch_pdl(collect2_kernel, dim3(2), dim3(256), 0, s, C[0], C[1]);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -26,6 +26,8 @@ namespace rfr {
 __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(VerifyArgs A) {
   __shared__ WarpBuf bufs[kVerifyWarps];
   __shared__ ProfSmem PS;
+  pdl_wait();  // programmatic launch: the previous kernel is complete
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   long long mm = A.m;
   if (A.m_dev) mm = min(mm, (long long)*A.m_dev);
@@ -55,7 +57,8 @@ cudaError_t launch_verify(const VerifyArgs& A, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (blocks > 8LL * nsm) blocks = 8LL * nsm;
   }
-  verify_kernel<<<(unsigned)blocks, kVerifyWarps * 32, 0, s>>>(A);
+  const cudaError_t e = launch_pdl(verify_kernel, dim3((unsigned)blocks), dim3(kVerifyWarps * 32), 0, s, A);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
