@@ -270,6 +270,34 @@ def test_device_chained_pieces_match_host_driven_pieces(big_inputs, monkeypatch)
     assert device >= 4
 
 
+@pytest.mark.parametrize("degs,seed", [((24, 76), 51), ((30, 70), 52)])
+def test_uneven_stop_with_a_large_piece_matches_sympy(degs, seed):
+    """A stop whose larger piece has more than 31 entities: the device piece
+    plan marks itself inactive and the call searches the pieces itself
+    (lists + join for the large one) or leaves them to the host; either way
+    the factorization equals sympy's and nothing is searched twice on the
+    device chain (rfr_stats.pieces != 2 for that call)."""
+    import sympy
+
+    x = sympy.symbols("x")
+    rng = random.Random(seed)
+    fs = []
+    for dg in degs:
+        while True:
+            co = [rng.randint(-30, 30) for _ in range(dg)] + [1]
+            f = sympy.Poly(list(reversed(co)), x)
+            if f.is_irreducible:
+                fs.append(f)
+                break
+    prod = fs[0] * fs[1]
+    p = P([int(c) for c in reversed(prod.all_coeffs())])
+    res = factor(p)
+    assert res.certificate
+    want = sorted([int(c) for c in reversed(f.all_coeffs())] for f in fs)
+    assert sorted(list(g.coeffs) for g, _ in res.factors) == want
+    assert res.stats.n >= 48
+
+
 def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
     """If the exact check rejects every verified factor of a stopped search
     (a false device PASS), factor() searches the whole pattern space and

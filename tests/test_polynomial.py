@@ -155,6 +155,30 @@ def test_kronecker_multiply_and_divide_match_schoolbook():
     assert hits > 100
 
 
+def test_divide_exact_monic_native_range_edges():
+    """The native monic long division (rfr_divide_monic_i64) hands back to
+    the big-integer path when a running quotient coefficient reaches 2^62 or
+    the operands leave int64 / 2^31: the answers still equal the schoolbook
+    ones on both sides of those limits."""
+    from paper_2410_15880_b200.polynomial import divide_exact, multiply
+
+    cases = [
+        ([1] + [0] * 9 + [1], [-(1 << 30), 1]),                   # quotient grows past 2^62: not exact
+        (list(multiply(P([-(1 << 30), 1]), P([5, 0, 1])).coeffs), [-(1 << 30), 1]),  # exact, small quotient
+        (list(multiply(P([(1 << 31) - 1, 1]), P([3, 1])).coeffs), [(1 << 31) - 1, 1]),  # |q_i| at 2^31 - 1
+        (list(multiply(P([1 << 31, 1]), P([3, 1])).coeffs), [1 << 31, 1]),  # |q_i| = 2^31: big-integer path
+        (list(multiply(P([7, 1]), P([(1 << 61), 2, 1])).coeffs), [7, 1]),  # p beyond 2^62
+        ([(1 << 62) - 1, 0, 1], [1, 1]),                                     # not exact, large constant
+    ]
+    for pc, q in cases:
+        got = divide_exact(P(pc), P(q))
+        want = _school_div(pc, q)
+        if want is None:
+            assert got is None
+        else:
+            assert got is not None and list(got.coeffs) == list(P(want).coeffs)
+
+
 def test_divide_exact_base_2_64_carries():
     """divide_exact tries the 64-bit Kronecker base first: a quotient whose
     coefficients overflow 64 bits is still found (Mignotte base), and a
