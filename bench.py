@@ -425,8 +425,9 @@ def run_ours(args):
             "key_window": "exact 64-bit first+second power-sum keys, +-T from rigorous root inclusion radii",
             "value_scope": "device-resident keys, whole pattern space searched (no early "
                            "termination: the cost of an irreducible input) + verification",
-            "l2": "256 MB buffer written between timed steps (flush); the inner quarter lists "
-                  "(2^23-2^24 entries per half) exceed L2 and are streamed from HBM",
+            "l2": "256 MB buffer written between timed steps (flush, > the 126 MB L2); the two "
+                  "inner quarter lists (2^22-2^23 entries, 32-64 MB each with runs of 128) are "
+                  "built inside the step and partly read back from L2 by the join",
             "parallelism": f"key-range shards x{world}" if world > 1 else "1 GPU",
         },
         "search_ms": round(float(np.mean(search)), 4),
