@@ -298,6 +298,28 @@ def test_uneven_stop_with_a_large_piece_matches_sympy(degs, seed):
     assert res.stats.n >= 48
 
 
+def test_repeated_calls_are_stable(big_inputs, factor_cases):
+    """Hundreds of back-to-back factor() calls (early stops, chained piece
+    searches, small whole searches in between) return the same answers and
+    leave the device memory in use where the first round left it (the
+    library's buffers are grown once and reused)."""
+    import torch
+
+    c3 = [poly_of(c["p"]) for c in big_inputs["c3"]]
+    small = [poly_of(c["input"]) for c in factor_cases[:20]]
+    first = {}
+    for p in c3 + small:
+        first[p.coeffs] = _got(factor(p))
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for rep in range(40):
+        for p in c3 + small[rep % 4::4]:
+            assert _got(factor(p)) == first[p.coeffs]
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (64 << 20)
+
+
 def test_early_exit_falls_back_to_the_whole_space(big_inputs, monkeypatch):
     """If the exact check rejects every verified factor of a stopped search
     (a false device PASS), factor() searches the whole pattern space and
