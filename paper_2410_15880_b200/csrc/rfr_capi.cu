@@ -84,7 +84,7 @@ struct Ctx {
   DevVec hist[4];  // merge history per list (pattern recovery)
   DevVec vprof, vpats, vpmod, vverd, vside, vcoef;  // verification scratch
   DevVec pctr, praw, ppost;  // the two pieces' counters / raw hits / survivors (concurrent)
-  DevVec pdesc, pver;        // device piece plan; the pieces' verification rows
+  DevVec pver;               // the chained pieces' verification rows
   DevVec lk[4][2], lp[4][2];  // list keys / patterns, ping-pong
   DevCounters* h_ctr = nullptr;  // pinned mirror
   void* h_stage = nullptr;       // pinned staging of rfr_verify (in, then out)
@@ -497,6 +497,25 @@ PieceDesc* piece_h_desc(int stride) {
 }
 // The collected rows of the pieces with >= 2 entities; false on an overflow
 // (more raw hits than raw_cap or more survivors than kPieceRows).
+// The rows of the chained piece searches (one pinned area: counters, then
+// up to 2 kPieceRows rows of both pieces); false when they did not fit.
+bool read_chained_piece_rows(int stride, std::vector<uint64_t>& xp, std::vector<uint8_t>& xv,
+                             std::vector<uint8_t>& xs, std::vector<int64_t>& xc) {
+  const char* hp = (const char*)g.h_piece;
+  const DevCounters c = *(const DevCounters*)hp;
+  const unsigned rows_cap = 2 * kPieceRows;
+  if (c.post_count > (unsigned long long)rows_cap) return false;
+  const char* rows = hp + sizeof(DevCounters);
+  for (unsigned long long k = 0; k < c.post_count; k++) {
+    xp.push_back(((const uint64_t*)rows)[k]);
+    xv.push_back(((const uint8_t*)(rows + rows_cap * 8))[k]);
+    xs.push_back(((const uint8_t*)(rows + rows_cap * 9))[k]);
+    const int64_t* cr = (const int64_t*)(rows + rows_cap * 10) + k * stride;
+    xc.insert(xc.end(), cr, cr + stride);
+  }
+  return true;
+}
+
 bool read_piece_rows(int stride, const int ns[2], unsigned long long raw_cap, std::vector<uint64_t>& xp,
                      std::vector<uint8_t>& xv, std::vector<uint8_t>& xs, std::vector<int64_t>& xc,
                      int64_t* buckets) {
@@ -728,7 +747,7 @@ static void release_ctx() {
   if (g.stream) cudaStreamSynchronize(g.stream);
   DevVec* vecs[] = {&g.keys, &g.keys2, &g.rho, &g.raw, &g.post, &g.ctr, &g.rotc, &g.jstarts, &g.pkeys,
                     &g.vprof, &g.vpats, &g.vpmod, &g.vverd, &g.vside, &g.vcoef, &g.pctr, &g.praw,
-                    &g.ppost, &g.pdesc, &g.pver};
+                    &g.ppost, &g.pver};
   for (DevVec* v : vecs) v->release();
   for (auto& h : g.hist) h.release();
   for (auto& a : g.lk)
@@ -1175,6 +1194,17 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       g.h_stage_bytes = out_bytes;
     }
     hs = (char*)g.h_stage;
+    // an early stop's two pieces, searched on the device right behind the
+    // main search (every piece kernel is a no-op unless the search stopped at
+    // a PASS whose pieces are small); RFR_HOST_PIECES=1 (A/B): the host-driven
+    // path only
+    dev_pieces = early_exit == 1 && early && !getenv("RFR_HOST_PIECES");
+    if (dev_pieces) {
+      RFR_CUDA_OK(g.pctr.ensure(sizeof(DevCounters)));
+      RFR_CUDA_OK(g.ppost.ensure(kPieceRaw * sizeof(uint64_t)));
+      RFR_CUDA_OK(g.pver.ensure(2 * al(2 * kPieceRows) + 2 * kPieceRows * (size_t)stride * sizeof(int64_t)));
+      if ((rc = ensure_piece_host(stride))) return rc;
+    }
     {  // counters and the first rows in one launch, straight into pinned memory
       CollectArgs C;
       C.ctr = d_ctr;
@@ -1189,21 +1219,15 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       C.h_verdict = (uint8_t*)(hs + h_verd);
       C.h_side = (uint8_t*)(hs + h_side);
       C.h_coeffs = (long long*)(hs + h_coef);
+      if (dev_pieces) {  // the pieces' counters start from zero
+        C.clear = (unsigned long long*)g.pctr.p;
+        C.clear_words = (int)(sizeof(DevCounters) / 8);
+      }
       RFR_CUDA_OK(launch_collect(C, s));
     }
-    // an early stop's two pieces, searched on the device right behind (every
-    // piece kernel is a no-op unless the search stopped at a PASS whose
-    // pieces are small); RFR_HOST_PIECES=1 (A/B): the host-driven path only
-    dev_pieces = false;
-    if (early_exit == 1 && early && !getenv("RFR_HOST_PIECES")) {
+    if (dev_pieces) {
       const size_t pv_side = al(2 * kPieceRows), pv_coef = 2 * pv_side;
-      RFR_CUDA_OK(g.pctr.ensure(2 * sizeof(DevCounters)));
-      RFR_CUDA_OK(g.praw.ensure(2 * kPieceRaw * sizeof(uint64_t)));
-      RFR_CUDA_OK(g.ppost.ensure(2 * kPieceRaw * sizeof(uint64_t)));
-      RFR_CUDA_OK(g.pkeys.ensure(2 * 2 * 64 * sizeof(uint64_t)));
-      RFR_CUDA_OK(g.pdesc.ensure(sizeof(PieceDesc)));
-      RFR_CUDA_OK(g.pver.ensure(pv_coef + 2 * kPieceRows * (size_t)stride * sizeof(int64_t)));
-      if ((rc = ensure_piece_host(stride))) return rc;
+      DevCounters* pctr = (DevCounters*)g.pctr.p;
       PiecePlanArgs pa;
       pa.ctr = d_ctr;
       pa.planned = (unsigned long long)g_buckets_planned;
@@ -1215,45 +1239,36 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       pa.n = n;
       pa.keys = d_keys;
       pa.keys2 = d_keys2;
-      pa.desc = (PieceDesc*)g.pdesc.p;
       pa.h_desc = piece_h_desc(stride);
-      pa.pkeys = (uint64_t*)g.pkeys.p;
-      pa.pctr = (DevCounters*)g.pctr.p;
-      VerifyArgs PV[2];
-      CollectArgs PC[2];
-      const size_t per = piece_per(stride);
+      pa.pctr = pctr;
+      pa.ppost = (uint64_t*)g.ppost.p;
       char* pvb = (char*)g.pver.p;
-      for (int pi = 0; pi < 2; pi++) {
-        DevCounters* ctr = (DevCounters*)g.pctr.p + pi;
-        uint64_t* post = (uint64_t*)g.ppost.p + pi * kPieceRaw;
-        PV[pi] = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
-        PV[pi].pats = post;
-        PV[pi].m = kPieceRows;
-        PV[pi].m_dev = &ctr->post_count;
-        PV[pi].found = nullptr;
-        PV[pi].verdict = (uint8_t*)pvb + pi * kPieceRows;
-        PV[pi].side = (uint8_t*)(pvb + pv_side) + pi * kPieceRows;
-        PV[pi].coeffs = (long long*)(pvb + pv_coef) + (size_t)pi * kPieceRows * stride;
-        PV[pi].stride = stride;
-        char* hp = (char*)g.h_piece + pi * per;
-        char* rows = hp + 2 * 64 * 8 + sizeof(DevCounters);
-        PC[pi].ctr = ctr;
-        PC[pi].pats = post;
-        PC[pi].verdict = PV[pi].verdict;
-        PC[pi].side = PV[pi].side;
-        PC[pi].coeffs = PV[pi].coeffs;
-        PC[pi].stride = stride;
-        PC[pi].rows = kPieceRows;
-        PC[pi].h_ctr = (DevCounters*)(hp + 2 * 64 * 8);
-        PC[pi].h_pats = (uint64_t*)rows;
-        PC[pi].h_verdict = (uint8_t*)(rows + kPieceRows * 8);
-        PC[pi].h_side = (uint8_t*)(rows + kPieceRows * 9);
-        PC[pi].h_coeffs = (long long*)(rows + kPieceRows * 10);
-      }
-      RFR_CUDA_OK(launch_pieces(pa, lo, width, lo2, width2, (uint64_t*)g.praw.p, kPieceRaw,
-                                (uint64_t*)g.ppost.p, kPieceRaw, PV, PC, g.nsm, s));
+      VerifyArgs PV = bind_profile(prof, d, base + o_prof, base + o_perm, base + o_pmod);
+      PV.pats = (const uint64_t*)g.ppost.p;
+      PV.m = 2 * kPieceRows;
+      PV.m_dev = &pctr->post_count;
+      PV.found = nullptr;
+      PV.verdict = (uint8_t*)pvb;
+      PV.side = (uint8_t*)(pvb + pv_side);
+      PV.coeffs = (long long*)(pvb + pv_coef);
+      PV.stride = stride;
+      char* hp = (char*)g.h_piece;  // [counters][2 kPieceRows rows]
+      char* rows = hp + sizeof(DevCounters);
+      CollectArgs PC;
+      PC.ctr = pctr;
+      PC.pats = PV.pats;
+      PC.verdict = PV.verdict;
+      PC.side = PV.side;
+      PC.coeffs = PV.coeffs;
+      PC.stride = stride;
+      PC.rows = 2 * kPieceRows;
+      PC.h_ctr = (DevCounters*)hp;
+      PC.h_pats = (uint64_t*)rows;
+      PC.h_verdict = (uint8_t*)(rows + 2 * kPieceRows * 8);
+      PC.h_side = (uint8_t*)(rows + 2 * kPieceRows * 9);
+      PC.h_coeffs = (long long*)(rows + 2 * kPieceRows * 10);
+      RFR_CUDA_OK(launch_pieces(pa, lo, width, lo2, width2, kPieceRaw, PV, PC, s));
       RFR_CUDA_OK(cudaEventRecord(g.ev[4], s));
-      dev_pieces = true;
     }
     g_tr.mark("post enqueued, sync");
     RFR_CUDA_OK(cudaStreamSynchronize(s));
@@ -1297,8 +1312,7 @@ int search_verify_impl(const uint64_t* keys, int n, uint64_t lo, uint64_t width,
       V0.stride = stride;
       const PieceDesc* D = dev_pieces ? piece_h_desc(stride) : nullptr;
       if (D && D->active && D->t == t) {  // searched on the device behind the main search
-        const int ns[2] = {D->ns[0], D->ns[1]};
-        if (read_piece_rows(stride, ns, kPieceRaw, xp, xv, xs, xc, &xbuckets)) {
+        if (read_chained_piece_rows(stride, xp, xv, xs, xc)) {
           complete = true;
           pieces_how = 2;
         }

@@ -49,6 +49,8 @@ struct CollectArgs {
   uint8_t* h_verdict;
   uint8_t* h_side;
   long long* h_coeffs;
+  unsigned long long* clear = nullptr;  // optional: words zeroed after the copy (the next chain's counters)
+  int clear_words = 0;
 };
 cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s);
 // The pieces of an early stop searched on the device behind the main search
@@ -71,15 +73,13 @@ struct PiecePlanArgs {
   int n;
   const uint64_t* keys;  // the search's keys and Tr3 keys (n each)
   const uint64_t* keys2;
-  PieceDesc* desc;    // device copy (read by the piece kernels)
-  PieceDesc* h_desc;  // pinned host copy (checked by the host)
-  uint64_t* pkeys;    // [piece][keys | keys2][64]
-  DevCounters* pctr;  // [2], cleared by the plan
+  PieceDesc* h_desc;   // pinned host copy of the plan (checked by the host)
+  DevCounters* pctr;   // both pieces: raw hits and survivors (cleared beforehand)
+  uint64_t* ppost;     // both pieces' survivors, as parent patterns
 };
 cudaError_t launch_pieces(const PiecePlanArgs& a, uint64_t lo, uint64_t width, uint64_t lo2, uint64_t width2,
-                          uint64_t* praw, unsigned long long raw_cap, uint64_t* ppost,
-                          unsigned long long post_cap, const struct VerifyArgs* V, const CollectArgs* C,
-                          int nsm, cudaStream_t s);
+                          unsigned long long post_cap, const struct VerifyArgs& V, const CollectArgs& C,
+                          cudaStream_t s);
 cudaError_t launch_deposit(uint64_t* d_pats, const unsigned long long* d_count, unsigned long long cap,
                            uint64_t mask, int nsm, cudaStream_t s);
 cudaError_t launch_recheck(const double* d_rho, const uint64_t* d_in,

@@ -1048,9 +1048,44 @@ cudaError_t launch_exhaustive(const uint64_t* d_keys, int n, uint64_t lo, uint64
 // patterns instead of one add and one compare per pattern (the Gray-code
 // exhaustive_kernel, kept as the independent checker of RFR_FORCE_EXHAUSTIVE).
 constexpr int kTableMaxBits = 12;
+// Where a small search's hits go: the raw hit list (RawEmit), or -- for the
+// pieces searched behind an early stop -- straight through the Tr3 window
+// into parent patterns (PieceEmit).
+struct RawEmit {
+  DevCounters* ctr;
+  uint64_t* out;
+  unsigned long long cap;
+  __device__ __forceinline__ void operator()(uint64_t pat) const {
+    const unsigned long long k = atomicAdd(&ctr->out_count, 1ull);
+    if (k < cap) out[k] = pat;
+  }
+};
+struct PieceEmit {
+  DevCounters* ctr;     // out_count: raw hits, post_count: survivors (both pieces)
+  const uint64_t* sk2;  // the piece's Tr3 keys (shared memory)
+  uint64_t mask;        // the piece's entities as parent bits
+  uint64_t lo2, width2;
+  uint64_t* post;
+  unsigned long long cap;
+  __device__ __forceinline__ void operator()(uint64_t u) const {
+    atomicAdd(&ctr->out_count, 1ull);
+    uint64_t sum = 0, v = 0, mm = mask;
+    for (int j = 0; u; j++, u >>= 1, mm &= mm - 1)
+      if (u & 1ull) {
+        sum += sk2[j];
+        v |= mm & (0ull - mm);
+      }
+    if (sum - lo2 <= width2) {
+      const unsigned long long k = atomicAdd(&ctr->post_count, 1ull);
+      if (k < cap) post[k] = v;
+    }
+  }
+};
+
+template <class Emit>
 __device__ __forceinline__ void table_search_body(const uint64_t* __restrict__ keys, int n, uint64_t lo,
-                                                  uint64_t width, int b, int g, uint64_t* __restrict__ out,
-                                                  unsigned long long cap, DevCounters* ctr, unsigned blk) {
+                                                  uint64_t width, int b, int g, DevCounters* ctr,
+                                                  unsigned blk, const Emit& emit_pat) {
   extern __shared__ __align__(16) unsigned char tsm[];
   uint64_t* tk = reinterpret_cast<uint64_t*>(tsm);                     // sorted low sums
   uint16_t* ti = reinterpret_cast<uint16_t*>(tsm + (8u << b));         // their low patterns
@@ -1145,10 +1180,7 @@ __device__ __forceinline__ void table_search_body(const uint64_t* __restrict__ k
       if (tk[mid] < a) l = mid + 1;
       else r = mid;
     }
-    auto emit = [&](uint32_t i) {
-      const unsigned long long k = atomicAdd(&ctr->out_count, 1ull);
-      if (k < cap) out[k] = (gh << b) | ti[i];
-    };
+    auto emit = [&](uint32_t i) { emit_pat((gh << b) | ti[i]); };
     for (uint32_t i = l; i < nt && tk[i] - a <= width; i++) emit(i);
     if (a + width < a)  // the window wraps past 2^64: its head is at the table's start
       for (uint32_t i = 0; i < l && tk[i] <= a + width; i++) emit(i);
@@ -1165,7 +1197,7 @@ __global__ void __launch_bounds__(256) table_search_kernel(const uint64_t* __res
                                                            unsigned long long cap, DevCounters* ctr) {
   pdl_wait();  // programmatic launch: the previous kernel is complete
   pdl_trigger();
-  table_search_body(keys, n, lo, width, b, g, out, cap, ctr, blockIdx.x);
+  table_search_body(keys, n, lo, width, b, g, ctr, blockIdx.x, RawEmit{ctr, out, cap});
 }
 
 // table bits and threads of a small search of n entities (<= 2^16 threads,
@@ -1241,6 +1273,7 @@ __global__ void collect_kernel(CollectArgs C) {
   }
   const unsigned nco = rows * (unsigned)C.stride;
   for (unsigned k = t; k < nco; k += blockDim.x) C.h_coeffs[k] = C.coeffs[k];
+  for (int k = t; k < C.clear_words; k += blockDim.x) C.clear[k] = 0ull;
 }
 cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
   cudaError_t e = launch_pdl(collect_kernel, dim3(1), dim3(256), 0, s, C);
@@ -1250,25 +1283,29 @@ cudaError_t launch_collect(const CollectArgs& C, cudaStream_t s) {
 
 // ------------------------------------------- pieces after an early stop
 // The two pieces of the verified factor searched right behind the main
-// search on the same stream, with no host round trip: piece_plan_kernel
-// takes the first PASS row (the pattern the host would pick), splits the
-// entities into t and its complement, compacts each piece's keys and clears
-// its counters; the table search, the Tr3 window + deposit, the verification
-// and the collection follow, each piece on its own grid row (blockIdx.y) or
-// launch.  Inactive (no stop, no PASS, a piece above kExhaustiveMaxN, more
-// rows than the caller takes) makes every later kernel a no-op; the host
-// compares the plan's t with its own before using the rows.
-__global__ void piece_plan_kernel(PiecePlanArgs a) {
+// search on the same stream, with no host round trip, in one grid (blockIdx.y
+// = piece): every CTA takes the first PASS row of the main search (the
+// pattern the host would pick), splits the entities into t and its
+// complement, compacts its piece's keys into shared memory and runs the
+// table search, whose hits go through the Tr3 window straight into parent
+// patterns (PieceEmit); one verification and one collection follow.
+// Inactive (no stop, no PASS, a piece above kExhaustiveMaxN, more rows than
+// the caller takes): every CTA returns at once.  CTA (0, 0) publishes its
+// plan (PieceDesc) to pinned memory, and the host compares its t with its own
+// before using the rows.  The piece counters were cleared by the main
+// search's collection (CollectArgs.clear).
+__global__ void __launch_bounds__(256) piece_kernel(const PiecePlanArgs a, uint64_t lo, uint64_t width,
+                                                    uint64_t lo2, uint64_t width2,
+                                                    unsigned long long post_cap) {
   pdl_wait();  // programmatic launch: the previous kernel is complete
   pdl_trigger();
   __shared__ unsigned long long s_t;
   __shared__ int s_act;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < (int)(2 * sizeof(DevCounters) / 8); i += blockDim.x)
-    reinterpret_cast<unsigned long long*>(a.pctr)[i] = 0ull;
+  __shared__ uint64_t pk[64], pk2[64];
+  const int tid = threadIdx.x, pi = blockIdx.y;
+  const uint64_t full = a.n >= 64 ? ~0ull : ((1ull << a.n) - 1ull);
   if (tid == 0) {
     const DevCounters& c = *a.ctr;
-    const uint64_t full = a.n >= 64 ? ~0ull : ((1ull << a.n) - 1ull);
     int act = 0;
     unsigned long long t = 0;
     if (c.buckets < a.planned && c.out_count <= a.raw_cap && c.post_count <= a.rows_cap) {
@@ -1282,124 +1319,51 @@ __global__ void piece_plan_kernel(PiecePlanArgs a) {
     }
     s_t = t;
     s_act = act;
-    PieceDesc d;
-    d.t = t;
-    d.mask[0] = t;
-    d.mask[1] = ~t & full;
-    d.ns[0] = __popcll(d.mask[0]);
-    d.ns[1] = __popcll(d.mask[1]);
-    d.active = act;
-    d.pad = 0;
-    *a.desc = d;
-    *a.h_desc = d;
+    if (blockIdx.x == 0 && pi == 0) {
+      PieceDesc d;
+      d.t = t;
+      d.mask[0] = t;
+      d.mask[1] = ~t & full;
+      d.ns[0] = __popcll(d.mask[0]);
+      d.ns[1] = __popcll(d.mask[1]);
+      d.active = act;
+      d.pad = 0;
+      *a.h_desc = d;
+    }
   }
   __syncthreads();
   if (!s_act) return;
-  const uint64_t full = a.n >= 64 ? ~0ull : ((1ull << a.n) - 1ull);
-  const uint64_t t = s_t;
-  for (int i = tid; i < a.n; i += blockDim.x) {  // compact: [piece][keys | keys2][64]
-    const int pi = (t >> i) & 1ull ? 0 : 1;
-    const uint64_t mk = pi ? (~t & full) : t;
-    const int j = __popcll(mk & ((1ull << i) - 1ull));
-    a.pkeys[pi * 128 + j] = a.keys[i];
-    a.pkeys[pi * 128 + 64 + j] = a.keys2[i];
-  }
-}
-
-__global__ void __launch_bounds__(256) piece_search_kernel(const PieceDesc* __restrict__ desc,
-                                                           const uint64_t* __restrict__ pkeys, uint64_t lo,
-                                                           uint64_t width, uint64_t* __restrict__ praw,
-                                                           unsigned long long cap, DevCounters* pctr) {
-  pdl_wait();  // programmatic launch: the previous kernel is complete
-  pdl_trigger();
-  const int pi = blockIdx.y;
-  if (!desc->active) return;
-  const int n = desc->ns[pi];
+  const uint64_t mask = pi ? (~s_t & full) : s_t;
+  const int n = __popcll(mask);
   if (n < 2) return;  // one linear or quadratic entity: irreducible
+  for (int i = tid; i < a.n; i += blockDim.x)  // compact the piece's keys
+    if ((mask >> i) & 1ull) {
+      const int j = __popcll(mask & ((1ull << i) - 1ull));
+      pk[j] = a.keys[i];
+      pk2[j] = a.keys2[i];
+    }
+  __syncthreads();
   const int m = n - 1;
   int b = table_bits(m);
   if (b > m) b = m;
   const int h = m - b;
   const int g = h > 16 ? h - 16 : 0;
-  table_search_body(pkeys + pi * 128, n, lo, width, b, g, praw + (size_t)pi * cap, cap, pctr + pi,
-                    blockIdx.x);
-}
-
-// Tr3 window over a piece's raw hits, then each survivor deposited into the
-// parent's pattern bits (keyfilter_kernel + deposit_kernel for both pieces)
-__global__ void piece_filter_kernel(const PieceDesc* __restrict__ desc, const uint64_t* __restrict__ pkeys,
-                                    const uint64_t* __restrict__ praw, unsigned long long raw_cap,
-                                    uint64_t lo2, uint64_t width2, uint64_t* __restrict__ ppost,
-                                    unsigned long long post_cap, DevCounters* pctr) {
-  pdl_wait();  // programmatic launch: the previous kernel is complete
-  pdl_trigger();
-  const int pi = blockIdx.y;
-  if (!desc->active || desc->ns[pi] < 2) return;
-  __shared__ uint64_t sk[64];
-  const int n = desc->ns[pi];
-  const uint64_t mask = desc->mask[pi];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = pkeys[pi * 128 + 64 + i];
-  __syncthreads();
-  DevCounters* ctr = pctr + pi;
-  unsigned long long m = ctr->out_count;
-  if (m > raw_cap) m = raw_cap;
-  const uint64_t* in = praw + (size_t)pi * raw_cap;
-  uint64_t* out = ppost + (size_t)pi * post_cap;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint64_t t = in[i];
-    uint64_t sum = 0, v = 0, u = t, mm = mask;
-    for (int j = 0; u; j++, u >>= 1, mm &= mm - 1)
-      if (u & 1ull) {
-        sum += sk[j];
-        v |= mm & (0ull - mm);
-      }
-    if (sum - lo2 <= width2) {
-      const unsigned long long k = atomicAdd(&ctr->post_count, 1ull);
-      if (k < post_cap) out[k] = v;
-    }
-  }
-}
-
-__global__ void collect2_kernel(CollectArgs C0, CollectArgs C1) {
-  pdl_wait();  // programmatic launch: the previous kernel is complete
-  pdl_trigger();
-  const CollectArgs& C = blockIdx.x ? C1 : C0;
-  const unsigned long long cnt = C.ctr->post_count;
-  const unsigned rows = (unsigned)(cnt < C.rows ? cnt : C.rows);
-  const int t = threadIdx.x;
-  if (t < (int)(sizeof(DevCounters) / 8))
-    ((unsigned long long*)C.h_ctr)[t] = ((const unsigned long long*)C.ctr)[t];
-  for (unsigned k = t; k < rows; k += blockDim.x) {
-    C.h_pats[k] = C.pats[k];
-    C.h_verdict[k] = C.verdict[k];
-    C.h_side[k] = C.side[k];
-  }
-  const unsigned nco = rows * (unsigned)C.stride;
-  for (unsigned k = t; k < nco; k += blockDim.x) C.h_coeffs[k] = C.coeffs[k];
+  table_search_body(pk, n, lo, width, b, g, a.pctr, blockIdx.x,
+                    PieceEmit{a.pctr, pk2, mask, lo2, width2, a.ppost, post_cap});
 }
 
 cudaError_t launch_pieces(const PiecePlanArgs& a, uint64_t lo, uint64_t width, uint64_t lo2, uint64_t width2,
-                          uint64_t* praw, unsigned long long raw_cap, uint64_t* ppost,
-                          unsigned long long post_cap, const struct VerifyArgs* V, const CollectArgs* C,
-                          int nsm, cudaStream_t s) {
-  cudaError_t e = launch_pdl(piece_plan_kernel, dim3(1), dim3(64), 0, s, a);
-  if (e != cudaSuccess) return e;
+                          unsigned long long post_cap, const VerifyArgs& V, const CollectArgs& C,
+                          cudaStream_t s) {
   static uint64_t attr_done = 0;
-  e = raise_smem_limit(piece_search_kernel, (size_t)10 << kTableMaxBits, attr_done);
+  cudaError_t e = raise_smem_limit(piece_kernel, (size_t)10 << kTableMaxBits, attr_done);
   if (e != cudaSuccess) return e;
   // <= 2^16 threads per piece (n <= kExhaustiveMaxN: b = 8, h <= 22, g = h - 16)
-  e = launch_pdl(piece_search_kernel, dim3(256, 2), dim3(256), (size_t)10 << 8, s, (const PieceDesc*)a.desc,
-                 (const uint64_t*)a.pkeys, lo, width, praw, raw_cap, a.pctr);
+  e = launch_pdl(piece_kernel, dim3(256, 2), dim3(256), (size_t)10 << 8, s, a, lo, width, lo2, width2,
+                 post_cap);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(piece_filter_kernel, dim3(nsm, 2), dim3(256), 0, s, (const PieceDesc*)a.desc,
-                 (const uint64_t*)a.pkeys, (const uint64_t*)praw, raw_cap, lo2, width2, ppost, post_cap, a.pctr);
-  if (e != cudaSuccess) return e;
-  for (int pi = 0; pi < 2; pi++)
-    if ((e = launch_verify(V[pi], s)) != cudaSuccess) return e;
-  e = launch_pdl(collect2_kernel, dim3(2), dim3(256), 0, s, C[0], C[1]);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  if ((e = launch_verify(V, s)) != cudaSuccess) return e;
+  return launch_collect(C, s);
 }
 
 // ---------------------------------------------------------- early exit
