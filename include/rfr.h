@@ -238,6 +238,10 @@ int rfr_peer_disconnect(void);
 
 /* The three primes of the modular division test (p_mod residues). */
 int rfr_verify_primes(uint64_t* primes3);
+/* p's coefficients modulo those three primes (the p_mod argument of
+ * rfr_verify / rfr_search_verify, 3 x (d+1), Python's sign rule) from
+ * signed 64-bit coefficients; RFR_E_ARG when some |c| >= 2^62. */
+int rfr_p_mod_i64(const int64_t* coeffs, int d, uint64_t* p_mod);
 
 /* ---- host-side numerics (native, not timed) ------------------------------ */
 /*

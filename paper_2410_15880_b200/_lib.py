@@ -43,6 +43,7 @@ EXPORTS = (
     "rfr_squarefree_mod",
     "rfr_squarefree_i64",
     "rfr_divide_monic_i64",
+    "rfr_p_mod_i64",
 )
 
 
@@ -155,17 +156,21 @@ def load():
             ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int64, U64_P, ctypes.c_int, U8_P, U8_P,
             I64_P, ctypes.c_int, ctypes.POINTER(RfrStats),
         ]
+        # array arguments as void*: raw addresses (int) are the cheapest to pass
+        # per call; ctypes pointer instances are accepted as well
+        VP = ctypes.c_void_p
         L.rfr_search_verify.argtypes = [
-            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
-            ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
-            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, I64_P, ctypes.POINTER(RfrStats),
+            VP, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, VP, ctypes.c_uint64,
+            ctypes.c_uint64, ctypes.POINTER(RfrProfile), VP, ctypes.c_int, VP, VP, VP,
+            VP, ctypes.c_int, ctypes.c_int64, ctypes.c_int, I64_P, ctypes.POINTER(RfrStats),
         ]
         L.rfr_search_verify_shard.argtypes = [
-            U64_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, U64_P, ctypes.c_uint64,
-            ctypes.c_uint64, ctypes.POINTER(RfrProfile), U64_P, ctypes.c_int, U64_P, U8_P, U8_P,
-            I64_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            VP, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, VP, ctypes.c_uint64,
+            ctypes.c_uint64, ctypes.POINTER(RfrProfile), VP, ctypes.c_int, VP, VP, VP,
+            VP, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_uint64, I64_P, ctypes.POINTER(RfrStats),
         ]
+        L.rfr_p_mod_i64.argtypes = [VP, ctypes.c_int, VP]
         L.rfr_peer_handle.argtypes = [ctypes.c_void_p]
         L.rfr_peer_connect.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.rfr_peer_disconnect.argtypes = []

@@ -1440,6 +1440,21 @@ int rfr_verify_primes(uint64_t* primes3) {
   return RFR_OK;
 }
 
+int rfr_p_mod_i64(const int64_t* coeffs, int d, uint64_t* p_mod) {
+  if (!coeffs || !p_mod || d < 0) return rfr_fail(RFR_E_ARG, "bad p_mod arguments");
+  const int64_t lim = (int64_t)1 << 62;
+  for (int k = 0; k <= d; k++)
+    if (coeffs[k] >= lim || coeffs[k] <= -lim) return rfr_fail(RFR_E_ARG, "coefficient beyond 2^62");
+  for (int i = 0; i < 3; i++) {
+    const int64_t q = (int64_t)kVerifyPrimes[i];
+    for (int k = 0; k <= d; k++) {
+      const int64_t r = coeffs[k] % q;
+      p_mod[(size_t)i * (d + 1) + k] = (uint64_t)(r < 0 ? r + q : r);
+    }
+  }
+  return RFR_OK;
+}
+
 int rfr_verify(const rfr_profile* prof, const uint64_t* pats, int64_t m, const uint64_t* p_mod,
                int d, uint8_t* verdict, uint8_t* side, int64_t* coeffs, int stride,
                rfr_stats* st) {

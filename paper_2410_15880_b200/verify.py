@@ -32,6 +32,8 @@ from dataclasses import dataclass, field
 from fractions import Fraction
 from functools import lru_cache
 
+from array import array as _array
+
 import numpy as np
 
 from . import _lib
@@ -166,9 +168,14 @@ def _p_mod(p: IntPolynomial) -> np.ndarray:
         _PRIMES = tuple(int(q) for q in primes)
         _PRIMES_I64 = primes.astype(np.int64)
     co = p.coeffs
-    if max(co) < (1 << 62) and min(co) > -(1 << 62):  # int64 fast path (Python sign rule)
-        a = np.array(co, dtype=np.int64)
-        return np.remainder(a[None, :], _PRIMES_I64[:, None]).astype(np.uint64)
+    try:  # int64 coefficients: reduced natively (rfr_p_mod_i64; Python's sign rule)
+        a = _array("q", co)
+    except OverflowError:
+        a = None
+    if a is not None:
+        out = np.empty((3, len(co)), dtype=np.uint64)
+        if _lib.load().rfr_p_mod_i64(a.buffer_info()[0], len(co) - 1, out.ctypes.data) == 0:
+            return out
     return np.array([[c % q for c in co] for q in _PRIMES], dtype=np.uint64)
 
 
@@ -263,16 +270,11 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
     pm = np.ascontiguousarray(_p_mod(p))
     cap = 1 << 12  # a regrow reruns the whole search: start where the survivors fit
     while True:
-        pats = np.empty(cap, dtype=np.uint64)
-        verdict = np.empty(cap, dtype=np.uint8)
-        side = np.empty(cap, dtype=np.uint8)
-        coeffs = np.empty((cap, _STRIDE), dtype=np.int64)
+        pats, verdict, side, coeffs, addr = _out_buffers(cap)
         nout = ctypes.c_int64(0)
         st = _lib.RfrStats()
-        args = (_lib.ptr(keys, _lib.U64_P), n, lo, width, _lib.ptr(keys3, _lib.U64_P), lo2, width2,
-                ctypes.byref(rp), _lib.ptr(pm, _lib.U64_P), p.degree, _lib.ptr(pats, _lib.U64_P),
-                verdict.ctypes.data_as(_lib.U8_P), side.ctypes.data_as(_lib.U8_P),
-                coeffs.ctypes.data_as(_lib.I64_P), _STRIDE, cap,
+        args = (keys.ctypes.data, n, lo, width, keys3.ctypes.data, lo2, width2,
+                ctypes.byref(rp), pm.ctypes.data, p.degree, *addr, _STRIDE, cap,
                 (1 if _PIECES else 2) if early_exit else 0)
         if nshards > 1:
             rc = lib.rfr_search_verify_shard(*args, shard, nshards, epoch, ctypes.byref(nout),
@@ -288,7 +290,30 @@ def _search_and_verify(prof: RootProfile, p: IntPolynomial, keys: np.ndarray, ha
     _fill_stats(stats, st)
     m = int(nout.value)
     complete = st.buckets >= st.buckets_planned
-    return pats[:m], verdict[:m], side[:m], coeffs[:m], complete, bool(st.early_stop)
+    # copies: the buffers are reused by the next call (the recursion on the
+    # pieces makes one while the caller still holds these rows)
+    return (pats[:m].copy(), verdict[:m].copy(), side[:m].copy(), coeffs[:m].copy(), complete,
+            bool(st.early_stop))
+
+
+_OUT: dict = {}
+
+
+def _out_buffers(cap: int):
+    """Result buffers of rfr_search_verify for cap rows (pats, verdict, side,
+    coefficients) and their addresses, kept for reuse across calls."""
+    b = _OUT.get(cap)
+    if b is None:
+        pats = np.empty(cap, dtype=np.uint64)
+        verdict = np.empty(cap, dtype=np.uint8)
+        side = np.empty(cap, dtype=np.uint8)
+        coeffs = np.empty((cap, _STRIDE), dtype=np.int64)
+        b = (pats, verdict, side, coeffs,
+             (pats.ctypes.data, verdict.ctypes.data, side.ctypes.data, coeffs.ctypes.data))
+        if len(_OUT) > 8:
+            _OUT.clear()
+        _OUT[cap] = b
+    return b
 
 
 def _sub_profile(prof: RootProfile, t: int) -> RootProfile:
