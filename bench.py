@@ -320,6 +320,9 @@ def run_ours(args):
         h2d += 8 * prof.n + 8 * (2 * prof.r + 4 * prof.c) + 4 * prof.n + 8 * m + 24 * (p.degree + 1)
         d2h += 8 + 8 * m + 2 * m + 8 * 65 * m
     e2e = float(np.mean(e2e_times)) if e2e_times else float("nan")
+    if os.environ.get("RFR_BENCH_DUMP"):  # diagnostics: the per-step times
+        print("e2e steps ms", [round(x, 3) for x in e2e_times], file=sys.stderr)
+        print("value steps ms", [round(x, 3) for x in times], file=sys.stderr)
     if dist is not None:  # max over ranks, as for the device-timed value
         tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
