@@ -181,12 +181,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RFR_BENCH_ONE_GPU=1 (a dry run of the N-rank code on a one-GPU box: every
+    # rank on cuda:0, gloo instead of NCCL; not a measurement)
+    one_gpu = os.environ.get("RFR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+        os.environ["RFR_DEVICE"] = "0"
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
     _lib.device()
 
@@ -395,7 +404,8 @@ def run_ours(args):
 
     join_ms = float(np.mean(joins))
     list_ms = float(np.mean(lists))
-    alg = float(np.mean([algorithmic_bytes(n) for n in ns]))
+    # per join launch: this rank's key-range shard of the records (1/N of them)
+    alg = float(np.mean([algorithmic_bytes(n) for n in ns])) / world
     peak, peak_kind = peaks()
     spec = 8000.0  # GB/s, the north star's "~8 TB/s"
     achieved = alg / (join_ms * 1e-3) / 1e9
