@@ -113,13 +113,81 @@ def frac(x: float) -> float:
 
 
 # ------------------------------------------------------------ hp roots
-def _dd_split(v: Fraction) -> tuple[float, float]:
+class _Dy:
+    """Exact dyadic rational m * 2^e (m, e ints): the entity arithmetic of
+    hp_profile (sums, products, halves of double-double values) without
+    Fraction's gcd normalisation -- the same exact values, ~10x faster."""
+
+    __slots__ = ("m", "e")
+
+    def __init__(self, m: int, e: int):
+        self.m, self.e = m, e
+
+    @staticmethod
+    def of(x) -> "_Dy":
+        if isinstance(x, _Dy):
+            return x
+        if isinstance(x, int):
+            return _Dy(x, 0)
+        n, d = float(x).as_integer_ratio()
+        return _Dy(n, 1 - d.bit_length())  # d is a power of two
+
+    def __add__(self, o):
+        o = _Dy.of(o)
+        if self.e <= o.e:
+            return _Dy(self.m + (o.m << (o.e - self.e)), self.e)
+        return _Dy((self.m << (self.e - o.e)) + o.m, o.e)
+
+    __radd__ = __add__
+
+    def __neg__(self):
+        return _Dy(-self.m, self.e)
+
+    def __sub__(self, o):
+        return self + (-_Dy.of(o))
+
+    def __rsub__(self, o):
+        return _Dy.of(o) + (-self)
+
+    def __mul__(self, o):
+        o = _Dy.of(o)
+        return _Dy(self.m * o.m, self.e + o.e)
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, k: int):
+        if k != 2:
+            raise ValueError("dyadic division by 2 only")
+        return _Dy(self.m, self.e - 1)
+
+    def __floor__(self) -> int:
+        return self.m >> -self.e if self.e < 0 else self.m << self.e
+
+    def __float__(self) -> float:
+        return math.ldexp(float(self.m), self.e)  # m rounded once: correctly rounded
+
+    def __abs__(self):
+        return _Dy(abs(self.m), self.e)
+
+
+def _key64(x) -> int:
+    """floor(frac(x) 2^64 + 1/2) mod 2^64, exactly (= floor(x 2^64 + 1/2) mod 2^64)."""
+    if isinstance(x, _Dy):
+        s = x.e + 64
+        k = x.m << s if s >= 0 else (x.m + (1 << (-s - 1))) >> (-s)
+        return k & (_TWO64 - 1)
+    return math.floor((x - math.floor(x)) * _TWO64 + Fraction(1, 2)) % _TWO64
+
+
+def _dd_split(v) -> tuple[float, float]:
     hi = float(v)
-    lo = float(v - Fraction(hi))
+    lo = float(v - (_Dy.of(hi) if isinstance(v, _Dy) else Fraction(hi)))
     return hi, lo
 
 
-def _dd_frac(hi: float, lo: float) -> Fraction:
+def _dd_frac(hi: float, lo: float, num=Fraction):
+    if num is _Dy:
+        return _Dy.of(hi) + _Dy.of(lo)
     return Fraction(hi) + Fraction(lo)
 
 
@@ -449,9 +517,13 @@ def _pair_up(re_hi, re_lo, im_hi, im_lo, err):
     return reals, pairs
 
 
-def hp_profile(p: IntPolynomial) -> RootProfile:
+def hp_profile(p: IntPolynomial, num=None) -> RootProfile:
     """High-precision profile of a monic square-free p: rho, perm, double-
-    double entities, the 64-bit keys in rho order and their error bounds."""
+    double entities, the 64-bit keys in rho order and their error bounds.
+    The entity values are exact rationals of the double-double roots: dyadic
+    (_Dy, the default) or Fraction (num=Fraction: the same values, slower;
+    tests/test_rootfinder.py checks the two agree field by field)."""
+    num = num or _Dy
     re_hi, re_lo, im_hi, im_lo, err, exact = _hp_roots(p)
     reals, pairs = _pair_up(re_hi, re_lo, im_hi, im_lo, err)
     # (kind, R = first power sum, tau = second, errR, errTau, data, p3 = third, errP3)
@@ -460,7 +532,7 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
     # exact rationals of the double-double values
     for i in reals:
         ex_vals.append(exact[i][0] if exact is not None else None)
-        u = _dd_frac(re_hi[i], re_lo[i])
+        u = _dd_frac(re_hi[i], re_lo[i], num)
         du = float(err[i])
         au = abs(float(u))
         ents.append(("r", u, u * u, du, 2 * au * du + du * du, i, u * u * u,
@@ -473,8 +545,8 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         else:
             ex_vals.append(None)
         # symmetrise: z = (z_a + conj z_b) / 2
-        re = (_dd_frac(re_hi[a], re_lo[a]) + _dd_frac(re_hi[b], re_lo[b])) / 2
-        im = (_dd_frac(im_hi[a], im_lo[a]) - _dd_frac(im_hi[b], im_lo[b])) / 2
+        re = (_dd_frac(re_hi[a], re_lo[a], num) + _dd_frac(re_hi[b], re_lo[b], num)) / 2
+        im = (_dd_frac(im_hi[a], im_lo[a], num) - _dd_frac(im_hi[b], im_lo[b], num)) / 2
         dz = float(max(err[a], err[b]))
         t = 2 * re
         m = re * re + im * im
@@ -524,9 +596,9 @@ def hp_profile(p: IntPolynomial) -> RootProfile:
         rho_k, kind, R, tau, dR, dtau, _, p3, dp3 = rows[k]
         rho.append(rho_k)
         perm.append(ent_of[k])
-        keys1.append(math.floor((R - math.floor(R)) * _TWO64 + Fraction(1, 2)) % _TWO64)
-        keys2.append(math.floor((tau - math.floor(tau)) * _TWO64 + Fraction(1, 2)) % _TWO64)
-        keys3.append(math.floor((p3 - math.floor(p3)) * _TWO64 + Fraction(1, 2)) % _TWO64)
+        keys1.append(_key64(R))
+        keys2.append(_key64(tau))
+        keys3.append(_key64(p3))
         e1 += dR * 2.0**64 + 1.0
         e2 += dtau * 2.0**64 + 1.0
         e3 += dp3 * 2.0**64 + 1.0

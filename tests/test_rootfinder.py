@@ -195,3 +195,36 @@ def test_inclusion_discs_multiprecision_path():
     for q in (2**61 - 1, 2**31 - 1, 1000003, 999983, 104729, 7919, 541, 97):
         p = p * P([-q, 0, 1])
     _check_discs(p)
+
+
+def test_dyadic_entity_arithmetic_matches_fractions(big_inputs):
+    """hp_profile's entity values are exact dyadic rationals (_Dy); computed
+    with Fraction instead, every field of the profile (double-double
+    entities, rho, keys, key error bounds) is the same."""
+    import random
+    from fractions import Fraction
+
+    from conftest import poly_of
+    from paper_2410_15880_b200 import IntPolynomial
+    from paper_2410_15880_b200.rootfinder import hp_profile
+
+    polys = [poly_of(c["p"]) for c in big_inputs["c3"][:2]] + [poly_of(big_inputs["c4"][0]["p"])]
+    rng = random.Random(9)
+    for _ in range(12):
+        d = rng.randint(5, 50)
+        polys.append(IntPolynomial([rng.randint(-40, 40) for _ in range(d)] + [1]))
+    checked = 0
+    for p in polys:
+        try:
+            a = hp_profile(p)
+        except Exception:
+            continue
+        b = hp_profile(p, num=Fraction)
+        for f in ("real_roots", "pair_sums", "pair_products", "rho", "real_lo", "sum_lo", "prod_lo",
+                  "keys1", "keys2", "keys3"):
+            assert np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(b, f))), f
+        for f in ("perm", "key_err1", "key_err2", "key_err3", "root_err"):
+            assert getattr(a, f) == getattr(b, f), f
+        checked += 1
+    assert checked >= 10
+
