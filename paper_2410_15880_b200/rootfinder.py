@@ -164,7 +164,14 @@ class _Dy:
         return self.m >> -self.e if self.e < 0 else self.m << self.e
 
     def __float__(self) -> float:
-        return math.ldexp(float(self.m), self.e)  # m rounded once: correctly rounded
+        m, e = self.m, self.e
+        b = abs(m).bit_length()
+        if b > 64:  # keep 64 bits and a sticky bit: float() then still rounds correctly
+            k = b - 64
+            a = abs(m)
+            t = (a >> k) | (1 if a & ((1 << k) - 1) else 0)
+            m, e = (t if m > 0 else -t), e + k
+        return math.ldexp(float(m), e)  # m rounded once: correctly rounded
 
     def __abs__(self):
         return _Dy(abs(self.m), self.e)

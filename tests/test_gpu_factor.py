@@ -548,7 +548,7 @@ def _structured_product(seed0, case):
 # structured-sweep faults: 2^35 hits from 35 integer roots (1/9), a Tr3 window
 # that dropped a factor with 10^6 coefficients (2/39), a Wilkinson-like
 # product whose polish did not converge (5/39)
-@pytest.mark.parametrize("seed0,case", [(1, 9), (2, 39), (5, 39), (3, 0)])
+@pytest.mark.parametrize("seed0,case", [(1, 9), (2, 39), (5, 39), (3, 0), (42001, 3), (42001, 127)])
 def test_structured_regressions_match_sympy(seed0, case):
     mode, p, want = _structured_product(seed0, case)
     if p.degree > 128:

@@ -228,3 +228,23 @@ def test_dyadic_entity_arithmetic_matches_fractions(big_inputs):
         checked += 1
     assert checked >= 10
 
+
+def test_dyadic_float_is_correctly_rounded_for_wide_mantissas():
+    """_Dy -> float is Fraction's correctly rounded value also when the
+    mantissa is far wider than a double (a double-double whose low part is
+    ~2^-900 below the high part: a 1000-bit mantissa), and for its powers."""
+    import random
+    from fractions import Fraction
+
+    from paper_2410_15880_b200.rootfinder import _Dy
+
+    rng = random.Random(1)
+    for _ in range(3000):
+        hi = rng.uniform(-1e6, 1e6) * 2.0 ** rng.randint(-60, 60)
+        lo = hi * 2.0 ** -53 * rng.uniform(-1, 1) * 2.0 ** -rng.randint(0, 900)
+        d = _Dy.of(hi) + _Dy.of(lo)
+        f = Fraction(hi) + Fraction(lo)
+        assert float(d) == float(f)
+        assert float(d * d * d) == float(f * f * f)
+        assert float(d - 3 * d * d) == float(f - 3 * f * f)
+
