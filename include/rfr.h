@@ -280,6 +280,14 @@ int rfr_squarefree_i64(const int64_t* coeffs, int d, uint64_t q);
  * big-integer path).
  */
 int rfr_divide_monic_i64(const int64_t* p, int dp, const int64_t* q, int dq, int64_t* r);
+/*
+ * Exact product of two polynomials with int64 coefficients (R/polynomial.py:
+ * 142-152), accumulated in 128-bit integers: 1 with out (da + db + 1
+ * entries) filled, -1 when a product coefficient reaches 2^62 or the
+ * operands are too large to accumulate safely ((min(da, db) + 1) max|a|
+ * max|b| >= 2^126); the caller then takes its big-integer path.
+ */
+int rfr_multiply_i64(const int64_t* a, int da, const int64_t* b, int db, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -44,6 +44,7 @@ EXPORTS = (
     "rfr_squarefree_i64",
     "rfr_divide_monic_i64",
     "rfr_p_mod_i64",
+    "rfr_multiply_i64",
 )
 
 
@@ -171,6 +172,8 @@ def load():
             ctypes.c_uint64, I64_P, ctypes.POINTER(RfrStats),
         ]
         L.rfr_p_mod_i64.argtypes = [VP, ctypes.c_int, VP]
+        L.rfr_multiply_i64.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.c_void_p]
         L.rfr_peer_handle.argtypes = [ctypes.c_void_p]
         L.rfr_peer_connect.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.rfr_peer_disconnect.argtypes = []

@@ -339,6 +339,33 @@ static int squarefree_euclid_fp(const uint64_t* cm, int d, uint64_t q64) {
 }
 }  // extern "C++"
 
+int rfr_multiply_i64(const int64_t* a, int da, const int64_t* b, int db, int64_t* out) {
+  if (da < 0 || db < 0) return -1;
+  // every partial sum of a coefficient is at most (min(da, db) + 1) max|a| max|b|:
+  // keep that below 2^126 so the 128-bit accumulation cannot wrap
+  unsigned __int128 ma = 0, mb = 0;
+  for (int i = 0; i <= da; i++) {
+    const unsigned __int128 v = a[i] < 0 ? (unsigned __int128)(-(__int128)a[i]) : (unsigned __int128)a[i];
+    if (v > ma) ma = v;
+  }
+  for (int i = 0; i <= db; i++) {
+    const unsigned __int128 v = b[i] < 0 ? (unsigned __int128)(-(__int128)b[i]) : (unsigned __int128)b[i];
+    if (v > mb) mb = v;
+  }
+  const unsigned __int128 terms = (unsigned __int128)((da < db ? da : db) + 1);
+  const unsigned __int128 cap = (unsigned __int128)1 << 126;
+  if (ma && mb && (ma > cap / mb || ma * mb > cap / terms)) return -1;
+  const __int128 lim = (__int128)1 << 62;
+  for (int k = 0; k <= da + db; k++) {
+    __int128 acc = 0;
+    const int i0 = k > db ? k - db : 0, i1 = k < da ? k : da;
+    for (int i = i0; i <= i1; i++) acc += (__int128)a[i] * b[k - i];
+    if (acc >= lim || acc <= -lim) return -1;
+    out[k] = (int64_t)acc;
+  }
+  return 1;
+}
+
 int rfr_divide_monic_i64(const int64_t* p, int dp, const int64_t* q, int dq, int64_t* r) {
   if (dq < 0 || dp < dq || q[dq] != 1) return -1;
   const int64_t p_lim = (int64_t)1 << 62, q_lim = (int64_t)1 << 31;
