@@ -308,7 +308,7 @@ static int squarefree_euclid(const uint64_t* cm, int d, uint64_t q, const Red R)
 // brings it back: branch-free, so the update loops vectorise (AVX2: 34 -> ~8
 // us at d = 100).  A residue is zero iff its representative is 0.0.
 static inline double red_fp(double x, double q, double qinv) { return x - std::rint(x * qinv) * q; }
-__attribute__((target_clones("avx2", "default")))
+__attribute__((target_clones("avx512f", "avx2", "default")))
 static int squarefree_euclid_fp(const uint64_t* cm, int d, uint64_t q64) {
   const double q = (double)q64, qinv = 1.0 / q;
   std::vector<double> a(d + 1), b(d);
