@@ -104,6 +104,12 @@ def _degree_masks(perm: tuple, r: int) -> tuple[int, int]:
     return real, sum(1 << i for i in range(len(perm))) & ~real
 
 
+# inputs whose profile was found without splitting integer roots off first:
+# the next call skips that screen (a stale entry only costs the polish's own
+# NonConvergence fallback, which splits them then)
+_PROFILED: set = set()
+
+
 @lru_cache(maxsize=256)
 def _profile_cached(coeffs: tuple) -> RootProfile:
     return hp_profile(IntPolynomial(coeffs))
@@ -641,10 +647,14 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
         # integer roots make the polish ill-conditioned (a Wilkinson-like
         # product of 39 of them did not converge): split them off exactly
         # before the multiprecision polish, and as a fallback if it fails
-        ints = _integer_roots(p, scan=False) if _coeff_bits(p) > 100 else []
+        ints = ([] if p.coeffs in _PROFILED
+                else _integer_roots(p, scan=False) if _coeff_bits(p) > 100 else [])
         if not ints:
             try:
                 prof = _profile_cached(p.coeffs)
+                if len(_PROFILED) > 4096:
+                    _PROFILED.clear()
+                _PROFILED.add(p.coeffs)  # profiled without an integer-root split
             except NonConvergence:
                 ints = _integer_roots(p, scan=True)
                 if not ints:
@@ -705,7 +715,8 @@ def _factor_monic_squarefree(p: IntPolynomial, cfg: ToleranceConfig, workers: in
             pats, verdict, side, coeffs, complete, stopped = search(None)
         stats.early_exits += int(stopped and complete)  # stopped, pieces searched in the call
         keep = pats != 0
-        pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]
+        if not keep.all():  # the empty pattern, when it is a row
+            pats, verdict, side, coeffs = pats[keep], verdict[keep], side[keep], coeffs[keep]
         stats.recombine_seconds += time.perf_counter() - t0
         stats.candidates += len(pats)
         t0 = time.perf_counter()
