@@ -554,10 +554,11 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
 // (off = 32 * nch).  Same record semantics as window_pass.
 constexpr int kMaxCh = kJoinWarps > 8 ? 6 : 12;  // chunks of one run in flight
 // chunk counts of runs of lambda = 256, 128 and 64 records per outer per
-// bucket (ceil((lambda + 3 sqrt(lambda) + 8) / 32)), compiled as their own
+// bucket (ceil((lambda + 2 sqrt(lambda) + 8) / 32): a run longer than that,
+// ~2 % of them, is finished by continue_pass), compiled as their own
 // run_pass instances: the default plan runs 128 on both sides, sharded plans
 // 64, RFR_LAMBDA_LOG=8 256
-constexpr int kNch256 = 10, kNch128 = 6, kNch64 = 3;
+constexpr int kNch256 = 10, kNch128 = 5, kNch64 = 3;
 // SMALLH: halo below 2^32 (factor-mode windows) and W = 2^sh with sh >= 32,
 // so "in bucket" and "in halo" are 32-bit tests on the high / low words.
 // 32-bit bucket/halo classification in the run pass (SMALLH): the halo fits

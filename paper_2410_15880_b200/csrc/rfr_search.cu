@@ -883,7 +883,7 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
     int run_log = inner_bits - P.r;  // log2 expected records per outer per bucket
     if (run_log >= 5) {
       const double lam = std::ldexp(1.0, run_log);
-      int nch = (int)std::ceil((lam + 3.0 * std::sqrt(lam) + 8.0) / 32.0);
+      int nch = (int)std::ceil((lam + 2.0 * std::sqrt(lam) + 8.0) / 32.0);
       if (nch > kMaxCh) nch = kMaxCh;  // longer runs continue in continue_pass
       return 32 * nch;
     }
