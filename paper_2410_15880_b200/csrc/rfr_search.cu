@@ -877,7 +877,7 @@ cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,
   // lane groups: about twice the expected run of one outer in one bucket
   // Lanes per outer window: a lane group of 2 * lambda lanes for short runs
   // (lambda = expected records per outer per bucket); for lambda >= 32 the
-  // warp-wide run pass with ceil((lambda + 3 sqrt(lambda) + 8) / 32) chunks
+  // warp-wide run pass with ceil((lambda + 2 sqrt(lambda) + 8) / 32) chunks
   // (encoded as gs = 32 * chunks > 32).
   auto gs_for = [&](int inner_bits) {
     int run_log = inner_bits - P.r;  // log2 expected records per outer per bucket

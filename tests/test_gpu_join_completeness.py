@@ -49,7 +49,10 @@ def _check(keys, T, monkeypatch, lo_hits, hi_hits):
     return len(ex)
 
 
-@pytest.mark.parametrize("n,hits", [(30, 3000), (34, 20000), (38, 60000), (40, 1000)])
+@pytest.mark.parametrize("n,hits", [(30, 3000), (34, 20000), (38, 60000), (40, 1000),
+                                    # factor-mode windows (T <= 2^31: the 32-bit classification
+                                    # and the batched B probe of the production run pass)
+                                    (38, 32), (40, 128)])
 def test_join_equals_exhaustive_random_keys(n, hits, monkeypatch):
     rng = np.random.default_rng(1000 + n)
     keys = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
