@@ -412,15 +412,30 @@ __global__ void __launch_bounds__(kMergeThreads) lists_merge_kernel(const uint64
 #pragma unroll
   for (int t = 0; t < kMergeItems; t++) {
     const bool takeA = j >= nb || (i < na && ka <= kb);
-    if (takeA) {
-      ok[t] = ka;
-      i++;
-      ka = i < na ? LA(i) : kInf;
+    if (kTma) {
+      if (takeA) {
+        ok[t] = ka;
+        i++;
+        ka = i < na ? LA(i) : kInf;
+      } else {
+        ok[t] = kb;
+        from_b |= 1u << t;
+        j++;
+        kb = j < nb ? LB(j) : kInf;
+      }
     } else {
-      ok[t] = kb;
-      from_b |= 1u << t;
-      j++;
-      kb = j < nb ? LB(j) : kInf;
+      // branch-free: the lanes of a warp take A or B at random, so a branch
+      // here runs both sides for every output; the staged tile holds the A
+      // run at [0, na) and the B' run at [na, tile), so the new head is one
+      // predicated shared load at a selected slot
+      ok[t] = takeA ? ka : kb;
+      from_b |= (takeA ? 0u : 1u) << t;
+      i += takeA ? 1u : 0u;
+      j += takeA ? 0u : 1u;
+      const bool more = takeA ? i < na : j < nb;
+      const uint64_t nv = more ? sK[kswz(takeA ? i : na + j)] : kInf;
+      ka = takeA ? nv : ka;
+      kb = takeA ? kb : nv;
     }
   }
   // each thread's run of outputs is contiguous and 64-byte aligned: store it
