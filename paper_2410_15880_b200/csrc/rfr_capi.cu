@@ -316,12 +316,7 @@ int search_core(const uint64_t* d_keys, int n, uint64_t lo, uint64_t width, int 
     RFR_CUDA_OK(cudaMemsetAsync(d_out, 0xff, cap * sizeof(uint64_t), g.stream2));
     RFR_CUDA_OK(cudaEventRecord(g.ev_fill, g.stream2));
   }
-  {
-    int maxbits = 0;
-    for (int i = 0; i < 4; i++) maxbits = P0.list[i].bits > maxbits ? P0.list[i].bits : maxbits;
-    const int per_level = getenv("RFR_SPLIT_KERNEL") ? 2 : 1;  // split + merge, or the merge alone
-    g_launches += 1 + (maxbits > kBaseBits ? per_level * (maxbits - kBaseBits) : 0);
-  }
+  g_launches += lists_launch_count(P0);
   if (time_it) RFR_CUDA_OK(cudaEventRecord(g.ev[1], s));
   for (auto& w : wins) {
     // every piece reuses the geometry planned for the widest (first) piece

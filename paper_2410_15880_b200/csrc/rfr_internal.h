@@ -7,6 +7,7 @@
 namespace rfr {
 size_t list_hist_bytes(int bits);
 ListHist list_hist_layout(const JoinPlan& P, char* const base[4]);
+int lists_launch_count(const JoinPlan& P);  // kernels launch_lists enqueues for this plan
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
                          uint32_t* d_rot, ListHist H, cudaStream_t s);
 cudaError_t launch_join(const JoinPlan& P, const ListBufs& fin, uint64_t* d_out,

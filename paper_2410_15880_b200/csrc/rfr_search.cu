@@ -810,6 +810,34 @@ ListHist list_hist_layout(const JoinPlan& P, char* const base[4]) {
   return H;
 }
 
+// Levels of at least this many merge tiles get their merge-path splits from
+// a separate split kernel (one warp per tile boundary, all searched at once)
+// instead of from two warps of every merge CTA, whose six other warps wait at
+// the barrier for that dependent chain of global loads (28 % of the stall
+// samples of the top level, profiles/r2n_merge_top_source.txt); the small
+// levels keep the single launch.  RFR_SPLIT_MIN_TILES overrides (0: every
+// level; RFR_SPLIT_KERNEL=1 is the same).
+unsigned int split_kernel_min_tiles() {
+  static long v = -2;
+  if (v == -2) {
+    const char* e = getenv("RFR_SPLIT_MIN_TILES");
+    v = e ? atol(e) : (getenv("RFR_SPLIT_KERNEL") ? 0 : 1024);
+    if (v < 0) v = 0;
+  }
+  return (unsigned int)(v > 0xffffffffL ? 0xffffffffL : v);
+}
+
+int lists_launch_count(const JoinPlan& P) {
+  int maxbits = 0;
+  for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
+  int n = 1;  // the base kernel
+  for (int k = kBaseBits; k < maxbits; k++) {
+    const unsigned int blocks = (unsigned int)(((2ull << k) + kMergeTile - 1) / kMergeTile);
+    n += blocks >= split_kernel_min_tiles() ? 2 : 1;
+  }
+  return n;
+}
+
 cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf0, ListBufs buf1,
                          uint32_t* d_rot, ListHist H, cudaStream_t s) {
   static uint64_t attr_done = 0;
@@ -818,19 +846,18 @@ cudaError_t launch_lists(const uint64_t* d_keys, const JoinPlan& P, ListBufs buf
   lists_base_kernel<<<4, 1024, sizeof(BaseSmem), s>>>(d_keys, P, buf0, d_rot);
   int maxbits = 0;
   for (int i = 0; i < 4; i++) maxbits = P.list[i].bits > maxbits ? P.list[i].bits : maxbits;
-  // RFR_SPLIT_KERNEL=1 (A/B): the separate split kernel before every merge;
   // RFR_MERGE_TMA=0/1: staging by loads + shared stores, or by TMA bulk copies
-  static int split_kernel = -1, tma = -1;
-  if (split_kernel < 0) split_kernel = getenv("RFR_SPLIT_KERNEL") ? 1 : 0;
+  static int tma = -1;
   if (tma < 0) {
     const char* e = getenv("RFR_MERGE_TMA");
     tma = e ? atoi(e) : 0;  // measured slower: off by default
   }
+  const unsigned int split_min = split_kernel_min_tiles();
   for (int k = kBaseBits; k < maxbits; k++) {
     const int parity = (k - kBaseBits) & 1;
     const uint64_t outputs = 2ull << k;
     const unsigned int blocks = (unsigned int)((outputs + kMergeTile - 1) / kMergeTile);
-    if (split_kernel) {
+    if (blocks >= split_min) {
       cudaError_t le = launch_pdl(lists_split_kernel, dim3((blocks + 1 + 7) / 8, 4), dim3(256), 0, s, d_keys, P,
                                   k, parity ? buf1 : buf0, (const uint32_t*)d_rot, H);
       if (le == cudaSuccess)
