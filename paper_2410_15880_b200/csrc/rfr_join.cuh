@@ -25,8 +25,9 @@
 //   B side   the same runs over B (negated, shifted keys); each emitted B
 //            record reads its level-1 home and the record it names and checks
 //            it exactly (the reference's windowed probe, recombine.py:
-//            328-358); records that meet a flagged slot (or span > 2 homes)
-//            are staged and probed at levels 2-3 out of line.
+//            328-358); records that meet a flagged slot (or whose window
+//            reaches a second home) are staged and probed at levels 2-3 out
+//            of line.
 //   Outers whose run outlasts the chunks in flight continue in
 //   continue_pass.  Loop state lives in shared memory and the shared base is
 //   re-derived at each use, so the pass calls (which may clobber every
@@ -47,6 +48,9 @@
 #endif
 #ifndef RFR_JOIN_TRACE
 #define RFR_JOIN_TRACE 0
+#endif
+#ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
+#define RFR_JOIN_ONEHOME 1
 #endif
 
 constexpr int kJoinThreads = kJoinThreadsPerCta;
@@ -517,12 +521,23 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
                                                const JoinK& K, bool e, uint64_t s, bool bghost,
                                                uint32_t ib, uint32_t jb, uint32_t& n_qprobe) {
   const uint64_t rel = s - K.cW;
-  const uint64_t lo_rel = rel >= K.H ? rel - K.H : 0ull;
   const int sh1 = K.sh - kL1Log;
+#if RFR_JOIN_ONEHOME
+  // one level-1 home checked in place; a window that reaches a second home
+  // (rare: 2H against a home of 2^(sh-14), ~2^-20 of the records at C3) is
+  // staged whole for probe_b_wide.  h0 unclamped: a record within H of the
+  // bucket start wraps it to a far home, so hn is huge and it goes wide too.
+  const uint32_t h0 = (uint32_t)((rel - K.H) >> sh1);
+  const uint32_t hn = (uint32_t)((rel + K.H) >> sh1) - h0;
+  const uint32_t m1 = (1u << kL1Log) - 1u;
+  const bool narrow = e && hn == 0;
+#else
+  const uint64_t lo_rel = rel >= K.H ? rel - K.H : 0ull;
   const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
   const uint32_t hn = (uint32_t)((rel + K.H) >> sh1) - h0;
   const uint32_t m1 = (1u << kL1Log) - 1u;
   const bool narrow = e && hn <= 1;  // wide windows go to probe_b_wide whole
+#endif
   const uint32_t e0 = narrow ? (uint32_t)S.t1[h0 & m1] : (uint32_t)kNone;
   const uint32_t r0 = min(e0 & 0x7fffu, (uint32_t)kCapRec - 1u);
   const uint64_t k0 = S.recK[r0];
@@ -531,6 +546,9 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
   n_qprobe += o0 ? 1u : 0u;
   if (hit0) emit_match(a, r0, ib, jb);
   bool deep = o0 && (e0 >> 15);
+#if RFR_JOIN_ONEHOME
+  return (e && hn != 0) ? 2 : (deep ? 1 : 0);
+#endif
   // second home: only when the window crosses a level-1 home boundary (rare
   // for factor-mode windows), so it is taken warp-uniformly
   if (__any_sync(0xffffffffu, narrow && hn == 1)) {
