@@ -53,6 +53,7 @@
 #define RFR_JOIN_ONEHOME 1
 #endif
 
+
 constexpr int kJoinThreads = kJoinThreadsPerCta;
 constexpr int kJoinWarps = kJoinThreads / 32;
 // index levels (slots): 8, 2 and 1/2 slots per expected record
@@ -542,8 +543,8 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
   const uint32_t r0 = min(e0 & 0x7fffu, (uint32_t)kCapRec - 1u);
   const uint64_t k0 = S.recK[r0];
   const bool o0 = e0 != kNone;
-  const bool hit0 = o0 && !(bghost && (k0 - K.cW >= K.W)) && (k0 - s + K.hw <= K.width);
   n_qprobe += o0 ? 1u : 0u;
+  const bool hit0 = o0 && !(bghost && (k0 - K.cW >= K.W)) && (k0 - s + K.hw <= K.width);
   if (hit0) emit_match(a, r0, ib, jb);
   bool deep = o0 && (e0 >> 15);
 #if RFR_JOIN_ONEHOME
@@ -653,11 +654,15 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
           m = q < lim && rel < K.W;
           e = m || (valid && (rel - K.W) < K.H);
         }
-        em = __ballot_sync(FULL, e);
+        // side B needs the kept mask only to skip an empty last chunk and for
+        // the continuation test: the earlier chunks of a run are (almost)
+        // never empty, and an empty one is harmless (every lane predicated off)
+        const bool last = NCH ? k == KM - 1 : k == nch - 1;
+        if (SIDE_A || RFR_JOIN_CHECK || last) em = __ballot_sync(FULL, e);
         if (RFR_JOIN_CHECK && (em & (em + 1u)) != 0u) __trap();
         mcl += m ? 1u : 0u;
         n_stat += e ? 1u : 0u;
-        if (em == 0) {
+        if ((SIDE_A || RFR_JOIN_CHECK || last) && em == 0) {
           // chunk entirely past the run (warp-uniform): nothing to store or probe
         } else if (SIDE_A) {
           const uint32_t ne = __popc(em);
