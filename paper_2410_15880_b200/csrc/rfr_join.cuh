@@ -635,7 +635,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     // once per outer.  A record at o >= Mi wraps to the head of the list and
     // has rel >= 2^64 - cW >= W, so it can be halo but never main.
     const uint32_t lim = Mi - pos;  // o < Mi  <=>  q < lim  (pos <= Mi)
-    uint32_t mcl = 0, nq = 0, em = 0;
+    uint32_t mcl = 0, nq = 0, em = 0, em_prev = 0;
 #pragma unroll
     for (int k = 0; k < KM; k++) {
       if (NCH || k < nch) {
@@ -660,6 +660,9 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
         const bool last = NCH ? k == KM - 1 : k == nch - 1;
         if (SIDE_A || RFR_JOIN_CHECK || last) em = __ballot_sync(FULL, e);
         if (RFR_JOIN_CHECK && (em & (em + 1u)) != 0u) __trap();
+        // ... and a prefix of the whole run: no kept record after a chunk that is not full
+        if (RFR_JOIN_CHECK && k > 0 && em != 0u && em_prev != FULL) __trap();
+        if (RFR_JOIN_CHECK) em_prev = em;
         mcl += m ? 1u : 0u;
         n_stat += e ? 1u : 0u;
         if ((SIDE_A || RFR_JOIN_CHECK || last) && em == 0) {
