@@ -681,17 +681,19 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
           if (NOOVF || !overflow) wfill += ne;
         } else {
           const int deep = probe_b_l1_fast(S, a, K, e, sv, !m, i, j, n_qprobe);
-          const uint32_t dm = __ballot_sync(FULL, deep != 0);
-          if (deep) {
-            const uint32_t kk = nq + __popc(dm & lt_mask);
-            S.qK[wid][kk] = sv;
-            S.qJ[wid][kk] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
-            S.qB[wid][kk] = (uint16_t)i;
-          }
-          nq += __popc(dm);
-          if (nq > (uint32_t)(kStageB - 32)) {  // keep room for one more chunk
-            n_qprobe += process_staged(a, cW, nq);
-            nq = 0;
+          if (__any_sync(FULL, deep != 0)) {  // ~1 chunk in 5 has a flagged-slot record
+            const uint32_t dm = __ballot_sync(FULL, deep != 0);
+            if (deep) {
+              const uint32_t kk = nq + __popc(dm & lt_mask);
+              S.qK[wid][kk] = sv;
+              S.qJ[wid][kk] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
+              S.qB[wid][kk] = (uint16_t)i;
+            }
+            nq += __popc(dm);
+            if (nq > (uint32_t)(kStageB - 32)) {  // keep room for one more chunk
+              n_qprobe += process_staged(a, cW, nq);
+              nq = 0;
+            }
           }
         }
       }
