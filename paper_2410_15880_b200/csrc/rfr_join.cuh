@@ -615,6 +615,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
                                ? a.dbg + 128 + (SIDE_A ? 0 : 64)
                                : nullptr;
   int trn = 0;
+  uint32_t nq = 0;  // staged deep probes, flushed when the staging area fills and after the pass
   for (uint32_t i = lo; i < hi; i++) {
     const uint32_t pos = (SIDE_A ? S.apos : S.bpos)[i];
     const uint32_t rot = (SIDE_A ? S.arot : S.brot)[i];
@@ -635,7 +636,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     // once per outer.  A record at o >= Mi wraps to the head of the list and
     // has rel >= 2^64 - cW >= W, so it can be halo but never main.
     const uint32_t lim = Mi - pos;  // o < Mi  <=>  q < lim  (pos <= Mi)
-    uint32_t mcl = 0, nq = 0, em = 0, em_prev = 0;
+    uint32_t mcl = 0, em = 0, em_prev = 0;
 #pragma unroll
     for (int k = 0; k < KM; k++) {
       if (NCH || k < nch) {
@@ -698,7 +699,6 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
         }
       }
     }
-    if (!SIDE_A && nq) n_qprobe += process_staged(a, cW, nq);
     const uint32_t mc = __reduce_add_sync(FULL, mcl);
     const bool sat = em == FULL && can_cont;  // warp-uniform
     if (lane == 0) (SIDE_A ? S.amain : S.bmain)[i] = mc | (sat ? kFlagCont : 0u);
@@ -711,6 +711,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
       asm volatile("prefetch.global.L2 [%0];" ::"l"(kin + ((rot + q) & (Mi - 1))));
     }
   }
+  if (!SIDE_A && nq) n_qprobe += process_staged(a, cW, nq);
   if (RFR_JOIN_TRACE && tr && trn < 63) tr[trn++] = clock64();
   return PassSt{wfill, n_stat, n_qprobe, overflow, cont};
 }
