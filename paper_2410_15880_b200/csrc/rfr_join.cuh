@@ -49,6 +49,9 @@
 #ifndef RFR_JOIN_TRACE
 #define RFR_JOIN_TRACE 0
 #endif
+#ifndef RFR_INDEX_PRED  // 1: the level-1 read-back stores a lost record with predicated stores
+#define RFR_INDEX_PRED 1
+#endif
 #ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
 #define RFR_JOIN_ONEHOME 1
 #endif
@@ -746,12 +749,35 @@ __device__ __noinline__ void build_index_levels() {
       const uint32_t r = wid * kPart + e;
       const bool lost = e < nw && (occ[u] & 0x7fffu) != r;
       const uint32_t lm = __ballot_sync(FULL, lost);
+#if RFR_INDEX_PRED
+      // the three stores of a lost record as predicated instructions: ~1 lane
+      // in 9 loses, so nearly every group has one, and a branch around them
+      // costs a divergence region per group
+      {
+        const uint32_t k = nl + __popc(lm & lt_mask);
+        const uint32_t a_lose = (uint32_t)__cvta_generic_to_shared(&lose[k < (uint32_t)kLose ? k : 0u]);
+        const uint32_t a_t2 = (uint32_t)__cvta_generic_to_shared(&S.t2[h1[u] >> 2]);
+        const uint32_t a_t1 = (uint32_t)__cvta_generic_to_shared(&S.t1[h1[u]]);
+        const uint16_t rv = (uint16_t)r, fv = (uint16_t)(occ[u] | 0x8000u);
+        asm volatile(
+            "{\n\t.reg .pred pl, pk;\n\t"
+            "setp.ne.u32 pl, %0, 0;\n\t"
+            "setp.lt.and.u32 pk, %1, %2, pl;\n\t"
+            "@pk st.shared.u16 [%3], %4;\n\t"
+            "@pl st.shared.u16 [%5], %4;\n\t"
+            "@pl st.shared.u16 [%6], %7;\n\t}"
+            ::"r"((uint32_t)lost), "r"(k), "r"((uint32_t)kLose), "r"(a_lose), "h"(rv), "r"(a_t2), "r"(a_t1),
+            "h"(fv)
+            : "memory");
+      }
+#else
       if (lost) {
         const uint32_t k = nl + __popc(lm & lt_mask);
         if (k < (uint32_t)kLose) lose[k] = (uint16_t)r;
         S.t2[h1[u] >> 2] = (uint16_t)r;
         S.t1[h1[u]] = (uint16_t)(occ[u] | 0x8000u);  // collision flag: B also probes levels 2-3
       }
+#endif
       nl += __popc(lm);
     }
   };
