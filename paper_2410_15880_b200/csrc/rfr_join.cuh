@@ -52,6 +52,9 @@
 #ifndef RFR_INDEX_PRED  // 1: the level-1 read-back stores a lost record with predicated stores
 #define RFR_INDEX_PRED 1
 #endif
+#ifndef RFR_APASS_PRED  // 1: the A run pass stores its records with predicated shared stores
+#define RFR_APASS_PRED 1
+#endif
 #ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
 #define RFR_JOIN_ONEHOME 1
 #endif
@@ -674,6 +677,25 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
         } else if (SIDE_A) {
           const uint32_t ne = __popc(em);
           if (!NOOVF && wfill + ne > (uint32_t)kPart) overflow = true;  // warp-uniform
+#if RFR_APASS_PRED
+          {  // the record's four stores, predicated (no divergence region per chunk)
+            const bool st = (NOOVF || !overflow) && e;
+            const uint32_t r = min(wid * kPart + wfill + lane, (uint32_t)kCapRec - 1u);  // em is a prefix
+            const uint32_t h1 = home_of(rel, K.sh - kL1Log, kL1Log);
+            asm volatile(
+                "{\n\t.reg .pred ps;\n\t"
+                "setp.ne.u32 ps, %0, 0;\n\t"
+                "@ps st.shared.u64 [%1], %2;\n\t"
+                "@ps st.shared.u32 [%3], %4;\n\t"
+                "@ps st.shared.u16 [%5], %6;\n\t"
+                "@ps st.shared.u16 [%7], %8;\n\t}"
+                ::"r"((uint32_t)st), "r"((uint32_t)__cvta_generic_to_shared(&S.recK[r])), "l"(sv),
+                "r"((uint32_t)__cvta_generic_to_shared(&S.recI[r])), "r"((i << aib) | j),
+                "r"((uint32_t)__cvta_generic_to_shared(&S.t1[h1])), "h"((uint16_t)r),
+                "r"((uint32_t)__cvta_generic_to_shared(&S.rh[r])), "h"((uint16_t)h1)
+                : "memory");
+          }
+#else
           if ((NOOVF || !overflow) && e) {
             const uint32_t r = wid * kPart + wfill + lane;  // em is a prefix
             S.recK[r] = sv;
@@ -682,6 +704,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
             S.t1[h1] = (uint16_t)r;
             S.rh[r] = (uint16_t)h1;
           }
+#endif
           if (NOOVF || !overflow) wfill += ne;
         } else {
           const int deep = probe_b_l1_fast(S, a, K, e, sv, !m, i, j, n_qprobe);
