@@ -55,6 +55,9 @@
 #ifndef RFR_APASS_PRED  // 1: the A run pass stores its records with predicated shared stores
 #define RFR_APASS_PRED 1
 #endif
+#ifndef RFR_JOIN_PREFETCH  // 1: each outer pulls its next bucket's run into L2
+#define RFR_JOIN_PREFETCH 1
+#endif
 #ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
 #define RFR_JOIN_ONEHOME 1
 #endif
@@ -732,7 +735,7 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
     // the next bucket's run of this outer starts at pos + mc: pull its lines
     // into L2 now (one 128-byte line per lane), so the next bucket's loads do
     // not all wait on HBM together right after the barrier
-    if ((uint32_t)lane < (uint32_t)(nch * 2)) {
+    if (RFR_JOIN_PREFETCH && (uint32_t)lane < (uint32_t)(nch * 2)) {
       const uint32_t q = pos + mc + (uint32_t)lane * 16u;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(kin + ((rot + q) & (Mi - 1))));
     }
