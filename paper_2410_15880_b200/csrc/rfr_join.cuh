@@ -811,6 +811,7 @@ __device__ __noinline__ void build_index_levels() {
   // ~256 +- 16 records: no warp pays a whole extra group for a few records)
   uint32_t e0 = 0;
   for (; e0 + 128 <= nw; e0 += 128) group(e0, std::integral_constant<int, 4>());
+#pragma unroll 1  // (unrolled, the tail ran as one 4-group body with bounds checks: ~127 instructions)
   for (; e0 < nw; e0 += 32) group(e0, std::integral_constant<int, 1>());
   if (nl > (uint32_t)kLose && lane == 0) S.ovf = 1;
   const int any2 = __syncthreads_or(nl > 0);
