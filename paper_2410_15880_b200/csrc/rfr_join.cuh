@@ -58,6 +58,9 @@
 #ifndef RFR_JOIN_PREFETCH  // 1: each outer pulls its next bucket's run into L2
 #define RFR_JOIN_PREFETCH 1
 #endif
+#ifndef RFR_JOIN_BHALO_WIDE  // 1: B halo records take the wide probe (no exclusion test in place)
+#define RFR_JOIN_BHALO_WIDE 1
+#endif
 #ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
 #define RFR_JOIN_ONEHOME 1
 #endif
@@ -540,7 +543,14 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
   const uint32_t h0 = (uint32_t)((rel - K.H) >> sh1);
   const uint32_t hn = (uint32_t)((rel + K.H) >> sh1) - h0;
   const uint32_t m1 = (1u << kL1Log) - 1u;
+#if RFR_JOIN_BHALO_WIDE
+  // B halo records (rel in [W, W + H): ~H/W of them, none in practice at
+  // factor-mode windows) go wide too, so the in-place check needs no
+  // halo x halo exclusion
+  const bool narrow = e && !bghost && hn == 0;
+#else
   const bool narrow = e && hn == 0;
+#endif
 #else
   const uint64_t lo_rel = rel >= K.H ? rel - K.H : 0ull;
   const uint32_t h0 = (uint32_t)(lo_rel >> sh1);
@@ -553,11 +563,19 @@ __device__ __forceinline__ int probe_b_l1_fast(const JoinSmem& S, const JoinArgs
   const uint64_t k0 = S.recK[r0];
   const bool o0 = e0 != kNone;
   n_qprobe += o0 ? 1u : 0u;
+#if RFR_JOIN_ONEHOME && RFR_JOIN_BHALO_WIDE
+  const bool hit0 = o0 && (k0 - s + K.hw <= K.width);
+#else
   const bool hit0 = o0 && !(bghost && (k0 - K.cW >= K.W)) && (k0 - s + K.hw <= K.width);
+#endif
   if (hit0) emit_match(a, r0, ib, jb);
   bool deep = o0 && (e0 >> 15);
 #if RFR_JOIN_ONEHOME
+#if RFR_JOIN_BHALO_WIDE
+  return (e && (hn != 0 || bghost)) ? 2 : (deep ? 1 : 0);
+#else
   return (e && hn != 0) ? 2 : (deep ? 1 : 0);
+#endif
 #endif
   // second home: only when the window crosses a level-1 home boundary (rare
   // for factor-mode windows), so it is taken warp-uniformly
