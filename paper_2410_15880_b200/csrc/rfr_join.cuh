@@ -61,6 +61,9 @@
 #ifndef RFR_JOIN_BHALO_WIDE  // 1: B halo records take the wide probe (no exclusion test in place)
 #define RFR_JOIN_BHALO_WIDE 1
 #endif
+#ifndef RFR_STAGE_PRED  // 1: a staged B record's three fields are written with predicated stores
+#define RFR_STAGE_PRED 1
+#endif
 #ifndef RFR_JOIN_ONEHOME  // 0: the run pass also checks a second level-1 home in place
 #define RFR_JOIN_ONEHOME 1
 #endif
@@ -731,12 +734,29 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
           const int deep = probe_b_l1_fast(S, a, K, e, sv, !m, i, j, n_qprobe);
           if (__any_sync(FULL, deep != 0)) {  // ~1 chunk in 5 has a flagged-slot record
             const uint32_t dm = __ballot_sync(FULL, deep != 0);
+#if RFR_STAGE_PRED
+            {
+              const uint32_t kk = min(nq + __popc(dm & lt_mask), (uint32_t)kStageB - 1u);
+              const uint32_t qj = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
+              asm volatile(
+                  "{\n\t.reg .pred pd;\n\t"
+                  "setp.ne.u32 pd, %0, 0;\n\t"
+                  "@pd st.shared.u64 [%1], %2;\n\t"
+                  "@pd st.shared.u32 [%3], %4;\n\t"
+                  "@pd st.shared.u16 [%5], %6;\n\t}"
+                  ::"r"((uint32_t)deep), "r"((uint32_t)__cvta_generic_to_shared(&S.qK[wid][kk])), "l"(sv),
+                  "r"((uint32_t)__cvta_generic_to_shared(&S.qJ[wid][kk])), "r"(qj),
+                  "r"((uint32_t)__cvta_generic_to_shared(&S.qB[wid][kk])), "h"((uint16_t)i)
+                  : "memory");
+            }
+#else
             if (deep) {
               const uint32_t kk = nq + __popc(dm & lt_mask);
               S.qK[wid][kk] = sv;
               S.qJ[wid][kk] = (m ? 0u : 0x80000000u) | (deep == 2 ? 0x40000000u : 0u) | j;
               S.qB[wid][kk] = (uint16_t)i;
             }
+#endif
             nq += __popc(dm);
             if (nq > (uint32_t)(kStageB - 32)) {  // keep room for one more chunk
               n_qprobe += process_staged(a, cW, nq);
