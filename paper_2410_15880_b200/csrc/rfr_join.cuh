@@ -61,6 +61,12 @@
 #ifndef RFR_JOIN_BHALO_WIDE  // 1: B halo records take the wide probe (no exclusion test in place)
 #define RFR_JOIN_BHALO_WIDE 1
 #endif
+#ifndef RFR_APASS_NOCLAMP  // 1: no slot clamp in the A run pass when its partition cannot overflow
+#define RFR_APASS_NOCLAMP 1
+#endif
+#ifndef RFR_INDEX_PRED2  // 1: the level-2 read-back also stores a lost record with predicated stores
+#define RFR_INDEX_PRED2 1
+#endif
 #ifndef RFR_STAGE_PRED  // 1: a staged B record's three fields are written with predicated stores
 #define RFR_STAGE_PRED 1
 #endif
@@ -704,7 +710,13 @@ __device__ __noinline__ PassSt run_pass(const JoinArgs& a, uint64_t cW, uint32_t
 #if RFR_APASS_PRED
           {  // the record's four stores, predicated (no divergence region per chunk)
             const bool st = (NOOVF || !overflow) && e;
+#if RFR_APASS_NOCLAMP
+            // NOOVF: wfill + 32 * chunks <= kPart, so the slot is always in the partition
+            const uint32_t r = NOOVF ? wid * kPart + wfill + lane
+                                     : min(wid * kPart + wfill + lane, (uint32_t)kCapRec - 1u);
+#else
             const uint32_t r = min(wid * kPart + wfill + lane, (uint32_t)kCapRec - 1u);  // em is a prefix
+#endif
             const uint32_t h1 = home_of(rel, K.sh - kL1Log, kL1Log);
             asm volatile(
                 "{\n\t.reg .pred ps;\n\t"
@@ -868,10 +880,24 @@ __device__ __noinline__ void build_index_levels() {
     }
     const uint32_t lm = __ballot_sync(FULL, lost);
     __syncwarp();
+#if RFR_INDEX_PRED2
+    {
+      const uint32_t a_l = (uint32_t)__cvta_generic_to_shared(&lose[min(nl2 + __popc(lm & lt_mask), (uint32_t)kLose - 1u)]);
+      const uint32_t a_3 = (uint32_t)__cvta_generic_to_shared(&S.t3[(h1 >> 4) & ((1u << kL3Log) - 1u)]);
+      asm volatile(
+          "{\n\t.reg .pred pq;\n\t"
+          "setp.ne.u32 pq, %0, 0;\n\t"
+          "@pq st.shared.u16 [%1], %2;\n\t"
+          "@pq st.shared.u16 [%3], %2;\n\t}"
+          ::"r"((uint32_t)lost), "r"(a_l), "h"((uint16_t)r), "r"(a_3)
+          : "memory");
+    }
+#else
     if (lost) {
       lose[nl2 + __popc(lm & lt_mask)] = (uint16_t)r;  // compact in place (target <= e)
       S.t3[h1 >> 4] = (uint16_t)r;
     }
+#endif
     nl2 += __popc(lm);
     __syncwarp();
   }
