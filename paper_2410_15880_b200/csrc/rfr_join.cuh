@@ -67,6 +67,9 @@
 #ifndef RFR_INDEX_PRED2  // 1: the level-2 read-back also stores a lost record with predicated stores
 #define RFR_INDEX_PRED2 1
 #endif
+#ifndef RFR_INDEX_G4MIN
+#define RFR_INDEX_G4MIN 96
+#endif
 #ifndef RFR_STAGE_PRED  // 1: a staged B record's three fields are written with predicated stores
 #define RFR_STAGE_PRED 1
 #endif
@@ -860,7 +863,9 @@ __device__ __noinline__ void build_index_levels() {
   // whole groups of 128 records, then the tail 32 at a time (partitions are
   // ~256 +- 16 records: no warp pays a whole extra group for a few records)
   uint32_t e0 = 0;
-  for (; e0 + 128 <= nw; e0 += 128) group(e0, std::integral_constant<int, 4>());
+  // (a four-group body also takes a tail of >= RFR_INDEX_G4MIN records: its
+  // lanes past nw are predicated off, cheaper than three or four tail passes)
+  for (; e0 + RFR_INDEX_G4MIN <= nw; e0 += 128) group(e0, std::integral_constant<int, 4>());
 #pragma unroll 1  // (unrolled, the tail ran as one 4-group body with bounds checks: ~127 instructions)
   for (; e0 < nw; e0 += 32) group(e0, std::integral_constant<int, 1>());
   if (nl > (uint32_t)kLose && lane == 0) S.ovf = 1;
